@@ -1,0 +1,249 @@
+"""Generate golden fixtures by running the REAL reference (simt_forge) here.
+
+Run in the build container only (the reference is not present on GPU boxes):
+
+    PYTHONDONTWRITEBYTECODE=1 PYTHONPATH=/root/reference/pkg/src \
+        python tests/golden/make_golden.py
+
+Writes (all small, committed):
+  bench_assets.json   the 11 bundled benchmark programs/harnesses, their 44
+                      seeded-bug variants and trigger traces (workload definitions)
+  ref_variants.json   execute_once verdict line for every trigger variant
+  ref_sampled.json    valid-domain + special-value inputs with diff readbacks
+  ref_batched.json    per-input records of the batched-round contract driven by
+                      the reference's own functions (schedule_next, mutate_testcase
+                      with a shared MutationSchedule, PhaseRunner, _absorb order)
+  ref_fuzzloop.json   reference fuzz_loop campaign outputs (findings, coverage,
+                      summary, corpus) for a few configs
+  ref_workloads.json  the same batched records for this repo's synthetic
+                      workloads (paper_2603_05725_b200/workloads)
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import struct
+import sys
+from pathlib import Path
+
+HERE = Path(__file__).resolve().parent
+REPO = HERE.parent.parent
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from simt_forge import bench as rb  # noqa: E402
+from simt_forge import campaign as rc  # noqa: E402
+from simt_forge.coverage import CoverageMap, build_report, new_edges_since, report_to_rec  # noqa: E402
+from simt_forge.device_memory import DeviceMemoryImage  # noqa: E402
+from simt_forge.mutation import (ArrayValue, FloatValue, IntValue, MutationSchedule,  # noqa: E402
+                                 TestCase, apply_trace, mutate_testcase,
+                                 sample_valid_testcase, serialize_testcase)
+from simt_forge.rng import Stream  # noqa: E402
+
+KEYBASE = 1 << 32
+
+
+def digest(tc) -> str:
+    return hashlib.sha256(serialize_testcase(tc, with_id=False).encode()).hexdigest()[:32]
+
+
+def edges_json(delta):
+    return {k: sorted([list(e) + [c] for e, c in v.items()]) for k, v in delta.edge_counts.items() if v}
+
+
+def assets():
+    out = {}
+    for b in rb.list_benchmarks():
+        ent = {"kernel": (b.root / "kernel.sir").read_text(),
+               "harness": (b.root / "harness.man").read_text(), "variants": {}}
+        for v in b.variants():
+            vd = {"trigger": v.trigger_path.read_text()}
+            if (v.root / "harness.man").exists():
+                vd["harness"] = (v.root / "harness.man").read_text()
+                vd["kernel"] = (v.root / "kernel.sir").read_text()
+            ent["variants"][v.bug_class] = vd
+        out[b.name] = ent
+    return out
+
+
+def variants():
+    out = {}
+    for b in rb.list_benchmarks():
+        for v in b.variants():
+            expected, ops = rb.load_trigger(v)
+            m = rc.load_harness(v.harness_path)
+            tc = rb.build_trigger_testcase(m, ops)
+            cov = CoverageMap.for_program(m.program)
+            res, _ = rc.execute_once(m, tc, coverage=cov)
+            out[f"{b.name}/{v.bug_class}"] = {
+                "expected": expected, "status": res.status, "retired": res.retired,
+                "report": res.report.to_line() if res.report else None, "edges": edges_json(cov)}
+    return out
+
+
+SPECIAL_F32 = [0x7FA00000, 0xFFC12345, 0x7F800000, 0xFF800000, 0x00000001, 0x80000000,
+               0x7F7FFFFF, 0x3E99999A, 0x4B800001, 0xCF000000, 0x4F000000, 0x7FFFFFFF]
+
+
+def sampled():
+    """Valid-domain inputs plus special-value arrays; readbacks pin f32/i32 bits."""
+    out = {}
+    for bi, b in enumerate(rb.list_benchmarks()):
+        m = b.load()
+        image = DeviceMemoryImage()
+        runner = rc.PhaseRunner(m, image, diff_readback=True)
+        runner.run_phase(rc.INIT, m.seed(1), iteration=0)
+        runner.mark_baseline()
+        snap = image.snapshot()
+        rng = Stream(99, bi)
+        recs = []
+        for i in range(24):
+            tc = sample_valid_testcase(m.argspecs, rng)
+            if i >= 12:  # sprinkle special bit patterns into float arrays/scalars
+                args = list(tc.args)
+                for k, v in enumerate(args):
+                    if isinstance(v, ArrayValue) and v.elem == "f32" and v.data:
+                        words = list(struct.unpack(f"<{len(v.data) // 4}I", v.data))
+                        for j in range(0, len(words), 3):
+                            words[j] = SPECIAL_F32[(i + j) % len(SPECIAL_F32)]
+                        args[k] = ArrayValue(struct.pack(f"<{len(words)}I", *words), v.elem,
+                                             v.extents, v.space)
+                    elif isinstance(v, FloatValue):
+                        args[k] = FloatValue(SPECIAL_F32[(i + k) % len(SPECIAL_F32)])
+                tc = TestCase(tuple(args), tc.rng_seed)
+            image.restore(snap)
+            runner.reset_to_baseline()
+            cov = CoverageMap.for_program(m.program)
+            res = runner.run_phase(rc.COMPUTE, tc, coverage=cov, iteration=i + 1)
+            recs.append({"testcase": serialize_testcase(tc, with_id=False), "status": res.status,
+                         "retired": res.retired,
+                         "report": res.report.to_line() if res.report else None,
+                         "readouts": {k: v.hex() for k, v in res.readouts.items()},
+                         "edges": edges_json(cov)})
+        out[b.name] = recs
+    return out
+
+
+def batched(m, *, master_seed, iterations, round_size, stop_bug_class=None,
+            stop_on_first_finding=False):
+    """Batched-round contract on the reference's own functions."""
+    specs = m.argspecs
+    seed_tc = m.seed(master_seed)
+    corpus = rc.Corpus()
+    corpus.add_seed(seed_tc)
+    findings = rc.FindingsLog()
+    gcov = CoverageMap.for_program(m.program)
+    sched = MutationSchedule()
+    image = DeviceMemoryImage(rng=Stream(master_seed, 2000))
+    runner = rc.PhaseRunner(m, image)
+    assert runner.run_phase(rc.INIT, seed_tc, iteration=0).status == "ok"
+    runner.mark_baseline()
+    snap = image.snapshot()
+    recs = []
+    round_corpus = None
+    stop = "iterations"
+    want = stop_bug_class
+    for it in range(1, iterations + 1):
+        if (it - 1) % round_size == 0:
+            round_corpus = rc.Corpus(list(corpus.entries))
+        image.restore(snap)
+        runner.reset_to_baseline()
+        if it == 1:
+            child, pidx = seed_tc, -1
+        else:
+            s = Stream(master_seed, KEYBASE + it)
+            parent = rc.schedule_next(round_corpus, s, it)
+            pidx = next(i for i, e in enumerate(round_corpus.entries) if e.tc is parent)
+            child = mutate_testcase(parent, specs, sched, s)
+        delta = gcov.fresh()
+        first = image._next_alloc_id
+        out = runner.run_phase(rc.COMPUTE, child, coverage=delta, iteration=it)
+        fresh = new_edges_since(delta, gcov)
+        gcov.merge_from(delta)
+        rec = {"it": it, "parent": pidx, "child": digest(child), "rng_seed": str(child.rng_seed),
+               "trace": [op.encode() for op in child.trace], "status": out.status,
+               "retired": out.retired, "allocs": image._next_alloc_id - first,
+               "edges": edges_json(delta), "admitted": False, "report": None}
+        halt = None
+        if out.report is not None:
+            out.report.iteration = it
+            rec["report"] = out.report.to_line()
+            findings.add(out.report)
+            if stop_on_first_finding:
+                halt = "first_finding"
+            elif want is not None and out.report.bug_class.value == want:
+                halt = f"bug_class:{want}"
+        elif fresh and it != 1:
+            corpus.admit(child, it)
+            rec["admitted"] = True
+        recs.append(rec)
+        if halt:
+            stop = halt
+            break
+    return {"records": recs, "findings": findings.render_text(),
+            "coverage": report_to_rec(build_report(gcov)),
+            "global_edges": edges_json(gcov), "stop": stop,
+            "corpus": [digest(e.tc) for e in corpus.entries]}
+
+
+BATCH_CFG = dict(master_seed=11, iterations=600, round_size=128)
+
+
+def batched_all():
+    return {b.name: batched(b.load(), **BATCH_CFG) for b in rb.list_benchmarks()}
+
+
+def fuzzloops(tmp):
+    out = {}
+    for name, seed, iters, kw in (("dot", 11, 400, {}), ("amax", 7, 300, {}),
+                                  ("rotm", 5, 300, {}),
+                                  ("axpy", 11, 3000, {"stop_bug_class": "SPATIAL_OOB"})):
+        m = rb.get_benchmark(name).load()
+        d = Path(tmp) / f"{name}-{seed}"
+        s = rc.fuzz_loop(m, rc.CampaignConfig(master_seed=seed, iterations=iters, out_dir=d, **kw))
+        out[f"{name}/{seed}/{iters}"] = {
+            "kw": kw, "summary": s.to_rec(), "findings": (d / "findings.txt").read_text(),
+            "coverage_rec": (d / "coverage.rec").read_text(),
+            "coverage_txt": (d / "coverage.txt").read_text(),
+            "corpus": sorted(p.name for p in (d / "corpus").iterdir()),
+            "crashes": sorted(p.name for p in (d / "crashes").iterdir()),
+        }
+    return out
+
+
+def workloads():
+    wdir = REPO / "paper_2603_05725_b200" / "workloads"
+    out = {}
+    for man in sorted(wdir.glob("*.man")):
+        m = rc.load_harness(man)
+        out[man.stem] = batched(m, master_seed=11, iterations=300, round_size=100)
+    return out
+
+
+def _dump(obj) -> str:
+    return json.dumps(obj, sort_keys=True, separators=(",", ":"))
+
+
+def main():
+    import tempfile
+    which = sys.argv[1:] or ["assets", "variants", "sampled", "batched", "fuzzloop", "workloads"]
+    if "assets" in which:
+        (HERE / "bench_assets.json").write_text(_dump(assets()))
+    if "variants" in which:
+        (HERE / "ref_variants.json").write_text(_dump(variants()))
+    if "sampled" in which:
+        (HERE / "ref_sampled.json").write_text(_dump(sampled()))
+    if "batched" in which:
+        data = {"config": BATCH_CFG, "keybase": KEYBASE, "runs": batched_all()}
+        (HERE / "ref_batched.json").write_text(_dump(data))
+    if "fuzzloop" in which:
+        with tempfile.TemporaryDirectory() as tmp:
+            (HERE / "ref_fuzzloop.json").write_text(_dump(fuzzloops(tmp)))
+    if "workloads" in which:
+        (HERE / "ref_workloads.json").write_text(_dump(workloads()))
+
+
+if __name__ == "__main__":
+    os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+    main()
