@@ -1,0 +1,102 @@
+/*
+ * sfg.h — C ABI of the B200 fuzzing inner loop (libsfg_b200.so).
+ *
+ * The reference (simt_forge, pure Python) has no FFI; its drop-in seams are
+ * Python calls.  Each entry point below replaces one of them for a whole
+ * batch ("round") of fuzz inputs, stream-ordered on the caller's CUDA stream:
+ *
+ *   sfg_plan + sfg_mutate + sfg_apply
+ *       <- schedule_next        pkg/src/simt_forge/campaign.py:593-603
+ *          mutate_testcase      pkg/src/simt_forge/mutation.py:499-518
+ *          PhaseRunner._materialize (payload bytes) campaign.py:440-450
+ *   sfg_execute
+ *       <- PhaseRunner.run_phase(COMPUTE)  campaign.py:483-561
+ *          executor.launch / _exec_one     executor.py:390-424, 210-377
+ *          sanitizer.check_access          sanitizer.py:145-187
+ *          CoverageMap.record_launch/edge  coverage.py:59-71
+ *   sfg_triage + sfg_commit
+ *       <- _absorb_iteration    campaign.py:825-846
+ *          new_edges_since / merge_from    coverage.py:85-113
+ *          FindingsLog.add      sanitizer.py:216-225
+ *   sfg_compact + sfg_regen
+ *       <- Corpus.admit         campaign.py:581-582
+ *   sfg_scan_u32 / sfg_scan_u64   order-dependent bookkeeping (rotation counts,
+ *          alloc ids, admission order) as exclusive prefix sums
+ *
+ * Conventions: every pointer argument except the host tables passed to
+ * sfg_program_create is a DEVICE pointer owned by the caller; `stream` is a
+ * cudaStream_t.  No call allocates or synchronizes.  Return 0 on success,
+ * nonzero on error with a message from sfg_last_error().  Record layouts are
+ * in paper_2603_05725_b200/csrc/sfg_types.h.
+ */
+#ifndef SFG_B200_H
+#define SFG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sfg_program sfg_program;
+
+typedef struct sfg_corpus_dev {  /* device corpus as of the round start */
+  const void* meta;              /* sfg_entry[n]          */
+  const void* vals;              /* sfg_val[n * n_args]   */
+  const void* data;              /* payload arena         */
+  int32_t n;
+  int32_t n_seeds;
+} sfg_corpus_dev;
+
+int sfg_abi_version(void);
+/* sizes/offsets of the record structs (layout self-check for host packers):
+ * 0 ins 1 kernel 2 hostop 3 binding 4 rec 5 val 6 op 7 child 8 entry 9 verdict
+ * 10 prog 11 offsetof(prog,kernels) 12 offsetof(prog,recent_weight) 13 offsetof(prog,copyout_arg) */
+size_t sfg_layout_probe(int which);
+const char* sfg_last_error(void);
+
+/* Upload the lowered harness (host tables; sizes in records). */
+int sfg_program_create(const void* prog, size_t prog_bytes, const void* ins, size_t n_ins,
+                       const void* hostops, size_t n_hostops, const void* binds, size_t n_binds,
+                       const void* base_recs, size_t n_recs, const void* const_blob,
+                       size_t const_bytes, const void* base_blob_dev, sfg_program** out);
+/* Replace the scalar header (campaign knobs: stop rule, budget, readback). */
+int sfg_program_update(sfg_program* p, const void* prog, size_t prog_bytes);
+void sfg_program_destroy(sfg_program* p);
+size_t sfg_execute_smem_bytes(const sfg_program* p);
+
+int sfg_plan(const sfg_program* p, const sfg_corpus_dev* c, int64_t it0, int n, int32_t* parent,
+             int8_t* picks, uint32_t* int_flags, void* stream);
+int sfg_mutate(const sfg_program* p, const sfg_corpus_dev* c, int64_t it0, int n,
+               const uint64_t* counts_prefix, const uint64_t* counts_base, void* children,
+               void* vals, void* stream);
+int sfg_apply(const sfg_program* p, const sfg_corpus_dev* c, int n, const void* children,
+              const void* vals, const uint64_t* work_base, uint8_t* work, void* stream);
+int sfg_regen(const sfg_program* p, const sfg_corpus_dev* c, int n_sel, const int32_t* sel,
+              const void* children, const void* vals, const uint64_t* dst_off, uint8_t* dst,
+              void* stream);
+int sfg_execute(const sfg_program* p, int n, const void* children, const void* vals,
+                const uint64_t* work_base, uint8_t* work, void* verdicts, uint32_t* edge_counts,
+                uint8_t* readouts, const uint64_t* readout_base, uint64_t* overlay, void* stream);
+int sfg_triage(const sfg_program* p, int n, const void* verdicts, const uint32_t* edge_counts,
+               const void* children, uint32_t* scalars, uint32_t* first_hit, uint64_t* edge_total,
+               uint32_t* key_first, uint64_t* key_count, uint32_t* entered, uint64_t* allocs,
+               const uint8_t* ghit, uint64_t* admit, void* stream);
+int sfg_commit(const sfg_program* p, const uint64_t* edge_total, uint8_t* ghit, void* stream);
+int sfg_child_bytes(const sfg_program* p, const void* vals, const uint64_t* admit, int n,
+                    uint64_t* bytes, void* stream);
+int sfg_compact(const sfg_program* p, const void* children, const void* vals, const uint64_t* admit,
+                const uint64_t* pos, const uint64_t* boff, int n, int n_corpus, uint64_t corpus_bytes,
+                void* cmeta, void* cvals, void* cchild, int32_t* sel, uint64_t* dst_off, void* stream);
+/* exclusive prefix sum of in[i*stride + col] into out[i*out_stride + col]; tmp holds
+ * ceil(n/2048) u64; *total (device) receives the sum when non-null */
+int sfg_scan_u32(const uint32_t* in, int64_t n, int stride, int col, uint64_t* out, int out_stride,
+                 uint64_t* tmp, uint64_t* total, void* stream);
+int sfg_scan_u64(const uint64_t* in, int64_t n, int stride, int col, uint64_t* out, int out_stride,
+                 uint64_t* tmp, uint64_t* total, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

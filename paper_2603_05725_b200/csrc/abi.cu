@@ -1,0 +1,268 @@
+// C ABI (include/sfg.h): host-side launch wrappers around the sm_100a kernels.
+// No torch types cross this boundary; the Python host passes raw device
+// pointers (torch tensors' data_ptr) and torch's current stream.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/sfg.h"
+#include "common.cuh"
+
+struct sfg_program {
+  sfg_prog P;
+  sfg_ins* ins;
+  sfg_hostop* hostops;
+  sfg_binding* binds;
+  sfg_rec* recs;
+  uint8_t* const_blob;
+  const uint8_t* base_blob;  // caller-owned device buffer
+  size_t smem;
+};
+
+static_assert(sizeof(sfg_ins) == 32, "sfg_ins layout");
+static_assert(sizeof(sfg_kernel) == 48, "sfg_kernel layout");
+static_assert(sizeof(sfg_hostop) == 72, "sfg_hostop layout");
+static_assert(sizeof(sfg_binding) == 16, "sfg_binding layout");
+static_assert(sizeof(sfg_rec) == 64, "sfg_rec layout");
+static_assert(sizeof(sfg_val) == 64, "sfg_val layout");
+static_assert(sizeof(sfg_op) == 32, "sfg_op layout");
+static_assert(sizeof(sfg_child) == 144, "sfg_child layout");
+static_assert(sizeof(sfg_entry) == 32, "sfg_entry layout");
+static_assert(sizeof(sfg_verdict) == 112, "sfg_verdict layout");
+static_assert(sizeof(sfg_prog) < 4096, "sfg_prog must fit the kernel parameter space");
+
+// one translation unit: the kernels are defined in these files
+#include "mutate.cu"
+#include "execute.cu"
+#include "triage.cu"
+
+static thread_local std::string g_err;
+
+static int fail(const char* where, cudaError_t e) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return 1;
+}
+
+#define SFG_CHECK_LAUNCH(name)                               \
+  do {                                                       \
+    cudaError_t _e = cudaGetLastError();                     \
+    if (_e != cudaSuccess) return fail(name, _e);            \
+  } while (0)
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+static inline CorpusView CV(const sfg_corpus_dev* c) {
+  return CorpusView{(const sfg_entry*)c->meta, (const sfg_val*)c->vals, (const uint8_t*)c->data, c->n, c->n_seeds};
+}
+
+template <typename T>
+static cudaError_t dupe(T** dst, const void* src, size_t count) {
+  *dst = nullptr;
+  if (count == 0) return cudaSuccess;
+  cudaError_t e = cudaMalloc((void**)dst, count * sizeof(T));
+  if (e != cudaSuccess) return e;
+  return cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+static size_t exec_smem(const sfg_prog& P) {
+  int maxregs = 1;
+  for (int k = 0; k < P.n_kernels; ++k) maxregs = P.kernels[k].regs > maxregs ? P.kernels[k].regs : maxregs;
+  const size_t ins = ((size_t)P.total_ins * sizeof(sfg_ins) + 15) & ~(size_t)15;
+  return ins + 4 * (size_t)32 * (maxregs * 24 + P.n_edges * 4);
+}
+
+template <typename T>
+static int scan_impl(const T* in, int64_t n, int stride, int col, uint64_t* out, int out_stride, uint64_t* tmp,
+                     uint64_t* total, void* stream, const char* name) {
+  const int64_t tiles = (n + 2047) / 2048;
+  if (n <= 0) {
+    if (total) cudaMemsetAsync(total, 0, sizeof(uint64_t), S(stream));
+    return 0;
+  }
+  sfg_scan_tiles<T><<<(unsigned)tiles, 256, 0, S(stream)>>>(in, n, stride, col, tmp);
+  SFG_CHECK_LAUNCH(name);
+  sfg_scan_tile_sums<<<1, 256, 0, S(stream)>>>(tmp, tiles, total);
+  SFG_CHECK_LAUNCH(name);
+  sfg_scan_apply<T><<<(unsigned)tiles, 256, 0, S(stream)>>>(in, n, stride, col, tmp, out, out_stride);
+  SFG_CHECK_LAUNCH(name);
+  return 0;
+}
+
+extern "C" {
+
+int sfg_abi_version(void) { return SFG_ABI_VERSION; }
+
+size_t sfg_layout_probe(int which) {
+  switch (which) {
+    case 0: return sizeof(sfg_ins);
+    case 1: return sizeof(sfg_kernel);
+    case 2: return sizeof(sfg_hostop);
+    case 3: return sizeof(sfg_binding);
+    case 4: return sizeof(sfg_rec);
+    case 5: return sizeof(sfg_val);
+    case 6: return sizeof(sfg_op);
+    case 7: return sizeof(sfg_child);
+    case 8: return sizeof(sfg_entry);
+    case 9: return sizeof(sfg_verdict);
+    case 10: return sizeof(sfg_prog);
+    case 11: return offsetof(sfg_prog, kernels);
+    case 12: return offsetof(sfg_prog, recent_weight);
+    case 13: return offsetof(sfg_prog, copyout_arg);
+    default: return 0;
+  }
+}
+const char* sfg_last_error(void) { return g_err.c_str(); }
+
+int sfg_program_create(const void* prog, size_t prog_bytes, const void* ins, size_t n_ins, const void* hostops,
+                       size_t n_hostops, const void* binds, size_t n_binds, const void* base_recs, size_t n_recs,
+                       const void* const_blob, size_t const_bytes, const void* base_blob_dev, sfg_program** out) {
+  if (prog_bytes != sizeof(sfg_prog)) {
+    g_err = "sfg_program_create: sfg_prog size mismatch (host " + std::to_string(prog_bytes) + ", device " +
+            std::to_string(sizeof(sfg_prog)) + ")";
+    return 1;
+  }
+  sfg_program* p = new sfg_program();
+  memcpy(&p->P, prog, sizeof(sfg_prog));
+  cudaError_t e;
+  if ((e = dupe(&p->ins, ins, n_ins)) != cudaSuccess ||
+      (e = dupe(&p->hostops, hostops, n_hostops)) != cudaSuccess ||
+      (e = dupe(&p->binds, binds, n_binds)) != cudaSuccess ||
+      (e = dupe(&p->recs, base_recs, n_recs)) != cudaSuccess ||
+      (e = dupe(&p->const_blob, const_blob, const_bytes)) != cudaSuccess) {
+    sfg_program_destroy(p);
+    return fail("sfg_program_create", e);
+  }
+  p->base_blob = (const uint8_t*)base_blob_dev;
+  p->smem = exec_smem(p->P);
+  e = cudaFuncSetAttribute(sfg_execute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem);
+  if (e != cudaSuccess) {
+    sfg_program_destroy(p);
+    return fail("sfg_program_create: execute smem", e);
+  }
+  *out = p;
+  return 0;
+}
+
+int sfg_program_update(sfg_program* p, const void* prog, size_t prog_bytes) {
+  if (prog_bytes != sizeof(sfg_prog)) {
+    g_err = "sfg_program_update: sfg_prog size mismatch";
+    return 1;
+  }
+  memcpy(&p->P, prog, sizeof(sfg_prog));
+  return 0;
+}
+
+void sfg_program_destroy(sfg_program* p) {
+  if (!p) return;
+  cudaFree(p->ins);
+  cudaFree(p->hostops);
+  cudaFree(p->binds);
+  cudaFree(p->recs);
+  cudaFree(p->const_blob);
+  delete p;
+}
+
+size_t sfg_execute_smem_bytes(const sfg_program* p) { return p->smem; }
+
+int sfg_plan(const sfg_program* p, const sfg_corpus_dev* c, int64_t it0, int n, int32_t* parent, int8_t* picks,
+             uint32_t* int_flags, void* stream) {
+  if (n <= 0) return 0;
+  sfg_plan_kernel<<<blocks_for(n, 128), 128, 0, S(stream)>>>(p->P, CV(c), it0, n, parent, picks, int_flags);
+  SFG_CHECK_LAUNCH("sfg_plan");
+  return 0;
+}
+
+int sfg_mutate(const sfg_program* p, const sfg_corpus_dev* c, int64_t it0, int n, const uint64_t* counts_prefix,
+               const uint64_t* counts_base, void* children, void* vals, void* stream) {
+  if (n <= 0) return 0;
+  sfg_mutate_kernel<<<blocks_for(n, 128), 128, 0, S(stream)>>>(p->P, CV(c), it0, n, counts_prefix, counts_base,
+                                                              (sfg_child*)children, (sfg_val*)vals);
+  SFG_CHECK_LAUNCH("sfg_mutate");
+  return 0;
+}
+
+int sfg_apply(const sfg_program* p, const sfg_corpus_dev* c, int n, const void* children, const void* vals,
+              const uint64_t* work_base, uint8_t* work, void* stream) {
+  if (n <= 0) return 0;
+  sfg_apply_kernel<<<blocks_for((int64_t)n * 32, 256), 256, 0, S(stream)>>>(
+      p->P, CV(c), n, (const sfg_child*)children, (const sfg_val*)vals, work_base, work);
+  SFG_CHECK_LAUNCH("sfg_apply");
+  return 0;
+}
+
+int sfg_regen(const sfg_program* p, const sfg_corpus_dev* c, int n_sel, const int32_t* sel, const void* children,
+              const void* vals, const uint64_t* dst_off, uint8_t* dst, void* stream) {
+  if (n_sel <= 0) return 0;
+  sfg_regen_kernel<<<blocks_for((int64_t)n_sel * 32, 256), 256, 0, S(stream)>>>(
+      p->P, CV(c), n_sel, sel, (const sfg_child*)children, (const sfg_val*)vals, dst_off, dst);
+  SFG_CHECK_LAUNCH("sfg_regen");
+  return 0;
+}
+
+int sfg_execute(const sfg_program* p, int n, const void* children, const void* vals, const uint64_t* work_base,
+                uint8_t* work, void* verdicts, uint32_t* edge_counts, uint8_t* readouts,
+                const uint64_t* readout_base, uint64_t* overlay, void* stream) {
+  if (n <= 0) return 0;
+  ExecView E{p->ins, p->hostops, p->binds, p->recs, p->base_blob, p->const_blob,
+                (const sfg_child*)children, (const sfg_val*)vals, work_base, work,
+                (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, overlay, n};
+  sfg_execute_kernel<<<blocks_for(n, 128), 128, p->smem, S(stream)>>>(p->P, E);
+  SFG_CHECK_LAUNCH("sfg_execute");
+  return 0;
+}
+
+int sfg_triage(const sfg_program* p, int n, const void* verdicts, const uint32_t* edge_counts, const void* children,
+               uint32_t* scalars, uint32_t* first_hit, uint64_t* edge_total, uint32_t* key_first,
+               uint64_t* key_count, uint32_t* entered, uint64_t* allocs, const uint8_t* ghit, uint64_t* admit,
+               void* stream) {
+  if (n <= 0) return 0;
+  const sfg_verdict* V = (const sfg_verdict*)verdicts;
+  sfg_stop_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(p->P, V, n, scalars);
+  SFG_CHECK_LAUNCH("sfg_triage/stop");
+  sfg_absorb_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(p->P, V, edge_counts, n, scalars, first_hit,
+                                                              (unsigned long long*)edge_total, key_first,
+                                                              (unsigned long long*)key_count, entered, allocs);
+  SFG_CHECK_LAUNCH("sfg_triage/absorb");
+  sfg_admit_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(p->P, V, edge_counts, (const sfg_child*)children, n,
+                                                             scalars, first_hit, ghit, admit);
+  SFG_CHECK_LAUNCH("sfg_triage/admit");
+  return 0;
+}
+
+int sfg_commit(const sfg_program* p, const uint64_t* edge_total, uint8_t* ghit, void* stream) {
+  sfg_commit_kernel<<<blocks_for(p->P.n_edges, 256), 256, 0, S(stream)>>>(
+      p->P.n_edges, (const unsigned long long*)edge_total, ghit);
+  SFG_CHECK_LAUNCH("sfg_commit");
+  return 0;
+}
+
+int sfg_child_bytes(const sfg_program* p, const void* vals, const uint64_t* admit, int n, uint64_t* bytes,
+                    void* stream) {
+  if (n <= 0) return 0;
+  sfg_child_bytes_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(p->P, (const sfg_val*)vals, admit, n, bytes);
+  SFG_CHECK_LAUNCH("sfg_child_bytes");
+  return 0;
+}
+
+int sfg_compact(const sfg_program* p, const void* children, const void* vals, const uint64_t* admit,
+                const uint64_t* pos, const uint64_t* boff, int n, int n_corpus, uint64_t corpus_bytes, void* cmeta,
+                void* cvals, void* cchild, int32_t* sel, uint64_t* dst_off, void* stream) {
+  if (n <= 0) return 0;
+  sfg_compact_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(
+      p->P, (const sfg_child*)children, (const sfg_val*)vals, admit, pos, boff, n, n_corpus, corpus_bytes,
+      (sfg_entry*)cmeta, (sfg_val*)cvals, (sfg_child*)cchild, sel, dst_off);
+  SFG_CHECK_LAUNCH("sfg_compact");
+  return 0;
+}
+
+int sfg_scan_u32(const uint32_t* in, int64_t n, int stride, int col, uint64_t* out, int out_stride, uint64_t* tmp,
+                 uint64_t* total, void* stream) {
+  return scan_impl(in, n, stride, col, out, out_stride, tmp, total, stream, "sfg_scan_u32");
+}
+
+int sfg_scan_u64(const uint64_t* in, int64_t n, int stride, int col, uint64_t* out, int out_stride, uint64_t* tmp,
+                 uint64_t* total, void* stream) {
+  return scan_impl(in, n, stride, col, out, out_stride, tmp, total, stream, "sfg_scan_u64");
+}
+
+}  // extern "C"

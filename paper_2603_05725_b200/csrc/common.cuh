@@ -1,0 +1,47 @@
+// Small device helpers shared by the kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sfg_types.h"
+
+#define SFG_DEV __device__ __forceinline__
+
+SFG_DEV float sfg_f(uint32_t b) { return __uint_as_float(b); }
+SFG_DEV uint32_t sfg_b(float f) { return __float_as_uint(f); }
+SFG_DEV bool sfg_isnan_bits(uint32_t b) { return (b & 0x7F800000u) == 0x7F800000u && (b & 0x007FFFFFu); }
+
+// binary32 add/sub/mul with the reference's host semantics: the value equals
+// IEEE RNE (double rounding of a single f32 op is innocuous), NaN results
+// follow x86-64 SSE as exhibited through ctypes.c_float (executor.py:42-44,
+// 319-330): first NaN operand wins and is quieted, invalid ops give 0xFFC00000.
+SFG_DEV uint32_t sfg_fop(int op, uint32_t a, uint32_t b) {
+  if (sfg_isnan_bits(a)) return a | 0x00400000u;
+  if (sfg_isnan_bits(b)) return b | 0x00400000u;
+  float r;
+  if (op == SFG_FADD) r = __fadd_rn(sfg_f(a), sfg_f(b));
+  else if (op == SFG_FSUB) r = __fsub_rn(sfg_f(a), sfg_f(b));
+  else r = __fmul_rn(sfg_f(a), sfg_f(b));
+  const uint32_t rb = sfg_b(r);
+  return sfg_isnan_bits(rb) ? 0xFFC00000u : rb;
+}
+
+SFG_DEV uint32_t sfg_quiet(uint32_t b) { return sfg_isnan_bits(b) ? (b | 0x00400000u) : b; }
+
+// read-only views of the device corpus (entries at round start)
+struct CorpusView {
+  const sfg_entry* meta;
+  const sfg_val* vals;
+  const uint8_t* data;
+  int32_t n;        // entries at round start
+  int32_t n_seeds;  // seeds form the prefix [0, n_seeds)
+};
+
+SFG_DEV uint64_t sfg_align16(uint64_t n) { return (n + 15ull) & ~15ull; }
+
+// bytes an input's work region reserves for array arg value v (materialized size,
+// reference PhaseRunner._materialize campaign.py:440-450)
+SFG_DEV uint64_t sfg_mat_size(const sfg_val& v) {
+  if (v.size_override != SFG_NO_OVERRIDE) return v.size_override > 0 ? (uint64_t)v.size_override : 0ull;
+  return v.nbytes;
+}

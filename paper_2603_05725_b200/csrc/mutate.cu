@@ -1,0 +1,435 @@
+// K1: batched type-aware mutation (schedule + op generation + payload apply).
+//
+// One fuzz input per thread for the draw-bound parts, one warp per input for
+// the byte-moving part.  Every draw comes from the input's own numpy-compatible
+// Philox stream (seed, keybase + it), so the child of input `it` is a pure
+// function of (corpus at round start, rotation counts prefix, it):
+//
+//   sfg_plan_kernel    schedule_next (campaign.py:593-603) + the op-count and
+//                      distinct-arg picks of mutate_testcase (mutation.py:502-511);
+//                      emits per-int-arg pick flags for the rotation-count scan
+//   sfg_mutate_kernel  re-derives the plan, then generate_op/apply_op per pick
+//                      (mutation.py:371-496, 258-365) at descriptor level,
+//                      child rng_seed = u64() (mutation.py:518), work layout
+//   sfg_apply_kernel   parent payload -> child work region with the data-level
+//                      ops applied (array_extreme/array_dim/array_elem), zero
+//                      fill up to the materialized size (campaign.py:440-450)
+//   sfg_regen_kernel   same payload rule, pristine bytes into a caller arena
+//                      (admitted children -> corpus, first crashes -> host)
+#include "common.cuh"
+#include "philox.cuh"
+
+namespace {
+
+constexpr double kTypeAware = 0.4;  // mutation.py:51
+__constant__ int32_t kIntDeltas[8] = {-16, -4, -2, -1, 1, 2, 4, 16};
+// f32 bit patterns of _ARITH_DELTAS (1.0, -1.0, 0.5, 2.0, 1024.0, 0.001), mutation.py:55
+__constant__ uint32_t kArith[6] = {0x3F800000u, 0xBF800000u, 0x3F000000u,
+                                   0x40000000u, 0x44800000u, 0x3A83126Fu};
+
+// Stream::weighted_choice over schedule_next's weights (rng.py:61-71).
+__device__ int pick_parent(SfgStream& s, const sfg_prog& P, const CorpusView& C, int64_t it) {
+  const double x0 = s.random();
+  // recent entries are a suffix of the non-seed entries (appended in admission order)
+  int lo = C.n_seeds, hi = C.n;
+  const int64_t cut = it - (int64_t)P.window;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (C.meta[mid].admitted_iteration >= cut) hi = mid; else lo = mid + 1;
+  }
+  const int64_t A = lo;             // weight-1 entries
+  const int64_t Rn = C.n - lo;      // recent entries, weight w
+  const double w = P.recent_weight;
+  const bool exact = (w == floor(w)) && w >= 0.0 && (double)A + w * (double)Rn < 9007199254740992.0;
+  if (exact) {
+    const double total = (double)A + w * (double)Rn;
+    const double x = x0 * total;
+    if (x < (double)A) return (int)floor(x);
+    if (Rn == 0 || w == 0.0) return C.n - 1;
+    int64_t j = (int64_t)floor((x - (double)A) / w);
+    if (j < 0) j = 0;
+    while (j > 0 && !(x >= (double)A + w * (double)j)) --j;
+    while (j < Rn && x >= (double)A + w * (double)(j + 1)) ++j;
+    return j >= Rn ? C.n - 1 : (int)(A + j);
+  }
+  double total = 0.0;
+  for (int i = 0; i < C.n; ++i) total += (i < A) ? 1.0 : w;
+  const double x = x0 * total;
+  double acc = 0.0;
+  for (int i = 0; i < C.n; ++i) {
+    acc += (i < A) ? 1.0 : w;
+    if (x < acc) return i;
+  }
+  return C.n - 1;
+}
+
+// mutate_testcase picks (mutation.py:502-511)
+__device__ int draw_picks(SfgStream& s, const sfg_prog& P, int8_t* picks) {
+  int cap = P.max_ops < P.n_mutable ? P.max_ops : P.n_mutable;
+  const int n_ops = 1 + s.geometric_small(0.5, cap - 1);
+  int8_t pool[SFG_MAX_ARGS];
+  int len = P.n_mutable;
+  for (int i = 0; i < len; ++i) pool[i] = P.mutable_args[i];
+  for (int k = 0; k < n_ops; ++k) {
+    const int idx = (int)s.integers(0, len);
+    picks[k] = pool[idx];
+    for (int i = idx; i + 1 < len; ++i) pool[i] = pool[i + 1];
+    --len;
+  }
+  return n_ops;
+}
+
+__device__ void gen_int_byte(SfgStream& s, sfg_op& op) {  // mutation.py:396-401
+  op.kind = SFG_M_INT_BYTE;
+  if (s.random() < 0.5) {
+    op.sub = 0;
+    op.byte = (uint8_t)s.integers(0, 4);
+    op.mask = (uint32_t)s.integers(1, 256);
+  } else {
+    op.sub = 1;
+    op.delta = kIntDeltas[s.integers(0, 8)];
+  }
+}
+
+__device__ void gen_float_op(SfgStream& s, sfg_op& op) {  // mutation.py:404-422
+  if (s.random() < kTypeAware) {
+    const int pick = (int)s.integers(0, 4);
+    if (pick == 0) {
+      op.kind = SFG_M_FLOAT_SIGN;
+    } else if (pick == 1) {
+      op.kind = SFG_M_FLOAT_EXPONENT;
+      op.sub = (uint8_t)s.integers(0, 3);  // ones, zeros, bit
+      if (op.sub == 2) op.byte = (uint8_t)s.integers(0, 8);
+    } else if (pick == 2) {
+      op.kind = SFG_M_FLOAT_MANTISSA;
+      op.mask = (uint32_t)s.integers(1, 1 << 23);
+    } else {
+      op.kind = SFG_M_FLOAT_ARITH;
+      op.mask = kArith[s.integers(0, 6)];
+    }
+    return;
+  }
+  op.kind = SFG_M_FLOAT_BYTE;
+  op.byte = (uint8_t)s.integers(0, 4);
+  op.mask = (uint32_t)s.integers(1, 256);
+}
+
+// _offset_palette (mutation.py:425-438): sorted distinct magnitudes in (0, 2*size], +m then -m
+__device__ int64_t offset_choice(SfgStream& s, const sfg_prog& P, uint64_t nbytes) {
+  const int64_t g = P.mut_granule, rz = P.mut_redzone;
+  const int64_t size = (int64_t)nbytes > g ? (int64_t)nbytes : g;
+  int64_t m[11] = {g, 2 * g, rz, rz + g, 2 * rz, 2 * rz + g, 2 * rz - g, size, size + 2 * rz,
+                   size + rz, 2 * size};
+  for (int i = 1; i < 11; ++i) {  // insertion sort
+    const int64_t v = m[i];
+    int j = i - 1;
+    while (j >= 0 && m[j] > v) { m[j + 1] = m[j]; --j; }
+    m[j + 1] = v;
+  }
+  int64_t u[11];
+  int n = 0;
+  for (int i = 0; i < 11; ++i)
+    if (m[i] > 0 && m[i] <= 2 * size && (n == 0 || u[n - 1] != m[i])) u[n++] = m[i];
+  if (n == 0) {
+    const int64_t k = s.integers(0, 2);
+    return k ? -g : g;
+  }
+  const int64_t k = s.integers(0, 2 * n);
+  return (k & 1) ? -u[k >> 1] : u[k >> 1];
+}
+
+__device__ void space_choice(SfgStream& s, uint8_t cur, sfg_op& op) {
+  uint8_t others[2];
+  int n = 0;
+  for (uint8_t sp = 0; sp < 3; ++sp)
+    if (sp != cur) others[n++] = sp;
+  op.sub = others[s.integers(0, 2)];
+}
+
+__device__ void gen_array_op(SfgStream& s, const sfg_prog& P, const sfg_val& v, sfg_op& op) {
+  if (v.count == 0) {  // mutation.py:443-450
+    const int pick = (int)s.integers(0, 3);
+    if (pick == 0) {
+      op.kind = SFG_M_ARRAY_DIM; op.sub = 1; op.mask = 4;
+    } else if (pick == 1) {
+      op.kind = SFG_M_PTR_SPACE; space_choice(s, v.space, op);
+    } else {
+      op.kind = SFG_M_PTR_OFFSET; op.delta = offset_choice(s, P, v.nbytes);
+    }
+    return;
+  }
+  if (s.random() < kTypeAware) {  // mutation.py:451-464
+    const int pick = (int)s.integers(0, 5);
+    if (pick == 0) {
+      op.kind = SFG_M_ARRAY_EXTREME; op.sub = (uint8_t)s.integers(0, 3);
+    } else if (pick == 1) {  // _gen_extents (mutation.py:477-487)
+      op.kind = SFG_M_ARRAY_DIM;
+      const uint32_t n = v.count;
+      if (n >= 2) {
+        const int nopt = (n % 2 == 0) ? 3 : 2;
+        const int k = (int)s.integers(0, nopt);
+        if (k == 0) { op.sub = 1; op.mask = n / 2; }
+        else if (k == 1) { op.sub = 2; op.mask = n; op.imask = 2; }
+        else { op.sub = 2; op.mask = 2; op.imask = n / 2; }
+      } else {
+        s.integers(0, 1);  // choice of a one-element list draws nothing (rng == 0)
+        op.sub = 1; op.mask = 2 * n + 2;
+      }
+    } else if (pick == 2) {
+      op.kind = SFG_M_ARRAY_EMPTY;
+    } else if (pick == 3) {
+      op.kind = SFG_M_PTR_SPACE; space_choice(s, v.space, op);
+    } else {
+      op.kind = SFG_M_PTR_OFFSET; op.delta = offset_choice(s, P, v.nbytes);
+    }
+    return;
+  }
+  op.kind = SFG_M_ARRAY_ELEM;  // mutation.py:465-474
+  op.index = (uint32_t)s.integers(0, (int64_t)v.count);
+  sfg_op in{};
+  if (v.elem == 1) {
+    do { in = sfg_op{}; gen_float_op(s, in); } while (in.kind == SFG_M_FLOAT_ARITH);
+  } else {
+    gen_int_byte(s, in);
+  }
+  op.inner = in.kind; op.isub = in.sub; op.ibyte = in.byte; op.imask = in.mask; op.delta = in.delta;
+}
+
+__device__ uint32_t int_bits_op(uint32_t v, uint8_t kind, uint8_t sub, uint8_t byte, uint32_t mask,
+                                int64_t delta) {
+  if (kind == SFG_M_INT_BOUNDARY) return sub == 0 ? 0u : (sub == 1 ? 0x7FFFFFFFu : 0x80000000u);
+  if (sub == 0) return v ^ ((mask & 0xFFu) << (8 * byte));      // flip
+  return (uint32_t)((int64_t)(int32_t)v + delta);                // add, wraps mod 2^32
+}
+
+__device__ uint32_t float_bits_op(uint32_t b, uint8_t kind, uint8_t sub, uint8_t byte, uint32_t mask) {
+  switch (kind) {                                                // mutation.py:281-306
+    case SFG_M_FLOAT_SIGN: return b ^ 0x80000000u;
+    case SFG_M_FLOAT_EXPONENT:
+      if (sub == 0) return b | 0x7F800000u;
+      if (sub == 1) return b & 0x807FFFFFu;
+      return b ^ (1u << (23 + byte));
+    case SFG_M_FLOAT_MANTISSA: return b ^ (mask & 0x007FFFFFu);
+    case SFG_M_FLOAT_BYTE: return b ^ ((mask & 0xFFu) << (8 * byte));
+    default: return sfg_fop(SFG_FADD, b, mask);                  // float_arith
+  }
+}
+
+// descriptor-level apply_op (mutation.py:258-357); payload bytes are done by emit_child
+__device__ void apply_desc(const sfg_prog& P, sfg_val& v, const sfg_op& op) {
+  switch (op.kind) {
+    case SFG_M_INT_BOUNDARY:
+    case SFG_M_INT_BYTE: v.bits = int_bits_op(v.bits, op.kind, op.sub, op.byte, op.mask, op.delta); break;
+    case SFG_M_FLOAT_SIGN: case SFG_M_FLOAT_EXPONENT: case SFG_M_FLOAT_MANTISSA:
+    case SFG_M_FLOAT_BYTE: case SFG_M_FLOAT_ARITH:
+      v.bits = float_bits_op(v.bits, op.kind, op.sub, op.byte, op.mask); break;
+    case SFG_M_ARRAY_EXTREME: v.nbytes = 4u * v.count; break;
+    case SFG_M_ARRAY_DIM:
+      v.ndim = op.sub; v.ext[0] = op.mask; v.ext[1] = op.sub == 2 ? op.imask : 0; v.ext[2] = v.ext[3] = 0;
+      v.count = op.sub == 2 ? op.mask * op.imask : op.mask;
+      v.nbytes = 4u * v.count;
+      break;
+    case SFG_M_ARRAY_EMPTY: v.ndim = 1; v.ext[0] = v.ext[1] = v.ext[2] = v.ext[3] = 0; v.count = 0; v.nbytes = 0; break;
+    case SFG_M_PTR_SPACE: v.space = op.sub; break;
+    case SFG_M_PTR_OFFSET: {
+      const int64_t lim = 2 * (int64_t)(v.nbytes > 4 ? v.nbytes : 4);
+      const int64_t d = op.delta < -lim ? -lim : (op.delta > lim ? lim : op.delta);
+      v.base_offset += d;
+      break;
+    }
+    default: break;  // ARRAY_ELEM: payload only
+  }
+}
+
+// byte p of the child's payload (p < child nbytes), given the parent's payload
+__device__ __forceinline__ uint8_t child_byte(const uint8_t* src, uint32_t src_n, const sfg_op* op,
+                                              uint8_t elem, uint64_t p) {
+  if (op != nullptr) {
+    if (op->kind == SFG_M_ARRAY_EXTREME) {
+      const uint32_t pat = elem == 1 ? (op->sub == 0 ? 0u : op->sub == 1 ? 0x7F7FFFFFu : 0xFF7FFFFFu)
+                                     : (op->sub == 0 ? 0u : op->sub == 1 ? 0x7FFFFFFFu : 0x80000000u);
+      return (uint8_t)(pat >> (8 * (p & 3)));
+    }
+    if (op->kind == SFG_M_ARRAY_ELEM && (p >> 2) == op->index) {
+      const uint64_t w0 = p & ~3ull;
+      uint32_t w = 0;
+      for (int k = 0; k < 4; ++k) w |= (uint32_t)(w0 + k < src_n ? src[w0 + k] : 0) << (8 * k);
+      if (elem == 1) w = float_bits_op(w, op->inner, op->isub, op->ibyte, op->imask);
+      else w = int_bits_op(w, op->inner, op->isub, op->ibyte, op->imask, op->delta);
+      return (uint8_t)(w >> (8 * (p & 3)));
+    }
+  }
+  return p < src_n ? src[p] : 0;
+}
+
+// Write bytes [0, limit) of a child array: payload bytes where p < child nbytes,
+// zeros beyond.  Lanes of a warp stride over 16-byte chunks; dst is 16-aligned.
+__device__ void emit_child(uint8_t* dst, uint64_t limit, const uint8_t* src, uint32_t src_n,
+                           const sfg_val& child, const sfg_op* op, int lane, int lanes) {
+  const bool extreme = op != nullptr && op->kind == SFG_M_ARRAY_EXTREME;
+  const uint64_t elem_chunk =
+      (op != nullptr && op->kind == SFG_M_ARRAY_ELEM) ? ((uint64_t)op->index * 4) >> 4 : ~0ull;
+  const uint64_t payload = child.nbytes;
+  const uint64_t copy_lim = payload < src_n ? payload : src_n;
+  const bool src_al = (((uintptr_t)src) & 15) == 0;
+  const uint64_t nchunks = (limit + 15) >> 4;
+  for (uint64_t c = lane; c < nchunks; c += lanes) {
+    const uint64_t p0 = c << 4;
+    if (!extreme && c != elem_chunk && src_al && p0 + 16 <= copy_lim && p0 + 16 <= limit) {
+      *reinterpret_cast<uint4*>(dst + p0) = __ldg(reinterpret_cast<const uint4*>(src + p0));
+      continue;
+    }
+    if (extreme && p0 + 16 <= payload && p0 + 16 <= limit) {
+      const uint32_t pat = child.elem == 1 ? (op->sub == 0 ? 0u : op->sub == 1 ? 0x7F7FFFFFu : 0xFF7FFFFFu)
+                                           : (op->sub == 0 ? 0u : op->sub == 1 ? 0x7FFFFFFFu : 0x80000000u);
+      *reinterpret_cast<uint4*>(dst + p0) = make_uint4(pat, pat, pat, pat);
+      continue;
+    }
+    if (p0 >= payload && p0 + 16 <= limit) {
+      *reinterpret_cast<uint4*>(dst + p0) = make_uint4(0, 0, 0, 0);
+      continue;
+    }
+    const uint64_t pe = p0 + 16 < limit ? p0 + 16 : limit;
+    for (uint64_t p = p0; p < pe; ++p) dst[p] = p < payload ? child_byte(src, src_n, op, child.elem, p) : 0;
+  }
+}
+
+}  // namespace
+
+extern "C" __global__ void sfg_plan_kernel(sfg_prog P, CorpusView C, int64_t it0, int n,
+                                           int32_t* parent_out, int8_t* picks_out, uint32_t* flags_out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t it = it0 + i;
+  int8_t picks[SFG_MAX_OPS] = {-1, -1, -1};
+  int parent = -1;
+  if (it != 1) {
+    SfgStream s;
+    s.init(P.master_seed, P.keybase + (uint64_t)it);
+    parent = pick_parent(s, P, C, it);
+    draw_picks(s, P, picks);
+  }
+  parent_out[i] = parent;
+  for (int k = 0; k < SFG_MAX_OPS; ++k) picks_out[i * SFG_MAX_OPS + k] = picks[k];
+  for (int c = 0; c < P.n_int_args; ++c) flags_out[(size_t)i * P.n_int_args + c] = 0;
+  for (int k = 0; k < SFG_MAX_OPS; ++k)
+    if (picks[k] >= 0 && P.int_slot[picks[k]] >= 0) flags_out[(size_t)i * P.n_int_args + P.int_slot[picks[k]]] = 1;
+}
+
+// counts_prefix[i][c]: rotation count of int column c seen by input i
+extern "C" __global__ void sfg_mutate_kernel(sfg_prog P, CorpusView C, int64_t it0, int n,
+                                             const uint64_t* counts_prefix, const uint64_t* counts_base,
+                                             sfg_child* child_out, sfg_val* vals_out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t it = it0 + i;
+  sfg_child ch;
+  memset(&ch, 0, sizeof(ch));
+  ch.it = it;
+  sfg_val* vout = vals_out + (size_t)i * P.n_args;
+  if (it == 1) {  // fuzz_loop evaluates the recorded seed first (campaign.py:739-740)
+    ch.parent = -1;
+    ch.rng_seed = C.meta[0].rng_seed;
+    for (int a = 0; a < P.n_args; ++a) vout[a] = C.vals[a];
+  } else {
+    SfgStream s;
+    s.init(P.master_seed, P.keybase + (uint64_t)it);
+    const int parent = pick_parent(s, P, C, it);
+    int8_t picks[SFG_MAX_OPS] = {-1, -1, -1};
+    const int n_ops = draw_picks(s, P, picks);
+    ch.parent = parent;
+    ch.n_ops = n_ops;
+    const sfg_val* pv = C.vals + (size_t)parent * P.n_args;
+    for (int a = 0; a < P.n_args; ++a) vout[a] = pv[a];
+    for (int k = 0; k < n_ops; ++k) {
+      const int a = picks[k];
+      sfg_op op;
+      memset(&op, 0, sizeof(op));
+      op.arg = (uint8_t)a;
+      sfg_val v = pv[a];
+      if (v.kind == SFG_V_I32) {  // MutationSchedule.next_int_op (mutation.py:378-386)
+        const int c = P.int_slot[a];
+        const uint64_t cnt = counts_base[c] + counts_prefix[(size_t)i * P.n_int_args + c];
+        if (cnt < 3) {
+          op.kind = SFG_M_INT_BOUNDARY;
+          op.sub = (uint8_t)cnt;
+        } else if (s.random() < kTypeAware) {
+          op.kind = SFG_M_INT_BOUNDARY;
+          op.sub = (uint8_t)s.integers(0, 3);
+        } else {
+          gen_int_byte(s, op);
+        }
+      } else if (v.kind == SFG_V_F32) {
+        gen_float_op(s, op);
+      } else {
+        gen_array_op(s, P, v, op);
+      }
+      apply_desc(P, v, op);
+      vout[a] = v;
+      ch.ops[k] = op;
+    }
+    ch.rng_seed = s.next64();
+  }
+  // work layout: array regions (materialized size, 16-aligned) then COMPUTE named allocs
+  uint64_t off = 0;
+  for (int a = 0; a < P.n_args; ++a) {
+    if (vout[a].kind != SFG_V_ARR) continue;
+    vout[a].data_off = off;
+    off += sfg_align16(sfg_mat_size(vout[a]));
+  }
+  ch.work_bytes = off + (uint64_t)P.named_work_bytes;
+  uint64_t rb = 0;
+  if (P.diff_readback) {
+    rb = (uint64_t)P.readout_bytes_fixed;
+    for (int k = 0; k < P.n_copyout_arg; ++k) rb += sfg_align16(vout[P.copyout_arg[k]].nbytes);
+  }
+  ch.readout_bytes = rb;
+  child_out[i] = ch;
+}
+
+// warp per input: parent payloads -> child work region (materialized contents)
+extern "C" __global__ void sfg_apply_kernel(sfg_prog P, CorpusView C, int n, const sfg_child* children,
+                                            const sfg_val* vals, const uint64_t* work_base, uint8_t* work) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = warp; i < n; i += nwarps) {
+    const sfg_child& ch = children[i];
+    const int parent = ch.parent < 0 ? 0 : ch.parent;
+    const sfg_val* pv = C.vals + (size_t)parent * P.n_args;
+    const sfg_val* cv = vals + (size_t)i * P.n_args;
+    uint8_t* base = work + work_base[i];
+    for (int a = 0; a < P.n_args; ++a) {
+      if (cv[a].kind != SFG_V_ARR) continue;
+      const sfg_op* op = nullptr;
+      for (int k = 0; k < ch.n_ops; ++k)
+        if (ch.ops[k].arg == a) op = &ch.ops[k];
+      emit_child(base + cv[a].data_off, sfg_mat_size(cv[a]), C.data + pv[a].data_off, pv[a].nbytes, cv[a],
+                 op, lane, 32);
+    }
+  }
+}
+
+// warp per selected input: pristine child payloads into dst (dst_off per (selected, arg))
+extern "C" __global__ void sfg_regen_kernel(sfg_prog P, CorpusView C, int n_sel, const int32_t* sel,
+                                            const sfg_child* children, const sfg_val* vals,
+                                            const uint64_t* dst_off, uint8_t* dst) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int j = warp; j < n_sel; j += nwarps) {
+    const int i = sel[j];
+    const sfg_child& ch = children[i];
+    const int parent = ch.parent < 0 ? 0 : ch.parent;
+    const sfg_val* pv = C.vals + (size_t)parent * P.n_args;
+    const sfg_val* cv = vals + (size_t)i * P.n_args;
+    for (int a = 0; a < P.n_args; ++a) {
+      if (cv[a].kind != SFG_V_ARR) continue;
+      const sfg_op* op = nullptr;
+      for (int k = 0; k < ch.n_ops; ++k)
+        if (ch.ops[k].arg == a) op = &ch.ops[k];
+      emit_child(dst + dst_off[(size_t)j * P.n_args + a], cv[a].nbytes, C.data + pv[a].data_off,
+                 pv[a].nbytes, cv[a], op, lane, 32);
+    }
+  }
+}

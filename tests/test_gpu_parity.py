@@ -1,0 +1,90 @@
+"""GPU parity: the sm_100a path (through the C ABI) vs the reference's golden
+vectors and the CPU oracle, bit-exact."""
+
+import hashlib
+
+import pytest
+
+from conftest import bench_manifest, bench_names, golden, trigger_ops
+from paper_2603_05725_b200.coverage import build_report, report_to_rec
+from paper_2603_05725_b200.testcase import parse_testcase, serialize_testcase
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = ("spatial_oob", "temporal_uaf", "space_mismatch", "provenance_escape")
+
+
+def _digest(tc):
+    return hashlib.sha256(serialize_testcase(tc, with_id=False).encode()).hexdigest()[:32]
+
+
+@pytest.fixture(scope="module")
+def engine_cls(cuda_ok):
+    from paper_2603_05725_b200.engine import DeviceCampaign
+    return DeviceCampaign
+
+
+@pytest.mark.parametrize("name", bench_names())
+def test_trigger_variants(engine_cls, name):
+    from oracle.mutate import apply_trace
+    ref = golden("ref_variants.json")
+    for variant in VARIANTS:
+        m = bench_manifest(name, variant)
+        _, ops = trigger_ops(name, variant)
+        tc = apply_trace(m.seed(0), ops)
+        dc = engine_cls(m, master_seed=1)
+        (out,) = dc.execute_testcases([tc])
+        want = ref[f"{name}/{variant}"]
+        assert out["status"] == want["status"]
+        assert out["report"].to_line() == want["report"], variant
+        assert out["retired"] == want["retired"]
+        assert out["edges"] == want["edges"]
+        dc.close()
+
+
+@pytest.mark.parametrize("name", bench_names())
+def test_sampled_inputs_readouts(engine_cls, name):
+    m = bench_manifest(name)
+    recs = golden("ref_sampled.json")[name]
+    dc = engine_cls(m, master_seed=1, diff_readback=True)
+    tcs = [parse_testcase(r["testcase"])[0] for r in recs]
+    outs = dc.execute_testcases(tcs, iteration0=1)
+    for i, (out, r) in enumerate(zip(outs, recs)):
+        assert out["status"] == r["status"], i
+        assert (out["report"].to_line() if out["report"] else None) == r["report"], i
+        assert {k: v.hex() for k, v in out["readouts"].items()} == r["readouts"], i
+        assert out["retired"] == r["retired"], i
+        assert out["edges"] == r["edges"], i
+    dc.close()
+
+
+@pytest.mark.parametrize("name", bench_names())
+def test_batched_rounds_match_reference(engine_cls, name):
+    data = golden("ref_batched.json")
+    cfg = data["config"]
+    ref = data["runs"][name]
+    m = bench_manifest(name)
+    dc = engine_cls(m, master_seed=cfg["master_seed"])
+    got = []
+    it = 1
+    while it <= cfg["iterations"]:
+        n = min(cfg["round_size"], cfg["iterations"] - it + 1)
+        res = dc.run_round(it, n)
+        got += dc.round_records(res)
+        it += n
+    assert len(got) == len(ref["records"])
+    for g, w in zip(got, ref["records"]):
+        assert g["parent"] == w["parent"], g["it"]
+        assert [op.encode() for op in g["child"].trace] == w["trace"], g["it"]
+        assert str(g["child"].rng_seed) == w["rng_seed"], g["it"]
+        assert _digest(g["child"]) == w["child"], g["it"]
+        assert g["status"] == w["status"], g["it"]
+        assert g["report"] == w["report"], g["it"]
+        assert g["retired"] == w["retired"], g["it"]
+        assert g["allocs"] == w["allocs"], g["it"]
+        assert g["edges"] == w["edges"], g["it"]
+        assert g["admitted"] == w["admitted"], g["it"]
+    assert dc.findings.render_text() == ref["findings"]
+    assert report_to_rec(build_report(dc.coverage_map())) == ref["coverage"]
+    assert [_digest(e[0]) for e in dc.host_entries] == ref["corpus"]
+    dc.close()

@@ -1,0 +1,136 @@
+"""CPU tests: host front end digests, lowering of every bundled harness, the
+C-ABI library's exports and record layouts (no GPU needed)."""
+
+import ctypes
+import re
+
+import pytest
+
+from conftest import bench_manifest, bench_names, golden
+from paper_2603_05725_b200 import _native
+from paper_2603_05725_b200 import lowering as lw
+from paper_2603_05725_b200.baseline import MemConfig, build_baseline, record_table
+from paper_2603_05725_b200.engine import MutationConfig
+from paper_2603_05725_b200.testcase import argspec_digest
+
+VARIANTS = ("spatial_oob", "temporal_uaf", "space_mismatch", "provenance_escape")
+
+
+@pytest.mark.parametrize("key", sorted(golden("ref_fuzzloop.json")))
+def test_digests_match_reference(key):
+    name = key.split("/")[0]
+    m = bench_manifest(name)
+    summ = golden("ref_fuzzloop.json")[key]["summary"]
+    prog, man, arg = re.search(r"program=(\w+) manifest=(\w+) argspec=(\w+)", summ).groups()
+    assert m.program_digest == prog
+    assert m.digest == man
+    assert argspec_digest(m.argspecs) == arg
+
+
+@pytest.mark.parametrize("name", bench_names())
+def test_every_harness_lowers(name):
+    for variant in (None,) + VARIANTS:
+        m = bench_manifest(name, variant)
+        base = build_baseline(m, m.seed(11), MemConfig())
+        low = lw.Lowered(m, base, mem=MemConfig(), mutation=MutationConfig(), master_seed=11, budget=10**6,
+                         window=256, recent_weight=4.0)
+        recs = record_table(base, low.labels)
+        assert len(low.ins) == sum(len(k.instructions) for k in m.program.kernels.values())
+        assert low.n_edges == sum(len(k.edges) for k in m.program.kernels.values())
+        assert len(recs) >= 2
+        # INIT lays out ws then lut exactly like the reference allocator
+        assert base.named["ws"][0] == 0x10000020
+        assert base.named["lut"][0] == 0x10800060
+        for key in range(0, low.n_keys, max(1, low.n_keys // 50)):
+            low.key_parts(key)
+
+
+def test_library_exports_and_layouts():
+    lib = _native.lib()
+    for sym in _native.EXPORTS:
+        assert hasattr(lib, sym), sym
+    assert lib.sfg_abi_version() == 1
+    sizes = [lib.sfg_layout_probe(i) for i in range(14)]
+    want = [lw.INS.itemsize, lw.KERNEL.itemsize, lw.HOSTOP.itemsize, lw.BINDING.itemsize, lw.REC.itemsize,
+            lw.VAL.itemsize, lw.OP.itemsize, lw.CHILD.itemsize, lw.ENTRY.itemsize, lw.VERDICT.itemsize,
+            lw.PROG.itemsize, lw.PROG.fields["kernels"][1], lw.PROG.fields["recent_weight"][1],
+            lw.PROG.fields["copyout_arg"][1]]
+    assert sizes == want
+
+
+def test_header_declares_every_export():
+    text = (_native.HEADER).read_text()
+    for sym in _native.EXPORTS:
+        assert re.search(rf"\b{sym}\s*\(", text), sym
+
+
+def test_op_codec_roundtrip_against_oracle_text():
+    """decode_op reproduces MutationOp.encode() text for ops the oracle generates."""
+    import numpy as np
+    from oracle.loop import batched_loop
+    m = bench_manifest("rotm")
+    res = batched_loop(m, master_seed=5, iterations=300, round_size=100)
+    seen = 0
+    for r in res.records[1:]:
+        for op in r["child"].trace:
+            o = np.zeros(1, lw.OP)[0]
+            _encode_for_test(o, op)
+            assert lw.decode_op(o).encode() == op.encode()
+            seen += 1
+    assert seen > 300
+
+
+def _encode_for_test(o, op):
+    """Test-side encoder (device ops are produced by the kernel; this mirrors the layout)."""
+    kind = lw.M_INDEX[op.kind]
+    o["kind"], o["arg"] = kind, op.arg
+    p = dict(op.params)
+    sub = {"zero": 0, "max": 1, "min": 2, "ones": 0, "zeros": 1, "bit": 2, "flip": 0, "add": 1,
+           "global": 0, "shared": 1, "local": 2}
+    if op.kind in ("int_boundary",):
+        o["sub"] = sub[p["which"]]
+    elif op.kind == "int_byte":
+        o["sub"] = sub[p["mode"]]
+        if p["mode"] == "flip":
+            o["byte"], o["mask"] = int(p["byte"]), int(p["mask"])
+        else:
+            o["delta"] = int(p["delta"])
+    elif op.kind == "float_exponent":
+        o["sub"] = sub[p["pattern"]]
+        if p["pattern"] == "bit":
+            o["byte"] = int(p["bit"])
+    elif op.kind in ("float_mantissa",):
+        o["mask"] = int(p["mask"], 0)
+    elif op.kind == "float_byte":
+        o["byte"], o["mask"] = int(p["byte"]), int(p["mask"])
+    elif op.kind == "float_arith":
+        o["mask"] = int(p["delta_bits"], 0)
+    elif op.kind == "array_extreme":
+        o["sub"] = sub[p["pattern"]]
+    elif op.kind == "array_dim":
+        e = [int(x) for x in p["extents"].split("x")]
+        o["sub"], o["mask"] = len(e), e[0]
+        if len(e) == 2:
+            o["imask"] = e[1]
+    elif op.kind == "ptr_space":
+        o["sub"] = sub[p["target"]]
+    elif op.kind == "ptr_offset":
+        o["delta"] = int(p["delta"])
+    elif op.kind == "array_elem":
+        o["index"] = int(p["index"])
+        inner = p["inner"]
+        o["inner"] = lw.M_INDEX[inner]
+        if inner == "int_byte":
+            o["isub"] = sub[p["inner_mode"]]
+            if p["inner_mode"] == "flip":
+                o["ibyte"], o["imask"] = int(p["inner_byte"]), int(p["inner_mask"])
+            else:
+                o["delta"] = int(p["inner_delta"])
+        elif inner == "float_exponent":
+            o["isub"] = sub[p["inner_pattern"]]
+            if p["inner_pattern"] == "bit":
+                o["ibyte"] = int(p["inner_bit"])
+        elif inner == "float_mantissa":
+            o["imask"] = int(p["inner_mask"], 0)
+        elif inner == "float_byte":
+            o["ibyte"], o["imask"] = int(p["inner_byte"]), int(p["inner_mask"])
