@@ -48,7 +48,7 @@ def workload_manifest(stem: str):
     return load_harness(REPO / "paper_2603_05725_b200" / "workloads" / f"{stem}.man")
 
 
-@pytest.fixture
+@pytest.fixture(scope="session")
 def cuda_ok():
     import torch
     if not torch.cuda.is_available():
