@@ -1,0 +1,270 @@
+#!/usr/bin/env python
+"""Benchmark: instrumented fuzz execs/s of the B200 fuzzing inner loop.
+
+Metric (BASELINE.json): fuzz execs/sec, one exec = parent pick + type-aware
+mutation + one COMPUTE phase (execute, sanitize, cover) + triage, i.e. the
+reference's ``compute_runs`` unit (campaign.py:648-652, 748).
+
+Workload: C2 of SURVEY.md §8(d) — the tiled matmul target with
+stride/size-argument OOB bugs (paper_2603_05725_b200/workloads/matmul.man),
+master_seed 11, batched rounds of R inputs.  One step = one round.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--round R] [--impl ours|reference]
+
+--impl reference times the CPU port of the reference loop (oracle/, test
+infrastructure; the Python reference itself cannot travel to the GPU box) on
+all host cores, same metric and workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+METRIC = "instrumented fuzz execs/sec"
+UNIT = "execs/s"
+WORKLOAD = "C2 tiled matmul 8x8x8, grid 2 x block 4, stride/size OOB (workloads/matmul.man), seed 11"
+
+
+# ---------------------------------------------------------------- CPU reference arm
+
+
+def _cpu_worker(args):
+    workload, seed, seconds = args
+    from oracle.loop import batched_loop
+    from paper_2603_05725_b200.workloads import load
+    m = load(workload)
+    done = 0
+    t0 = time.perf_counter()
+    chunk = 64
+    while time.perf_counter() - t0 < seconds:
+        batched_loop(m, master_seed=seed, iterations=chunk, round_size=chunk, keep_records=False)
+        done += chunk
+    return done, time.perf_counter() - t0
+
+
+def cpu_rate(workload: str, seconds: float, procs: int | None = None):
+    import multiprocessing as mp
+    procs = procs or os.cpu_count() or 1
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(procs) as pool:
+        out = pool.map(_cpu_worker, [(workload, 11 + i, seconds) for i in range(procs)])
+    wall = time.perf_counter() - t0
+    execs = sum(d for d, _ in out)
+    return execs / wall, execs, wall, procs
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    per_step = []
+    total_execs = 0
+    procs = os.cpu_count() or 1
+    for s in range(a.warmup + a.steps):
+        rate, execs, wall, procs = cpu_rate(a.workload, a.ref_seconds, procs)
+        if s >= a.warmup:
+            per_step.append(wall)
+            total_execs += execs
+    value = total_execs / sum(per_step)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1000 * statistics.mean(per_step),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "i32/f32",
+            "data": "synthetic", "config": {"workload": WORKLOAD, "sample": f"{a.ref_seconds}s per process per step"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
+                             "sample": f"oracle batched loop, {procs} processes x {a.ref_seconds}s per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------- GPU arm
+
+
+class ClockSampler:
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 6:
+                    self.rows.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+    from paper_2603_05725_b200.engine import DeviceCampaign
+    from paper_2603_05725_b200.workloads import load
+
+    m = load(a.workload)
+    R = a.round
+    dc = DeviceCampaign(m, master_seed=11 + rank)  # weak scaling: one campaign shard per GPU
+    dc.timing = True
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    it = 1
+
+    def step():
+        nonlocal it
+        dc.run_round(it, R)
+        it += R
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = []
+    k3 = []
+    launches0 = dc.launches
+    with ClockSampler(local) as clk:
+        for _ in range(a.steps):
+            flush.zero_()  # L2 (126 MB) flushed between timed steps, outside the timed region
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            step()
+            e.record()
+            ev.append((s, e))
+            k3.append(dc.last_exec_events)
+        torch.cuda.synchronize()
+    launches = dc.launches - launches0
+    ms = [s.elapsed_time(e) for s, e in ev]
+    k3_ms = [s.elapsed_time(e) for s, e in k3]
+    t_local = sum(ms) / 1000.0
+    t = torch.tensor([t_local], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max = float(t.item())
+    value = world * a.steps * R / t_max
+
+    # ---- end to end through the public API with host buffers
+    e2e = run_e2e(a, dc, torch, R)
+
+    # ---- dominant kernel roofline (execute: issue-bound interpreter; HBM figure reported honestly)
+    peaks = json.loads((REPO / "MEASURED_PEAKS.json").read_text()) if (REPO / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    k3_avg_s = statistics.mean(k3_ms) / 1000.0
+    bytes_exec = dc.algorithmic_exec_bytes()
+    achieved = bytes_exec * R / k3_avg_s / 1e9
+    retired = dc.last_retired_mean
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+            "traffic": None, "kernel": "sfg_execute_kernel", "bytes_per_exec": bytes_exec,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
+            "note": "execute is SM-issue bound (interpreter); see issue_roofline"}
+    sm_mhz = clk.summary().get("sm_mhz") or 1965.0
+    issue = {"sim_instr_per_s": retired * R / k3_avg_s, "sim_instr_per_exec": retired,
+             "k3_ms_per_round": statistics.mean(k3_ms),
+             "k3_share_of_step": statistics.mean(k3_ms) / statistics.mean(ms),
+             "lane_instr_peak_per_s": 148 * 4 * 32 * sm_mhz * 1e6}
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not a.no_cpu:
+            rate, execs, wall, procs = cpu_rate(a.workload, a.cpu_seconds)
+            cpu = {"value": rate, "unit": UNIT, "cores": procs, "kind": "port",
+                   "sample": f"oracle batched loop on {a.workload}, {procs} processes x {a.cpu_seconds}s, {execs} execs"}
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": t_max * 1000 / a.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "i32/f32", "data": "synthetic",
+                "config": {"workload": WORKLOAD, "round_size": R, "execs_per_step": world * R,
+                           "l2": "flushed between steps (256 MiB write, untimed)", "parallelism": f"shard{world}"},
+                "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(), "roofline": roof,
+                "issue_roofline": issue, "cpu_baseline": cpu}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(a, dc, torch, R):
+    """Same metric through the public round API with host buffers: every step
+    re-uploads the corpus from pinned host memory and reads the round's verdict
+    records back to pinned host memory."""
+    host = dc.corpus_host_pinned()
+    ver = torch.empty(R * 112, dtype=torch.uint8, pin_memory=True)
+    h2d = sum(t.numel() for t in host)
+    d2h = ver.numel()
+    it = 10_000_000_000  # a fresh id range so e2e inputs differ from the timed ones
+    ev = []
+    for k in range(a.warmup + a.steps):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        dc.load_corpus_from_host(host)
+        dc.run_round(it, R)
+        ver.copy_(dc.r_verdicts[:R * 112], non_blocking=True)
+        e.record()
+        it += R
+        if k >= a.warmup:
+            ev.append((s, e))
+    torch.cuda.synchronize()
+    t = sum(s.elapsed_time(e) for s, e in ev) / 1000.0
+    return {"value": a.steps * R / t, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=16)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--round", type=int, default=65536)
+    p.add_argument("--workload", default="matmul")
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--cpu-seconds", type=float, default=15.0)
+    p.add_argument("--ref-seconds", type=float, default=10.0)
+    p.add_argument("--no-cpu", action="store_true")
+    a = p.parse_args()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

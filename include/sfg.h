@@ -89,12 +89,12 @@ int sfg_child_bytes(const sfg_program* p, const void* vals, const uint64_t* admi
 int sfg_compact(const sfg_program* p, const void* children, const void* vals, const uint64_t* admit,
                 const uint64_t* pos, const uint64_t* boff, int n, int n_corpus, uint64_t corpus_bytes,
                 void* cmeta, void* cvals, void* cchild, int32_t* sel, uint64_t* dst_off, void* stream);
-/* exclusive prefix sum of in[i*stride + col] into out[i*out_stride + col]; tmp holds
+/* exclusive prefix sum of in[i*stride + col] into out[i*out_stride + out_col]; tmp holds
  * ceil(n/2048) u64; *total (device) receives the sum when non-null */
 int sfg_scan_u32(const uint32_t* in, int64_t n, int stride, int col, uint64_t* out, int out_stride,
-                 uint64_t* tmp, uint64_t* total, void* stream);
+                 int out_col, uint64_t* tmp, uint64_t* total, void* stream);
 int sfg_scan_u64(const uint64_t* in, int64_t n, int stride, int col, uint64_t* out, int out_stride,
-                 uint64_t* tmp, uint64_t* total, void* stream);
+                 int out_col, uint64_t* tmp, uint64_t* total, void* stream);
 
 #ifdef __cplusplus
 }

@@ -89,7 +89,7 @@ def lib():
     L.sfg_layout_probe.argtypes = [i32]
     L.sfg_layout_probe.restype = sz
     for f in ("sfg_scan_u32", "sfg_scan_u64"):
-        getattr(L, f).argtypes = [vp, i64, i32, i32, vp, i32, vp, vp, vp]
+        getattr(L, f).argtypes = [vp, i64, i32, i32, vp, i32, i32, vp, vp, vp]
     for f in EXPORTS:
         if f not in ("sfg_abi_version", "sfg_last_error", "sfg_program_destroy", "sfg_execute_smem_bytes",
                      "sfg_layout_probe"):

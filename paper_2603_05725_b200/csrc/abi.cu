@@ -72,8 +72,8 @@ static size_t exec_smem(const sfg_prog& P) {
 }
 
 template <typename T>
-static int scan_impl(const T* in, int64_t n, int stride, int col, uint64_t* out, int out_stride, uint64_t* tmp,
-                     uint64_t* total, void* stream, const char* name) {
+static int scan_impl(const T* in, int64_t n, int stride, int col, uint64_t* out, int out_stride, int out_col,
+                     uint64_t* tmp, uint64_t* total, void* stream, const char* name) {
   const int64_t tiles = (n + 2047) / 2048;
   if (n <= 0) {
     if (total) cudaMemsetAsync(total, 0, sizeof(uint64_t), S(stream));
@@ -83,7 +83,7 @@ static int scan_impl(const T* in, int64_t n, int stride, int col, uint64_t* out,
   SFG_CHECK_LAUNCH(name);
   sfg_scan_tile_sums<<<1, 256, 0, S(stream)>>>(tmp, tiles, total);
   SFG_CHECK_LAUNCH(name);
-  sfg_scan_apply<T><<<(unsigned)tiles, 256, 0, S(stream)>>>(in, n, stride, col, tmp, out, out_stride);
+  sfg_scan_apply<T><<<(unsigned)tiles, 256, 0, S(stream)>>>(in, n, stride, col, tmp, out, out_stride, out_col);
   SFG_CHECK_LAUNCH(name);
   return 0;
 }
@@ -255,14 +255,14 @@ int sfg_compact(const sfg_program* p, const void* children, const void* vals, co
   return 0;
 }
 
-int sfg_scan_u32(const uint32_t* in, int64_t n, int stride, int col, uint64_t* out, int out_stride, uint64_t* tmp,
-                 uint64_t* total, void* stream) {
-  return scan_impl(in, n, stride, col, out, out_stride, tmp, total, stream, "sfg_scan_u32");
+int sfg_scan_u32(const uint32_t* in, int64_t n, int stride, int col, uint64_t* out, int out_stride, int out_col,
+                 uint64_t* tmp, uint64_t* total, void* stream) {
+  return scan_impl(in, n, stride, col, out, out_stride, out_col, tmp, total, stream, "sfg_scan_u32");
 }
 
-int sfg_scan_u64(const uint64_t* in, int64_t n, int stride, int col, uint64_t* out, int out_stride, uint64_t* tmp,
-                 uint64_t* total, void* stream) {
-  return scan_impl(in, n, stride, col, out, out_stride, tmp, total, stream, "sfg_scan_u64");
+int sfg_scan_u64(const uint64_t* in, int64_t n, int stride, int col, uint64_t* out, int out_stride, int out_col,
+                 uint64_t* tmp, uint64_t* total, void* stream) {
+  return scan_impl(in, n, stride, col, out, out_stride, out_col, tmp, total, stream, "sfg_scan_u64");
 }
 
 }  // extern "C"

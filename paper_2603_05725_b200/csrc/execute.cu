@@ -345,7 +345,7 @@ SFG_DEV bool host_check(const sfg_prog& P, const Lane& L, sfg_verdict& V, int64_
 }
 
 SFG_DEV void edge_hit(uint32_t* ecnt, int e, bool& overflow) {
-  uint32_t* p = ecnt + e * 32;
+  uint32_t* p = ecnt + e * 32 + (threadIdx.x & 31);
   if (*p == 0xFFFFFFFFu) overflow = true; else ++*p;
 }
 

@@ -80,7 +80,7 @@ __global__ void sfg_scan_tile_sums(uint64_t* tile_sums, int64_t ntiles, uint64_t
 
 template <typename T>
 __global__ void sfg_scan_apply(const T* in, int64_t n, int stride, int col, const uint64_t* tile_off,
-                               uint64_t* out, int out_stride) {
+                               uint64_t* out, int out_stride, int out_col) {
   __shared__ uint64_t sh[32];
   const int64_t t0 = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
   uint64_t v[kScanItems];
@@ -92,15 +92,15 @@ __global__ void sfg_scan_apply(const T* in, int64_t n, int stride, int col, cons
   uint64_t total;
   uint64_t run = tile_off[blockIdx.x] + block_exclusive_scan(s, sh, total);
   for (int k = 0; k < kScanItems; ++k) {
-    if (t0 + k < n) out[(size_t)(t0 + k) * out_stride + col] = run;
+    if (t0 + k < n) out[(size_t)(t0 + k) * out_stride + out_col] = run;
     run += v[k];
   }
 }
 
 template __global__ void sfg_scan_tiles<uint32_t>(const uint32_t*, int64_t, int, int, uint64_t*);
 template __global__ void sfg_scan_tiles<uint64_t>(const uint64_t*, int64_t, int, int, uint64_t*);
-template __global__ void sfg_scan_apply<uint32_t>(const uint32_t*, int64_t, int, int, const uint64_t*, uint64_t*, int);
-template __global__ void sfg_scan_apply<uint64_t>(const uint64_t*, int64_t, int, int, const uint64_t*, uint64_t*, int);
+template __global__ void sfg_scan_apply<uint32_t>(const uint32_t*, int64_t, int, int, const uint64_t*, uint64_t*, int, int);
+template __global__ void sfg_scan_apply<uint64_t>(const uint64_t*, int64_t, int, int, const uint64_t*, uint64_t*, int, int);
 
 // ---- triage
 // stop/fatal: scalars[0] = stop index (UINT32_MAX none), scalars[1] = fatal index

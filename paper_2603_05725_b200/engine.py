@@ -213,7 +213,7 @@ class DeviceCampaign:
                          self.n_corpus, self.n_seeds)
 
     def _scan64(self, src, n, stride, col, out, out_stride, total_slot):
-        _native.check(self.L.sfg_scan_u64(src.data_ptr(), n, stride, col, out.data_ptr(), out_stride,
+        _native.check(self.L.sfg_scan_u64(src.data_ptr(), n, stride, col, out.data_ptr(), out_stride, 0,
                                           self.r_tmp.data_ptr(), self.r_tot.data_ptr() + 8 * total_slot,
                                           _stream()), "scan")
 
@@ -228,7 +228,7 @@ class DeviceCampaign:
         _native.check(L.sfg_plan(hp, ctypes.byref(cd), it0, n, self.r_parent.data_ptr(), self.r_picks.data_ptr(),
                                  self.r_flags.data_ptr(), s), "plan")
         for c in range(C):
-            _native.check(L.sfg_scan_u32(self.r_flags.data_ptr(), n, C, c, self.r_prefix.data_ptr(), C,
+            _native.check(L.sfg_scan_u32(self.r_flags.data_ptr(), n, C, c, self.r_prefix.data_ptr(), C, c,
                                          self.r_tmp.data_ptr(), self.r_tot.data_ptr() + 8 * (8 + c % 8), s),
                           "scan flags")
         _native.check(L.sfg_mutate(hp, ctypes.byref(cd), it0, n, self.r_prefix.data_ptr(),
