@@ -194,7 +194,7 @@ def run_ours(a):
     k3_avg_s = statistics.mean(k3_ms) / 1000.0
     bytes_exec = dc.algorithmic_exec_bytes()
     achieved = bytes_exec * R / k3_avg_s / 1e9
-    retired = dc.last_retired_mean
+    retired = dc.retired_mean(R)
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
             "traffic": None, "kernel": "sfg_execute_kernel", "bytes_per_exec": bytes_exec,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",

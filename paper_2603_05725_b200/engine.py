@@ -128,6 +128,9 @@ class DeviceCampaign:
         self._round_cap = 0
         self._work_cap = 0
         self.rounds = 0
+        self.launches = 0          # kernels launched through the C ABI (bench evidence)
+        self.timing = False        # record CUDA events around the execute kernel
+        self.last_exec_events = None
 
     # ---- buffers ---------------------------------------------------------------------
     def _u8(self, n):
@@ -213,6 +216,7 @@ class DeviceCampaign:
                          self.n_corpus, self.n_seeds)
 
     def _scan64(self, src, n, stride, col, out, out_stride, total_slot):
+        self.launches += 3
         _native.check(self.L.sfg_scan_u64(src.data_ptr(), n, stride, col, out.data_ptr(), out_stride, 0,
                                           self.r_tmp.data_ptr(), self.r_tot.data_ptr() + 8 * total_slot,
                                           _stream()), "scan")
@@ -225,6 +229,7 @@ class DeviceCampaign:
         if it0 + n - 1 >= 2 and self.low.prog["n_mutable"] == 0:
             raise MutationError("no mutable arguments")
         C = self.C
+        self.launches += 3 + 3 * C
         _native.check(L.sfg_plan(hp, ctypes.byref(cd), it0, n, self.r_parent.data_ptr(), self.r_picks.data_ptr(),
                                  self.r_flags.data_ptr(), s), "plan")
         for c in range(C):
@@ -250,13 +255,21 @@ class DeviceCampaign:
         return self._triage(it0, n)
 
     def _execute(self, n):
+        self.launches += 1
+        if self.timing:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
         _native.check(self.L.sfg_execute(
             self.h, n, self.r_children.data_ptr(), self.r_vals.data_ptr(), self.r_work_base.data_ptr(),
             self.r_work.data_ptr(), self.r_verdicts.data_ptr(), self.r_ecnt.data_ptr(), _ptr(self.r_readouts),
             self.r_ro_base.data_ptr(), _ptr(self.r_overlay), _stream()), "execute")
+        if self.timing:
+            ev[1].record()
+            self.last_exec_events = ev
 
     def _triage(self, it0, n) -> RoundResult:
         L, hp, s = self.L, self.h, _stream()
+        self.launches += 4
         self.r_scalars.fill_(-1)
         self.r_first.fill_(-1)
         self.r_kfirst.fill_(-1)
@@ -299,6 +312,7 @@ class DeviceCampaign:
 
     def _admit(self, n, n_adm):
         L, hp, s = self.L, self.h, _stream()
+        self.launches += 3
         _native.check(L.sfg_child_bytes(hp, self.r_vals.data_ptr(), self.r_admit.data_ptr(), n,
                                         self.r_bytes.data_ptr(), s), "child_bytes")
         self._scan64(self.r_bytes, n, 1, 0, self.r_boff, 1, 4)
@@ -360,6 +374,35 @@ class DeviceCampaign:
                 self.findings.add_many(rep, int(kc[k]))
                 out.append((i, rep))
         return out
+
+    # ---- bench / e2e helpers ----------------------------------------------------------
+    def corpus_host_pinned(self):
+        """Pinned host copies of the device corpus (meta, vals, child records, payload)."""
+        out = []
+        for t, nb in ((self.c_meta, self.n_corpus * ENTRY.itemsize),
+                      (self.c_vals, self.n_corpus * self.n_args * VAL.itemsize),
+                      (self.c_child, self.n_corpus * CHILD.itemsize), (self.c_data, self.corpus_bytes)):
+            h = torch.empty(max(nb, 1), dtype=torch.uint8, pin_memory=True)
+            h[:nb].copy_(t[:nb])
+            out.append(h)
+        return out
+
+    def load_corpus_from_host(self, host):
+        """Re-upload the corpus from pinned host buffers (stream-ordered H2D copies)."""
+        for t, h in zip((self.c_meta, self.c_vals, self.c_child, self.c_data), host):
+            t[:h.numel()].copy_(h, non_blocking=True)
+
+    def algorithmic_exec_bytes(self) -> int:
+        """Unavoidable off-chip bytes of one exec in the execute kernel: the child's
+        argument payload read once (SURVEY.md §8(d) C_write counterpart), its 64-byte
+        verdict and a 4*ceil(E/32)-byte edge-hit bitmap written."""
+        seed = self.host_entries[0][0]
+        payload = sum(len(v.data) if hasattr(v, "data") else 4 for v in seed.args)
+        return payload + 64 + 4 * ((self.E + 31) // 32)
+
+    def retired_mean(self, n: int) -> float:
+        v = _np(self.r_verdicts[:n * VERDICT.itemsize], VERDICT)
+        return float(v["retired"].astype(np.float64).mean())
 
     # ---- views for tests / reporting ----------------------------------------------------
     def coverage_map(self) -> CoverageMap:
