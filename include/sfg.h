@@ -65,6 +65,13 @@ int sfg_program_create(const void* prog, size_t prog_bytes, const void* ins, siz
 int sfg_program_update(sfg_program* p, const void* prog, size_t prog_bytes);
 void sfg_program_destroy(sfg_program* p);
 size_t sfg_execute_smem_bytes(const sfg_program* p);
+/* Generated CUDA source of the program's specialized execute kernel (0 if the
+ * generic interpreter is used, i.e. SFG_JIT=0). Copies at most cap-1 bytes. */
+size_t sfg_program_jit_source(const sfg_program* p, char* buf, size_t cap);
+/* Generate + NVRTC-compile the specialized kernel for a lowered program without
+ * loading it (no GPU needed).  out receives the source (and log on failure). */
+int sfg_jit_check(const void* prog, size_t prog_bytes, const void* ins, uint64_t max_edge_events, char* out,
+                  size_t cap, size_t* cubin_bytes);
 
 int sfg_plan(const sfg_program* p, const sfg_corpus_dev* c, int64_t it0, int n, int32_t* parent,
              int8_t* picks, uint32_t* int_flags, void* stream);

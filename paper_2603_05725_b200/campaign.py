@@ -1,0 +1,218 @@
+"""``fuzz_loop`` with the reference's signature and result types, on the GPU.
+
+Drop-in for ``simt_forge.campaign.fuzz_loop`` (campaign.py:683-822): same
+``CampaignConfig`` fields (plus ``round_size`` and ``device``), same
+``CampaignSummary`` (findings as a ``FindingsLog`` of ``BugReport``,
+``CoverageMap``, ``Corpus`` of ``TestCase``), same output directory layout.
+
+Semantics are the batched-round contract: iterations are
+processed in rounds of ``round_size`` inputs; input ``it`` draws from its own
+Philox stream ``(master_seed, 2**32 + it)`` and schedules its parent from the
+corpus as it stood at its round's start.  Everything else (rotation counts,
+alloc ids, absorption order, admission, dedupe, stop rules) follows the
+reference in ``it`` order, so results equal the reference functions driven
+the same way (tests/golden/make_golden.py ``batched``).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from pathlib import Path
+
+from .baseline import MemConfig
+from .coverage import build_report, render_text, report_to_rec
+from .engine import DeviceCampaign, MutationConfig
+from .findings import BugClass, FindingsLog
+from .lowering import LoweringError
+from .manifest import HarnessManifest, load_harness  # noqa: F401  (re-export)
+from .testcase import argspec_digest, serialize_testcase
+
+
+class CampaignFatalError(Exception):
+    pass
+
+
+@dataclass
+class CorpusEntry:
+    tc: object
+    admitted_iteration: int
+    is_seed: bool
+
+
+@dataclass
+class Corpus:
+    entries: list = field(default_factory=list)
+
+    @property
+    def seeds(self) -> int:
+        return sum(1 for e in self.entries if e.is_seed)
+
+    @property
+    def interesting(self) -> int:
+        return sum(1 for e in self.entries if not e.is_seed)
+
+
+@dataclass
+class CampaignConfig:
+    master_seed: int = 1
+    iterations: int = 1000
+    workers: int = 1
+    mode: str = "amortized"
+    out_dir: Path | None = None
+    stop_on_first_finding: bool = False
+    stop_bug_class: BugClass | str | None = None
+    max_wall_seconds: float | None = None
+    instruction_budget: int = 1_000_000
+    mem_config: MemConfig = field(default_factory=MemConfig)
+    mutation: MutationConfig = field(default_factory=MutationConfig)
+    admission_window: int = 256
+    recent_weight: float = 4.0
+    diff_readback: bool = False
+    hooks: object = None
+    round_size: int = 65536
+    device: str | None = None
+
+
+@dataclass
+class CampaignSummary:
+    master_seed: int
+    iterations_requested: int
+    iterations_executed: int
+    workers: int
+    mode: str
+    program_digest: str
+    manifest_digest: str
+    argspec_digest: str
+    findings: FindingsLog
+    coverage: object
+    corpus: Corpus
+    stop_reason: str
+    init_runs: int
+    compute_runs: int
+    term_runs: int
+    wall_seconds: float
+    out_dir: Path | None
+
+    @property
+    def execs_per_second(self) -> float:
+        return self.compute_runs / self.wall_seconds if self.wall_seconds > 0 else 0.0
+
+    def to_rec(self) -> str:
+        return "\n".join([
+            "summary v1",
+            f"master_seed={self.master_seed} workers={self.workers} mode={self.mode}",
+            f"iterations_requested={self.iterations_requested} iterations_executed={self.iterations_executed}",
+            f"program={self.program_digest} manifest={self.manifest_digest} argspec={self.argspec_digest}",
+            f"findings_unique={len(self.findings)} findings_total={self.findings.total}",
+            f"corpus_seeds={self.corpus.seeds} corpus_interesting={self.corpus.interesting}",
+            f"init_runs={self.init_runs} compute_runs={self.compute_runs} term_runs={self.term_runs}",
+            f"stop={self.stop_reason}",
+        ]) + "\n"
+
+
+def _worker_ranges(total: int, workers: int):
+    base, rem = divmod(total, workers)
+    out, start = [], 1
+    for w in range(workers):
+        n = base + (1 if w < rem else 0)
+        out.append(range(start, start + n))
+        start += n
+    return out
+
+
+def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
+    if config.mode not in ("amortized", "reinit"):
+        raise CampaignFatalError(f"unknown mode {config.mode!r}")
+    if config.workers < 1 or config.iterations < 1:
+        raise CampaignFatalError("workers and iterations must be >= 1")
+    if config.hooks is not None:
+        raise LoweringError("per-event Python hooks are not supported on the device path")
+    for op in manifest.phases["term"]:
+        if op.kind not in ("free", "sync"):
+            raise LoweringError("TERM phases other than frees are not lowered")
+    out_dir = Path(config.out_dir) if config.out_dir is not None else None
+    specs = manifest.argspecs
+    if out_dir is not None:
+        (out_dir / "corpus").mkdir(parents=True, exist_ok=True)
+        (out_dir / "crashes").mkdir(parents=True, exist_ok=True)
+        (out_dir / "program.sir").write_text(manifest.program_text)
+        (out_dir / "harness.man").write_text(manifest.portable_text("program.sir"))
+    t0 = time.perf_counter()
+    deadline = t0 + config.max_wall_seconds if config.max_wall_seconds else None
+    dc = DeviceCampaign(manifest, master_seed=config.master_seed, mem=config.mem_config,
+                        mutation=config.mutation, budget=config.instruction_budget,
+                        window=config.admission_window, recent_weight=config.recent_weight,
+                        diff_readback=config.diff_readback, stop_on_first_finding=config.stop_on_first_finding,
+                        stop_bug_class=config.stop_bug_class, device=config.device,
+                        ids_reset_per_input=config.mode == "reinit")
+    if out_dir is not None:
+        _write_corpus_entry(out_dir, dc.host_entries[0][0], specs)
+    stop_reason = "iterations"
+    executed = 0
+    init_runs = term_runs = 0
+    try:
+        for w, rng_ in enumerate(_worker_ranges(config.iterations, config.workers)):
+            if stop_reason != "iterations":
+                break
+            dc.new_worker()   # fresh rotation counts + alloc ids (one image per worker)
+            if config.mode == "amortized":
+                init_runs += 1
+            it = rng_.start
+            while it < rng_.stop:
+                if deadline is not None and time.perf_counter() > deadline:
+                    stop_reason = "wall_clock"
+                    break
+                n = min(config.round_size, rng_.stop - it)
+                before = len(dc.host_entries)
+                res = dc.run_round(it, n)
+                executed += res.executed
+                if config.mode == "reinit":
+                    init_runs += res.executed
+                    term_runs += res.executed
+                if out_dir is not None:
+                    for tc, _, _ in dc.host_entries[before:]:
+                        _write_corpus_entry(out_dir, tc, specs)
+                    if res.new_keys:
+                        tcs = dc.child_testcases([i for i, _ in res.new_keys])
+                        for (i, rep), tc in zip(res.new_keys, tcs):
+                            _write_crash(out_dir, rep, tc, specs, manifest)
+                if res.stop is not None:
+                    want = config.stop_bug_class
+                    stop_reason = ("first_finding" if config.stop_on_first_finding else
+                                   f"bug_class:{getattr(want, 'value', want)}")
+                    break
+                it += n
+            if config.mode == "amortized":
+                term_runs += 1
+    except CampaignFatalError:
+        if out_dir is not None:
+            (out_dir / "FAILED").write_text("campaign fatal\n")
+        raise
+    wall = time.perf_counter() - t0
+    corpus = Corpus([CorpusEntry(tc, adm, seed) for tc, adm, seed in dc.host_entries])
+    cov = dc.coverage_map()
+    summary = CampaignSummary(config.master_seed, config.iterations, executed, config.workers, config.mode,
+                              manifest.program_digest, manifest.digest, argspec_digest(specs), dc.findings,
+                              cov, corpus, stop_reason, init_runs, executed, term_runs, wall, out_dir)
+    if out_dir is not None:
+        rep = build_report(cov)
+        (out_dir / "coverage.txt").write_text(render_text(rep))
+        (out_dir / "coverage.rec").write_text(report_to_rec(rep))
+        (out_dir / "findings.txt").write_text(dc.findings.render_text())
+        (out_dir / "summary.rec").write_text(summary.to_rec())
+        (out_dir / "timing.rec").write_text(
+            f"timing v1\nwall_seconds={wall:.6f} execs_per_second={summary.execs_per_second:.2f}\n")
+    dc.close()
+    return summary
+
+
+def _write_corpus_entry(out_dir: Path, tc, specs) -> None:
+    (out_dir / "corpus" / f"{tc.id}.tc").write_text(serialize_testcase(tc, specs))
+
+
+def _write_crash(out_dir: Path, report, tc, specs, manifest) -> None:
+    extra = [f"crash class={report.bug_class.value} dedupe={report.dedupe_key} kernel={report.kernel} "
+             f"iid={report.iid} addr=0x{report.address:x} width={report.width} iteration={report.iteration}",
+             f"origin harness=../harness.man program={manifest.program_digest} manifest={manifest.digest}"]
+    (out_dir / "crashes" / f"{report.dedupe_key}.tc").write_text(serialize_testcase(tc, specs, extra=extra))

@@ -2,6 +2,7 @@
 // No torch types cross this boundary; the Python host passes raw device
 // pointers (torch tensors' data_ptr) and torch's current stream.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -10,6 +11,9 @@
 
 struct sfg_program {
   sfg_prog P;
+  cudaLibrary_t jit_lib = nullptr;    // specialized execute kernel (jit.cu), if built
+  cudaKernel_t jit_kernel = nullptr;
+  std::string jit_source, jit_log;
   sfg_ins* ins;
   sfg_hostop* hostops;
   sfg_binding* binds;
@@ -35,6 +39,7 @@ static_assert(sizeof(sfg_prog) < 4096, "sfg_prog must fit the kernel parameter s
 #include "mutate.cu"
 #include "execute.cu"
 #include "triage.cu"
+#include "jit.cu"
 
 static thread_local std::string g_err;
 
@@ -134,6 +139,24 @@ int sfg_program_create(const void* prog, size_t prog_bytes, const void* ins, siz
   }
   p->base_blob = (const uint8_t*)base_blob_dev;
   p->smem = exec_smem(p->P);
+  const char* jit_env = getenv("SFG_JIT");
+  if (!(jit_env && jit_env[0] == '0')) {
+    // bound on per-input edge events decides whether counters need overflow checks
+    uint64_t events = 0;
+    const sfg_hostop* H = (const sfg_hostop*)hostops;
+    for (size_t h = 0; h < n_hostops; ++h)
+      if (H[h].kind == SFG_H_LAUNCH) {
+        const double ev = (double)H[h].grid * (double)H[h].block * (double)p->P.budget;
+        events = (ev + (double)events >= 1.8e19) ? ~0ull : events + (uint64_t)ev;
+      }
+    const int rc = sfg_jit_build(p->P, (const sfg_ins*)ins, events, p->jit_source, p->jit_log, &p->jit_lib,
+                                 &p->jit_kernel);
+    if (rc != 0) {
+      g_err = "sfg_program_create: JIT build failed (" + std::to_string(rc) + "): " + p->jit_log.substr(0, 6000);
+      sfg_program_destroy(p);
+      return 1;
+    }
+  }
   e = cudaFuncSetAttribute(sfg_execute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem);
   if (e != cudaSuccess) {
     sfg_program_destroy(p);
@@ -154,6 +177,7 @@ int sfg_program_update(sfg_program* p, const void* prog, size_t prog_bytes) {
 
 void sfg_program_destroy(sfg_program* p) {
   if (!p) return;
+  if (p->jit_lib) cudaLibraryUnload(p->jit_lib);
   cudaFree(p->ins);
   cudaFree(p->hostops);
   cudaFree(p->binds);
@@ -163,6 +187,38 @@ void sfg_program_destroy(sfg_program* p) {
 }
 
 size_t sfg_execute_smem_bytes(const sfg_program* p) { return p->smem; }
+
+int sfg_jit_check(const void* prog, size_t prog_bytes, const void* ins, uint64_t max_edge_events, char* out,
+                  size_t cap, size_t* cubin_bytes) {
+  if (prog_bytes != sizeof(sfg_prog)) {
+    g_err = "sfg_jit_check: sfg_prog size mismatch";
+    return 1;
+  }
+  sfg_prog P;
+  memcpy(&P, prog, sizeof P);
+  std::string src, log;
+  std::vector<char> cubin;
+  const int rc = sfg_jit_compile(P, (const sfg_ins*)ins, max_edge_events, src, log, cubin);
+  const std::string text = rc ? log + "\n----\n" + src : src;
+  if (out && cap) {
+    const size_t n = text.size() < cap - 1 ? text.size() : cap - 1;
+    memcpy(out, text.data(), n);
+    out[n] = 0;
+  }
+  if (cubin_bytes) *cubin_bytes = cubin.size();
+  if (rc) g_err = "sfg_jit_check: compile failed";
+  return rc;
+}
+
+size_t sfg_program_jit_source(const sfg_program* p, char* buf, size_t cap) {
+  if (!p->jit_kernel) return 0;
+  if (buf && cap) {
+    const size_t n = p->jit_source.size() < cap - 1 ? p->jit_source.size() : cap - 1;
+    memcpy(buf, p->jit_source.data(), n);
+    buf[n] = 0;
+  }
+  return p->jit_source.size();
+}
 
 int sfg_plan(const sfg_program* p, const sfg_corpus_dev* c, int64_t it0, int n, int32_t* parent, int8_t* picks,
              uint32_t* int_flags, void* stream) {
@@ -206,6 +262,13 @@ int sfg_execute(const sfg_program* p, int n, const void* children, const void* v
   ExecView E{p->ins, p->hostops, p->binds, p->recs, p->base_blob, p->const_blob,
                 (const sfg_child*)children, (const sfg_val*)vals, work_base, work,
                 (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, overlay, n};
+  if (p->jit_kernel) {
+    void* args[] = {(void*)&p->P, (void*)&E};
+    const cudaError_t e = cudaLaunchKernel((const void*)p->jit_kernel, dim3(blocks_for(n, 128)), dim3(128), args, 0,
+                                           S(stream));
+    if (e != cudaSuccess) return fail("sfg_execute (jit)", e);
+    return 0;
+  }
   sfg_execute_kernel<<<blocks_for(n, 128), 128, p->smem, S(stream)>>>(p->P, E);
   SFG_CHECK_LAUNCH("sfg_execute");
   return 0;

@@ -1,7 +1,9 @@
 // Small device helpers shared by the kernels.
 #pragma once
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
 #include <stdint.h>
+#endif
 
 #include "sfg_types.h"
 
@@ -36,6 +38,15 @@ struct CorpusView {
   int32_t n;        // entries at round start
   int32_t n_seeds;  // seeds form the prefix [0, n_seeds)
 };
+
+// cvt_f32_to_i32 (executor.py:51-65): NaN -> 0, saturate, round half to even
+SFG_DEV uint32_t sfg_cvt_f2i(uint32_t fb) {
+  const float fv = sfg_f(fb);
+  if (sfg_isnan_bits(fb)) return 0u;
+  if (fv >= 2147483647.0f) return 0x7FFFFFFFu;
+  if (fv <= -2147483648.0f) return 0x80000000u;
+  return (uint32_t)__float2int_rn(fv);
+}
 
 SFG_DEV uint64_t sfg_align16(uint64_t n) { return (n + 15ull) & ~15ull; }
 

@@ -1,353 +1,205 @@
-// K3: execute + sanitize + cover, one fuzz input per lane.
+// K3 (generic path): the SIR interpreter runner for exec_core's host-op driver.
 //
-// Each lane runs its input's COMPUTE host-op script (campaign.py:483-561) and
-// interprets every launch's simulated threads strictly sequentially
-// (block-major, thread-major, run-to-completion, first-bug-stop, per-thread
-// retired budget; executor.py:390-424), so results are bit-identical with the
-// reference interpreter.  32 inputs of the same harness share a warp.
-//
-// Memory model per input (no per-input copy of the 16+ MiB image):
-//   * allocation records: the post-INIT baseline table (constant) + this
-//     input's own allocations/frees, in a small local-memory table; shadow
-//     codes are derived analytically from it (device_memory.py:347-393 proves
-//     shadow == f(registry, quarantine)), so nothing is staged per granule;
-//   * payload bytes: the input's materialized arrays and COMPUTE allocs live in
-//     its work region (written by sfg_apply_kernel); INIT buffers are read from
-//     the shared baseline blob with a per-input byte overlay for writes.
-//   * simulated register files live in shared memory, [reg][lane] so that a
-//     converged warp touches 32 consecutive banks; per-edge hit counters too.
-//
-// Sanitizer order = sanitizer.py:145-187 (SPACE_MISMATCH -> TEMPORAL_UAF ->
-// shadow scan (SPATIAL_OOB / freed) -> PROVENANCE_ESCAPE -> WILD_ACCESS), with
-// a provenance fast path that is provably equivalent when the tagged record's
-// live payload contains the whole access.
-#include "common.cuh"
+// Simulated register files live in shared memory, [reg][lane], so a converged
+// warp touches 32 consecutive banks; per-edge hit counters likewise [edge][lane].
+// Instruction semantics follow executor.py:210-377 (see exec_core.cuh).
+#include "exec_core.cuh"
 
 namespace {
 
-constexpr uint8_t SH_RZ = 0xFA, SH_FREED = 0xFD, SH_UNALLOC = 0xFF;
-constexpr int kMaxQ = 32;
-constexpr int kMaxFree = 32;
+struct InterpRunner {
+  const sfg_ins* s_ins;
+  uint64_t* s_alo;
+  uint32_t *s_r, *s_f;
+  int32_t *s_ahi, *s_ap;
+  uint32_t* s_ecnt;
+  int lane, n_edges;
+  bool overflow;
 
-enum : uint8_t { R_FREED = 1, R_RES = 2, R_BASE = 4 };
-
-struct LRec {            // 48 bytes
-  int64_t base, size, slot_start, slot_end;
-  int64_t phys;          // baseline: blob offset, own: work-region offset
-  int32_t id;            // >0 campaign id (baseline), <0 -(k+1) own k-th allocation
-  int16_t label;
-  uint8_t space, flags;
-};
-
-struct Lane {
-  LRec rec[SFG_MAX_LANE_RECS];
-  int nrec, nalloc, nq, nfree, nov;
-  int64_t cursor[3], qbytes[3];
-  int16_t quar[kMaxQ];
-  sfg_free fl[kMaxFree];
-  int64_t named_addr[SFG_MAX_NAMED];
-  int16_t named_rec[SFG_MAX_NAMED];
-  int16_t mat_rec[SFG_MAX_ARGS];
-  uint64_t ro_cursor;
-};
-
-}  // namespace
-
-struct ExecView {
-  const sfg_ins* ins;
-  const sfg_hostop* hostops;
-  const sfg_binding* binds;
-  const sfg_rec* base_recs;
-  const uint8_t* base_blob;
-  const uint8_t* const_blob;
-  const sfg_child* children;
-  const sfg_val* vals;
-  const uint64_t* work_base;
-  uint8_t* work;
-  sfg_verdict* verdicts;
-  uint32_t* edge_counts;       // [n][n_edges]
-  uint8_t* readouts;
-  const uint64_t* readout_base;
-  uint64_t* overlay;           // [n][SFG_OVERLAY] packed (addr << 8 | byte)
-  int n;
-};
-
-namespace {
-
-typedef __int128 i128;
-
-// space bases 0x1000_0000 / 0x2000_0000 / 0x3000_0000 (device_memory.py:41-45)
-SFG_DEV int64_t sbase(int s) { return (int64_t)(s + 1) << 28; }
-
-struct Report {
-  int cls, mech, shadow;       // shadow -1 none
-  int rec;                     // attributed lane record, -1 none
-};
-
-// ---------------------------------------------------------------------------
-// allocation registry (device_memory.py:397-517), analytic shadow
-
-SFG_DEV int space_of(const sfg_prog& P, i128 a) {
-  for (int s = 0; s < 3; ++s)
-    if (a >= (i128)sbase(s) && a < (i128)(sbase(s) + P.space_size[s])) return s;
-  return -1;
-}
-
-SFG_DEV int resolve_payload(const Lane& L, int sp, int64_t a) {
-  for (int k = 0; k < L.nrec; ++k) {
-    const LRec& r = L.rec[k];
-    if ((r.flags & R_RES) && r.space == sp && r.base <= a && a < r.base + r.size) return k;
+  SFG_DEV void begin_input() {
+    overflow = false;
+    for (int e = 0; e < n_edges; ++e) s_ecnt[e * 32 + lane] = 0;
   }
-  return -1;
-}
 
-SFG_DEV int resolve_slot(const Lane& L, int sp, int64_t a) {
-  for (int k = 0; k < L.nrec; ++k) {
-    const LRec& r = L.rec[k];
-    if ((r.flags & R_RES) && r.space == sp && r.slot_start <= a && a < r.slot_end) return k;
+  SFG_DEV void hit(int e) {
+    uint32_t* p = s_ecnt + e * 32 + lane;
+    if (*p == 0xFFFFFFFFu) overflow = true; else ++*p;
   }
-  return -1;
-}
 
-struct Scan { int kind; int64_t gaddr; int code; };  // kind 0 none, 1 spatial, 2 freed, 3 wild
+  SFG_DEV void flush(uint32_t* erow, bool& ovf) {
+    for (int e = 0; e < n_edges; ++e) erow[e] = s_ecnt[e * 32 + lane];
+    ovf = overflow;
+  }
 
-// _scan_shadow (sanitizer.py:102-142) on shadow codes derived from the registry
-SFG_DEV Scan scan_shadow(const sfg_prog& P, const Lane& L, i128 a, int64_t width) {
-  const int sp = space_of(P, a);
-  if (sp < 0) return {3, 0, SH_UNALLOC};
-  const int64_t g = P.granule;
-  const int64_t sb = sbase(sp);
-  const int64_t addr = (int64_t)a;
-  const int64_t end = addr + width;
-  int64_t gi = (addr - sb) / g;
-  while (true) {
-    const int64_t gstart = sb + gi * g;
-    if (gstart >= end) return {0, 0, 0};
-    if (gi * g >= P.space_size[sp]) return {3, gstart, SH_UNALLOC};
-    const int k = resolve_slot(L, sp, gstart);
-    if (k < 0) return {3, gstart, SH_UNALLOC};
-    const LRec& r = L.rec[k];
-    const int64_t pay_end = r.base + ((r.size + g - 1) / g) * g;
-    if (gstart < r.base || gstart >= pay_end) return {1, gstart, SH_RZ};
-    if (r.flags & R_FREED) return {2, gstart, SH_FREED};
-    const int64_t full_end = r.base + (r.size / g) * g;
-    if (gstart < full_end) {       // run of addressable granules: jump past it
-      gi = (full_end - sb) / g;
-      continue;
+  SFG_DEV int run_thread(const sfg_prog& P, int kidx, Lane& L, Mem& M, sfg_verdict& V, const Pre& pre, int ctaid,
+                         int tid, int grid, int block, uint64_t& total_retired) {
+    const sfg_kernel& K = P.kernels[kidx];
+    const sfg_ins* kins = s_ins + K.ins_base;
+    const int regs = K.regs;
+    for (int q = 0; q < regs; ++q) {  // make_thread (executor.py:191-202)
+      s_r[q * 32 + lane] = q < pre.nr ? pre.r[q] : 0u;
+      s_f[q * 32 + lane] = q < pre.nf ? pre.f[q] : 0u;
+      s_alo[q * 32 + lane] = q < pre.na ? (uint64_t)pre.a[q] : 0ull;
+      s_ahi[q * 32 + lane] = q < pre.na ? (pre.a[q] < 0 ? -1 : 0) : 0;
+      s_ap[q * 32 + lane] = q < pre.na ? pre.ap[q] : 0;
     }
-    const int64_t code = r.size % g;  // partial tail granule
-    const int64_t lo = (addr > gstart ? addr : gstart) - gstart;
-    const int64_t hi = (end < gstart + g ? end : gstart + g) - gstart;
-    if (lo >= code || hi > code) return {1, gstart, (int)code};
-    ++gi;
-  }
-}
-
-// check_access (sanitizer.py:145-187).  prov: lane record index + 1, 0 none.
-SFG_DEV bool check_access(const sfg_prog& P, const Lane& L, i128 a, int64_t width, int decl, int prov,
-                          Report& rep, int& hit) {
-  // fast path: the tagged live record contains the whole access in its declared space
-  if (prov > 0) {
-    const LRec& t = L.rec[prov - 1];
-    if ((t.flags & (R_RES | R_FREED)) == R_RES && t.space == decl && a >= (i128)t.base &&
-        a + width <= (i128)(t.base + t.size)) {
-      hit = prov - 1;
-      return false;
+    uint32_t preds = 0;
+    int pc = 0;
+    uint64_t retired = 0;
+    int rc = RUN_EXIT;
+    while (true) {
+      const sfg_ins I = kins[pc];
+      ++retired;
+      if (I.op == SFG_EXIT) break;
+      if (I.op == SFG_BRA) {
+        bool taken = true;
+        if (I.flags & SFG_F_PRED) taken = (((preds >> I.s1) & 1u) != 0) != ((I.flags & SFG_F_PNEG) != 0);
+        hit(taken ? I.edge_tk : I.edge_ft);
+        pc = taken ? I.target : pc + 1;
+        if (retired >= P.budget) { rc = RUN_BUDGET; break; }
+        continue;
+      }
+      switch (I.op) {
+        case SFG_LD:
+        case SFG_ST: {
+          const i128 areg = ((i128)s_ahi[I.s1 * 32 + lane] << 64) | (i128)s_alo[I.s1 * 32 + lane];
+          const i128 a = areg + (i128)I.imm2;
+          const int prov = s_ap[I.s1 * 32 + lane];
+          const bool st = I.op == SFG_ST;
+          Report rep;
+          int rh = -1;
+          if (check_access(P, L, a, I.width, I.space, prov, rep, rh)) {
+            fill_report(V, P, L, rep, kidx, pc, ctaid, tid, a, I.width, st, I.space, prov);
+            rc = RUN_FINDING;
+            break;
+          }
+          const LRec& r = L.rec[rh];
+          const int64_t aa = (int64_t)a;
+          if (st) {
+            uint64_t val;
+            if (I.mode == SFG_MK_F32) val = (I.flags & SFG_F_S2_IMM) ? (uint64_t)(uint32_t)I.imm1 : s_f[I.s2 * 32 + lane];
+            else if (I.mode == SFG_MK_B64) val = s_alo[I.s2 * 32 + lane];
+            else val = (I.flags & SFG_F_S2_IMM) ? (uint64_t)I.imm1 : (uint64_t)s_r[I.s2 * 32 + lane];
+            if (!mem_write(M, L, r, aa, I.width, val)) { V.status = SFG_ST_OVERLAY; rc = RUN_FATAL; }
+          } else {
+            const uint64_t val = mem_read(M, L, r, aa, I.width);
+            switch (I.mode) {
+              case SFG_MK_F32: s_f[I.dst * 32 + lane] = sfg_quiet((uint32_t)val); break;
+              case SFG_MK_B64:
+                s_alo[I.dst * 32 + lane] = val;
+                s_ahi[I.dst * 32 + lane] = 0;
+                s_ap[I.dst * 32 + lane] = 0;
+                break;
+              default: s_r[I.dst * 32 + lane] = (uint32_t)val; break;  // b8/b16 zero-extend, b32 bits
+            }
+          }
+          break;
+        }
+        case SFG_MOV:
+          if (I.mode == SFG_CLS_R) {
+            s_r[I.dst * 32 + lane] = (I.flags & SFG_F_S1_IMM) ? (uint32_t)I.imm1 : s_r[I.s1 * 32 + lane];
+          } else if (I.mode == SFG_CLS_F) {
+            s_f[I.dst * 32 + lane] = (I.flags & SFG_F_S1_IMM) ? (uint32_t)I.imm1 : s_f[I.s1 * 32 + lane];
+          } else if (I.mode == SFG_CLS_A) {
+            if (I.flags & SFG_F_S1_IMM) {
+              s_alo[I.dst * 32 + lane] = (uint64_t)I.imm1;
+              s_ahi[I.dst * 32 + lane] = (I.flags & SFG_F_U64IMM) ? 0 : (I.imm1 < 0 ? -1 : 0);
+              s_ap[I.dst * 32 + lane] = 0;
+            } else {
+              s_alo[I.dst * 32 + lane] = s_alo[I.s1 * 32 + lane];
+              s_ahi[I.dst * 32 + lane] = s_ahi[I.s1 * 32 + lane];
+              s_ap[I.dst * 32 + lane] = s_ap[I.s1 * 32 + lane];
+            }
+          } else {
+            preds = (preds & ~(1u << I.dst)) | (((preds >> I.s1) & 1u) << I.dst);
+          }
+          break;
+        case SFG_ADD:
+        case SFG_SUB:
+        case SFG_MUL:
+          if (I.mode == SFG_CLS_A) {
+            const i128 base = ((i128)s_ahi[I.s1 * 32 + lane] << 64) | (i128)s_alo[I.s1 * 32 + lane];
+            const int64_t d = (I.flags & SFG_F_S2_IMM) ? I.imm2 : (int64_t)(int32_t)s_r[I.s2 * 32 + lane];
+            const i128 res = I.op == SFG_ADD ? base + (i128)d : base - (i128)d;
+            s_alo[I.dst * 32 + lane] = (uint64_t)res;
+            s_ahi[I.dst * 32 + lane] = (int32_t)(int64_t)(res >> 64);
+            s_ap[I.dst * 32 + lane] = s_ap[I.s1 * 32 + lane];
+          } else {
+            const uint32_t x = (I.flags & SFG_F_S1_IMM) ? (uint32_t)I.imm1 : s_r[I.s1 * 32 + lane];
+            const uint32_t y = (I.flags & SFG_F_S2_IMM) ? (uint32_t)I.imm2 : s_r[I.s2 * 32 + lane];
+            s_r[I.dst * 32 + lane] = I.op == SFG_ADD ? x + y : (I.op == SFG_SUB ? x - y : x * y);
+          }
+          break;
+        case SFG_FADD:
+        case SFG_FSUB:
+        case SFG_FMUL: {
+          const uint32_t x = (I.flags & SFG_F_S1_IMM) ? (uint32_t)I.imm1 : s_f[I.s1 * 32 + lane];
+          const uint32_t y = (I.flags & SFG_F_S2_IMM) ? (uint32_t)I.imm2 : s_f[I.s2 * 32 + lane];
+          s_f[I.dst * 32 + lane] = sfg_fop(I.op, x, y);
+          break;
+        }
+        case SFG_SETP: {
+          bool res;
+          if (I.flags & SFG_F_FLOAT) {
+            const float x = sfg_f((I.flags & SFG_F_S1_IMM) ? (uint32_t)I.imm1 : s_f[I.s1 * 32 + lane]);
+            const float y = sfg_f((I.flags & SFG_F_S2_IMM) ? (uint32_t)I.imm2 : s_f[I.s2 * 32 + lane]);
+            switch (I.mode) {
+              case SFG_CMP_EQ: res = x == y; break;
+              case SFG_CMP_NE: res = x != y; break;
+              case SFG_CMP_LT: res = x < y; break;
+              case SFG_CMP_LE: res = x <= y; break;
+              case SFG_CMP_GT: res = x > y; break;
+              default: res = x >= y; break;
+            }
+          } else {
+            const int64_t x = (I.flags & SFG_F_S1_IMM) ? I.imm1 : (int64_t)(int32_t)s_r[I.s1 * 32 + lane];
+            const int64_t y = (I.flags & SFG_F_S2_IMM) ? I.imm2 : (int64_t)(int32_t)s_r[I.s2 * 32 + lane];
+            switch (I.mode) {
+              case SFG_CMP_EQ: res = x == y; break;
+              case SFG_CMP_NE: res = x != y; break;
+              case SFG_CMP_LT: res = x < y; break;
+              case SFG_CMP_LE: res = x <= y; break;
+              case SFG_CMP_GT: res = x > y; break;
+              default: res = x >= y; break;
+            }
+          }
+          preds = (preds & ~(1u << I.dst)) | ((uint32_t)res << I.dst);
+          break;
+        }
+        case SFG_CVT:
+          if (I.mode == SFG_CVT_F_FROM_I) {
+            s_f[I.dst * 32 + lane] = (I.flags & SFG_F_S1_IMM)
+                                         ? (uint32_t)I.imm1
+                                         : sfg_b(__int2float_rn((int32_t)s_r[I.s1 * 32 + lane]));
+          } else if (I.flags & SFG_F_S1_IMM) {
+            s_r[I.dst * 32 + lane] = (uint32_t)I.imm1;
+          } else {  // cvt_f32_to_i32 (executor.py:51-65)
+            const uint32_t fb = s_f[I.s1 * 32 + lane];
+            const float fv = sfg_f(fb);
+            int32_t out;
+            if (sfg_isnan_bits(fb)) out = 0;
+            else if (fv >= 2147483647.0f) out = 2147483647;
+            else if (fv <= -2147483648.0f) out = (int32_t)0x80000000u;
+            else out = __float2int_rn(fv);
+            s_r[I.dst * 32 + lane] = (uint32_t)out;
+          }
+          break;
+        default: {  // SREG
+          const int v = I.mode == SFG_SR_TID ? tid : I.mode == SFG_SR_NTID ? block
+                      : I.mode == SFG_SR_CTAID ? ctaid : grid;
+          s_r[I.dst * 32 + lane] = (uint32_t)v;
+          break;
+        }
+      }
+      if (rc != RUN_EXIT) break;
+      if (I.edge_ft >= 0) hit(I.edge_ft);
+      ++pc;
+      if (retired >= P.budget) { rc = RUN_BUDGET; break; }
     }
+    total_retired += retired;
+    return rc;
   }
-  const int sp = space_of(P, a);
-  int r = sp >= 0 ? resolve_payload(L, sp, (int64_t)a) : -1;
-  if (r >= 0 && L.rec[r].space != decl) { rep = {SFG_C_SPACE_MISMATCH, SFG_MECH_REGISTRY, -1, r}; return true; }
-  if (r >= 0 && (L.rec[r].flags & R_FREED)) { rep = {SFG_C_TEMPORAL_UAF, SFG_MECH_SHADOW, SH_FREED, r}; return true; }
-  const Scan v = scan_shadow(P, L, a, width);
-  if (v.kind == 1) {
-    rep = {SFG_C_SPATIAL_OOB, SFG_MECH_SHADOW, v.code, r >= 0 ? r : resolve_slot(L, space_of(P, v.gaddr), v.gaddr)};
-    return true;
-  }
-  if (v.kind == 2) {
-    rep = {SFG_C_TEMPORAL_UAF, SFG_MECH_SHADOW, v.code, resolve_slot(L, space_of(P, v.gaddr), v.gaddr)};
-    return true;
-  }
-  if (prov > 0) {
-    const LRec& t = L.rec[prov - 1];
-    if (!(a >= (i128)t.base && a + width <= (i128)(t.base + t.size))) {
-      rep = {SFG_C_PROVENANCE_ESCAPE, SFG_MECH_PROVENANCE, v.kind ? v.code : -1, prov - 1};
-      return true;
-    }
-  }
-  if (v.kind == 3) { rep = {SFG_C_WILD_ACCESS, SFG_MECH_SHADOW, v.code, -1}; return true; }
-  hit = r;
-  return false;
-}
-
-// _alloc_common (device_memory.py:407-440), scope 0; returns record index or -status
-SFG_DEV int lane_alloc(const sfg_prog& P, Lane& L, int sp, int64_t size, int label, int64_t phys) {
-  const int64_t g = P.granule, rz = P.redzone;
-  const int64_t slot = rz + ((size + g - 1) / g) * g + rz;
-  int best = -1;
-  for (int k = 0; k < L.nfree; ++k)
-    if (L.fl[k].space == sp && L.fl[k].scope == 0 && L.fl[k].slot == slot && (best < 0 || L.fl[k].off < L.fl[best].off))
-      best = k;
-  int64_t off;
-  if (best >= 0) {
-    off = L.fl[best].off;
-    L.fl[best] = L.fl[--L.nfree];
-  } else {
-    if (L.cursor[sp] + slot > P.scope_size[sp]) return -SFG_ST_OUT_OF_SPACE;
-    off = L.cursor[sp];
-    L.cursor[sp] += slot;
-  }
-  if (L.nrec >= SFG_MAX_LANE_RECS) return -SFG_ST_LANE_RECS;
-  LRec& r = L.rec[L.nrec];
-  r.slot_start = sbase(sp) + off;
-  r.slot_end = r.slot_start + slot;
-  r.base = r.slot_start + rz;
-  r.size = size;
-  r.phys = phys;
-  r.id = -(++L.nalloc);
-  r.label = (int16_t)label;
-  r.space = (uint8_t)sp;
-  r.flags = R_RES;
-  return L.nrec++;
-}
-
-// free (device_memory.py:442-487); returns 0 ok, 1 invalid free, -status fatal
-SFG_DEV int lane_free(const sfg_prog& P, Lane& L, int64_t addr) {
-  const int sp = space_of(P, addr);
-  if (sp < 0) return 1;
-  int k = -1;
-  for (int j = 0; j < L.nrec; ++j)
-    if ((L.rec[j].flags & R_RES) && L.rec[j].space == sp && L.rec[j].base == addr) k = j;
-  if (k < 0 || (L.rec[k].flags & R_FREED)) return 1;
-  LRec& r = L.rec[k];
-  r.flags |= R_FREED;
-  if (L.nq >= kMaxQ) return -SFG_ST_LANE_RECS;
-  L.quar[L.nq++] = (int16_t)k;
-  L.qbytes[sp] += r.slot_end - r.slot_start;
-  while (L.qbytes[sp] > P.qcap[sp]) {  // _evict_one: first quarantined record of this space
-    int qi = 0;
-    while (qi < L.nq && L.rec[L.quar[qi]].space != sp) ++qi;
-    const int e = L.quar[qi];
-    for (int j = qi; j + 1 < L.nq; ++j) L.quar[j] = L.quar[j + 1];
-    --L.nq;
-    LRec& v = L.rec[e];
-    v.flags &= ~R_RES;
-    if (L.nfree >= kMaxFree) return -SFG_ST_LANE_RECS;
-    L.fl[L.nfree++] = sfg_free{v.slot_start - sbase(sp), v.slot_end - v.slot_start, sp, 0};
-    L.qbytes[sp] -= v.slot_end - v.slot_start;
-  }
-  return 0;
-}
-
-// ---------------------------------------------------------------------------
-// payload bytes
-
-struct Mem {
-  const ExecView* E;
-  uint8_t* work;               // this input's work region
-  const uint8_t* blob;
-  uint64_t* ov;                // this input's overlay entries
 };
-
-SFG_DEV uint8_t base_byte(const Mem& M, const Lane& L, const LRec& r, int64_t a) {
-  for (int k = L.nov - 1; k >= 0; --k) {
-    const uint64_t e = M.ov[k];
-    if ((int64_t)(e >> 8) == a) return (uint8_t)e;
-  }
-  return M.blob[r.phys + (a - r.base)];
-}
-
-SFG_DEV uint64_t mem_read(const Mem& M, const Lane& L, const LRec& r, int64_t a, int w) {
-  uint64_t v = 0;
-  if (!(r.flags & R_BASE)) {
-    const uint8_t* p = M.work + r.phys + (a - r.base);
-    if ((((uintptr_t)p) & (w - 1)) == 0) {
-      if (w == 4) return *reinterpret_cast<const uint32_t*>(p);
-      if (w == 8) return *reinterpret_cast<const uint64_t*>(p);
-      if (w == 2) return *reinterpret_cast<const uint16_t*>(p);
-      return *p;
-    }
-    for (int k = 0; k < w; ++k) v |= (uint64_t)p[k] << (8 * k);
-    return v;
-  }
-  for (int k = 0; k < w; ++k) v |= (uint64_t)base_byte(M, L, r, a + k) << (8 * k);
-  return v;
-}
-
-SFG_DEV bool mem_write(const Mem& M, Lane& L, const LRec& r, int64_t a, int w, uint64_t v) {
-  if (!(r.flags & R_BASE)) {
-    uint8_t* p = M.work + r.phys + (a - r.base);
-    if ((((uintptr_t)p) & (w - 1)) == 0) {
-      if (w == 4) *reinterpret_cast<uint32_t*>(p) = (uint32_t)v;
-      else if (w == 8) *reinterpret_cast<uint64_t*>(p) = v;
-      else if (w == 2) *reinterpret_cast<uint16_t*>(p) = (uint16_t)v;
-      else *p = (uint8_t)v;
-      return true;
-    }
-    for (int k = 0; k < w; ++k) p[k] = (uint8_t)(v >> (8 * k));
-    return true;
-  }
-  for (int k = 0; k < w; ++k) {
-    if (M.ov == nullptr || L.nov >= SFG_OVERLAY) return false;
-    M.ov[L.nov++] = ((uint64_t)(a + k) << 8) | ((v >> (8 * k)) & 0xFF);
-  }
-  return true;
-}
-
-// ---------------------------------------------------------------------------
-
-SFG_DEV void fill_report(sfg_verdict& V, const sfg_prog& P, const Lane& L, const Report& rep, int kernel,
-                         int iid, int ctaid, int tid, i128 a, int width, bool store, int space, int prov) {
-  V.status = SFG_ST_FINDING;
-  V.bug_class = rep.cls;
-  V.kernel = kernel;
-  V.iid = iid;
-  V.ctaid = ctaid;
-  V.tid = tid;
-  V.width = width;
-  V.shadow = rep.shadow;
-  V.addr_lo = (int64_t)(uint64_t)a;
-  V.addr_hi = (int64_t)(a >> 64);
-  V.is_store = store;
-  V.space = (uint8_t)(space < 0 ? 255 : space);
-  V.mech = (uint8_t)rep.mech;
-  V.prov = prov > 0 ? L.rec[prov - 1].id : 0;
-  if (rep.rec >= 0) {
-    const LRec& r = L.rec[rep.rec];
-    V.alloc = r.id;
-    V.label = r.label;
-    V.alloc_base = r.base;
-    V.alloc_size = r.size;
-    V.alloc_state = (r.flags & R_FREED) ? 1 : 0;
-  } else {
-    V.alloc = 0;
-    V.label = -1;
-    V.alloc_base = 0;
-    V.alloc_size = 0;
-    V.alloc_state = 255;
-  }
-  const int g = kernel < 0 ? P.total_ins : P.kernels[kernel].ins_base + iid;
-  const int site = rep.rec >= 0 ? L.rec[rep.rec].label : P.n_labels;
-  V.key = (rep.cls * (P.total_ins + 1) + g) * (P.n_labels + 1) + site;
-}
-
-// host copy check (sanitizer.py:190-196): declared space = the space the address lands in
-SFG_DEV bool host_check(const sfg_prog& P, const Lane& L, sfg_verdict& V, int64_t addr, int64_t width, bool store,
-                        int& hit) {
-  Report rep;
-  const int sp = space_of(P, addr);
-  const int decl = sp < 0 ? 0 : sp;
-  if (check_access(P, L, addr, width, decl, 0, rep, hit)) {
-    fill_report(V, P, L, rep, -1, -1, -1, -1, addr, (int)width, store, decl, 0);
-    return true;
-  }
-  return false;
-}
-
-SFG_DEV void edge_hit(uint32_t* ecnt, int e, bool& overflow) {
-  uint32_t* p = ecnt + e * 32 + (threadIdx.x & 31);
-  if (*p == 0xFFFFFFFFu) overflow = true; else ++*p;
-}
 
 }  // namespace
 
@@ -364,341 +216,21 @@ extern "C" __global__ void __launch_bounds__(128) sfg_execute_kernel(sfg_prog P,
   const size_t ins_bytes = ((size_t)P.total_ins * sizeof(sfg_ins) + 15) & ~(size_t)15;
   const size_t warp_bytes = (size_t)32 * (maxregs * 24 + P.n_edges * 4);
   uint8_t* wbase = smem + ins_bytes + (size_t)wib * warp_bytes;
-  uint64_t* s_alo = reinterpret_cast<uint64_t*>(wbase);                     // [reg][32]
-  uint32_t* s_r = reinterpret_cast<uint32_t*>(wbase + (size_t)32 * maxregs * 8);
-  uint32_t* s_f = s_r + 32 * maxregs;
-  int32_t* s_ahi = reinterpret_cast<int32_t*>(s_f + 32 * maxregs);
-  int32_t* s_ap = s_ahi + 32 * maxregs;
-  uint32_t* s_ecnt = reinterpret_cast<uint32_t*>(s_ap + 32 * maxregs);    // [edge][32]
+  InterpRunner R;
+  R.s_ins = s_ins;
+  R.s_alo = reinterpret_cast<uint64_t*>(wbase);
+  R.s_r = reinterpret_cast<uint32_t*>(wbase + (size_t)32 * maxregs * 8);
+  R.s_f = R.s_r + 32 * maxregs;
+  R.s_ahi = reinterpret_cast<int32_t*>(R.s_f + 32 * maxregs);
+  R.s_ap = R.s_ahi + 32 * maxregs;
+  R.s_ecnt = reinterpret_cast<uint32_t*>(R.s_ap + 32 * maxregs);
+  R.lane = lane;
+  R.n_edges = P.n_edges;
   __syncthreads();
-
   const int gw = blockIdx.x * nwb + wib;
   const int nw = gridDim.x * nwb;
   for (int base_i = gw * 32; base_i < E.n; base_i += nw * 32) {
     const int i = base_i + lane;
-    if (i >= E.n) continue;
-    const sfg_child& ch = E.children[i];
-    const sfg_val* cv = E.vals + (size_t)i * P.n_args;
-    Lane L;
-    Mem M{&E, E.work + E.work_base[i], E.base_blob,
-          E.overlay ? E.overlay + (size_t)i * SFG_OVERLAY : nullptr};
-    sfg_verdict V;
-    memset(&V, 0, sizeof(V));
-    V.status = SFG_ST_OK;
-    V.key = -1;
-    V.label = -1;
-    V.shadow = -1;
-    V.alloc_state = 255;
-    V.space = 255;
-    // baseline allocator state (the restored snapshot, device_memory.py:574-618)
-    L.nrec = P.n_base_recs;
-    for (int k = 0; k < P.n_base_recs; ++k) {
-      const sfg_rec& b = E.base_recs[k];
-      LRec& r = L.rec[k];
-      r.base = b.base; r.size = b.size; r.slot_start = b.slot_start; r.slot_end = b.slot_end;
-      r.phys = b.phys; r.id = b.id; r.label = b.label; r.space = b.space;
-      r.flags = (uint8_t)(R_BASE | (b.state ? R_FREED : 0) | (b.resident ? R_RES : 0));
-    }
-    L.nalloc = 0;
-    L.nov = 0;
-    L.nq = P.n_quar;
-    for (int k = 0; k < P.n_quar; ++k) L.quar[k] = (int16_t)P.quar[k];
-    L.nfree = P.n_free;
-    for (int k = 0; k < P.n_free; ++k) L.fl[k] = P.freel[k];
-    for (int s = 0; s < 3; ++s) { L.cursor[s] = P.cursor[s]; L.qbytes[s] = P.qbytes[s]; }
-    for (int k = 0; k < P.n_named; ++k) { L.named_addr[k] = P.named[k].addr; L.named_rec[k] = (int16_t)P.named[k].rec; }
-    for (int k = 0; k < P.n_args; ++k) L.mat_rec[k] = -1;
-    L.ro_cursor = 0;
-    for (int e = 0; e < P.n_edges; ++e) s_ecnt[e * 32 + lane] = 0;
-    bool ecnt_overflow = false;
-    uint64_t total_retired = 0;
-    uint8_t* ro = (P.diff_readback && E.readouts) ? E.readouts + E.readout_base[i] : nullptr;
-    const uint64_t arrays_end = ch.work_bytes - (uint64_t)P.named_work_bytes;
-
-    bool stop = false;
-    for (int h = 0; h < P.n_hostops && !stop; ++h) {
-      const sfg_hostop& op = E.hostops[h];
-      if (op.kind == SFG_H_SYNC) continue;
-      if (op.kind == SFG_H_ALLOC) {
-        if (op.size <= 0) { V.status = SFG_ST_ZERO_ALLOC; stop = true; break; }
-        const int64_t phys = (int64_t)arrays_end + op.work_off;
-        const int k = lane_alloc(P, L, op.space, op.size, op.label, phys);
-        if (k < 0) { V.status = -k; stop = true; break; }
-        for (int64_t b = 0; b < op.size; ++b) M.work[phys + b] = 0;
-        L.named_addr[op.buf] = L.rec[k].base;
-        L.named_rec[op.buf] = (int16_t)k;
-        continue;
-      }
-      if (op.kind == SFG_H_COPY_IN) {
-        const int64_t addr = L.named_addr[op.buf];
-        int64_t len = op.size;
-        const sfg_val* src_v = nullptr;
-        if (op.src_form == SFG_SRC_ARG) {
-          src_v = &cv[op.src_arg];
-          len = src_v->kind == SFG_V_ARR ? (int64_t)src_v->nbytes : 4;
-        }
-        if (len == 0) continue;
-        int hit = -1;
-        if (host_check(P, L, V, addr, len, true, hit)) { stop = true; break; }
-        const LRec& r = L.rec[hit];
-        for (int64_t b = 0; b < len; ++b) {
-          uint8_t byte = 0;
-          if (op.src_form == SFG_SRC_SEQ32) byte = (uint8_t)((uint32_t)(b >> 2) >> (8 * (b & 3)));
-          else if (op.src_form == SFG_SRC_HEX) byte = E.const_blob[op.blob_off + b];
-          else if (op.src_form == SFG_SRC_ARG) {
-            if (src_v->kind == SFG_V_ARR) {
-              // the child's pristine payload is the prefix of its work region, unless execution
-              // already wrote it; copy_in from an array arg reads the test-case value (campaign.py:508)
-              byte = M.work[src_v->data_off + b];
-            } else {
-              byte = (uint8_t)(src_v->bits >> (8 * b));
-            }
-          }
-          if (!mem_write(M, L, r, addr + b, 1, byte)) { V.status = SFG_ST_OVERLAY; stop = true; break; }
-        }
-        continue;
-      }
-      if (op.kind == SFG_H_COPY_OUT_NAMED || op.kind == SFG_H_COPY_OUT_ARG) {
-        int64_t addr, len;
-        if (op.kind == SFG_H_COPY_OUT_ARG) {
-          if (!P.diff_readback) continue;
-          if (L.mat_rec[op.arg_ref] < 0) continue;
-          addr = L.rec[L.mat_rec[op.arg_ref]].base;
-          len = cv[op.arg_ref].nbytes;
-        } else {
-          addr = L.named_addr[op.buf];
-          len = op.size;
-        }
-        if (len == 0) continue;
-        int hit = -1;
-        if (host_check(P, L, V, addr, len, false, hit)) { stop = true; break; }
-        if (ro != nullptr) {
-          const LRec& r = L.rec[hit];
-          for (int64_t b = 0; b < len; ++b) ro[L.ro_cursor + b] = (uint8_t)mem_read(M, L, r, addr + b, 1);
-          L.ro_cursor += (len + 15) & ~15ll;
-        }
-        continue;
-      }
-      if (op.kind == SFG_H_FREE) {
-        const int64_t addr = L.named_addr[op.buf];
-        const int res = lane_free(P, L, addr);
-        if (res < 0) { V.status = -res; stop = true; break; }
-        if (res == 1) {  // invalid_free_report (sanitizer.py:199-205)
-          const int sp = space_of(P, addr);
-          int r = sp >= 0 ? resolve_payload(L, sp, addr) : -1;
-          if (r < 0 && sp >= 0) r = resolve_slot(L, sp, addr);
-          Report rep{SFG_C_INVALID_FREE, SFG_MECH_REGISTRY, -1, r};
-          fill_report(V, P, L, rep, -1, -1, -1, -1, addr, 0, false, sp, 0);
-          stop = true;
-          break;
-        }
-        continue;
-      }
-      // ---- launch: bind arguments (campaign.py:452-479), materializing arrays lazily
-      const sfg_kernel& K = P.kernels[op.kernel];
-      uint32_t pre_r[SFG_MAX_ARGS], pre_f[SFG_MAX_ARGS];
-      int64_t pre_a[SFG_MAX_ARGS];
-      int32_t pre_ap[SFG_MAX_ARGS];
-      int nr = 0, nf = 0, na = 0;
-      for (int b = 0; b < op.n_bind && !stop; ++b) {
-        const sfg_binding& B = E.binds[op.bind_base + b];
-        if (B.form == SFG_B_LIT_I32) { pre_r[nr++] = (uint32_t)B.lit; continue; }
-        if (B.form == SFG_B_LIT_F32) { pre_f[nf++] = (uint32_t)B.lit; continue; }
-        if (B.form == SFG_B_BUF) {
-          pre_a[na] = L.named_addr[B.idx];
-          pre_ap[na++] = L.named_rec[B.idx] + 1;
-          continue;
-        }
-        const sfg_val& v = cv[B.idx];
-        if (v.kind == SFG_V_I32) { pre_r[nr++] = v.bits; continue; }
-        if (v.kind == SFG_V_F32) { pre_f[nf++] = sfg_quiet(v.bits); continue; }
-        if (L.mat_rec[B.idx] < 0) {
-          const int64_t size = (int64_t)sfg_mat_size(v);
-          const int k = lane_alloc(P, L, v.space, size, P.label_arg_base + B.idx, (int64_t)v.data_off);
-          if (k < 0) { V.status = -k; stop = true; break; }
-          L.mat_rec[B.idx] = (int16_t)k;
-        }
-        const LRec& r = L.rec[L.mat_rec[B.idx]];
-        pre_a[na] = r.base + v.base_offset;
-        pre_ap[na++] = L.mat_rec[B.idx] + 1;
-      }
-      if (stop) break;
-      V.entered |= 1u << op.kernel;
-      V.launches++;
-      const sfg_ins* kins = s_ins + K.ins_base;
-      const int regs = K.regs;
-      const int grid = op.grid, block = op.block;
-      for (int ctaid = 0; ctaid < grid && !stop; ++ctaid) {
-        for (int tid = 0; tid < block && !stop; ++tid) {
-          // make_thread (executor.py:191-202)
-          for (int q = 0; q < regs; ++q) {
-            s_r[q * 32 + lane] = q < nr ? pre_r[q] : 0u;
-            s_f[q * 32 + lane] = q < nf ? pre_f[q] : 0u;
-            s_alo[q * 32 + lane] = q < na ? (uint64_t)pre_a[q] : 0ull;
-            s_ahi[q * 32 + lane] = q < na ? (pre_a[q] < 0 ? -1 : 0) : 0;
-            s_ap[q * 32 + lane] = q < na ? pre_ap[q] : 0;
-          }
-          uint32_t preds = 0;
-          int pc = 0;
-          uint64_t retired = 0;
-          while (true) {
-            const sfg_ins I = kins[pc];
-            ++retired;
-            if (I.op == SFG_EXIT) break;
-            if (I.op == SFG_BRA) {
-              bool taken = true;
-              if (I.flags & SFG_F_PRED) taken = (((preds >> I.s1) & 1u) != 0) != ((I.flags & SFG_F_PNEG) != 0);
-              edge_hit(s_ecnt, taken ? I.edge_tk : I.edge_ft, ecnt_overflow);
-              pc = taken ? I.target : pc + 1;
-              if (retired >= P.budget) { V.status = SFG_ST_BUDGET; stop = true; break; }
-              continue;
-            }
-            switch (I.op) {
-              case SFG_LD:
-              case SFG_ST: {
-                const i128 areg = ((i128)s_ahi[I.s1 * 32 + lane] << 64) | (i128)s_alo[I.s1 * 32 + lane];
-                const i128 a = areg + (i128)I.imm2;
-                const int prov = s_ap[I.s1 * 32 + lane];
-                const bool st = I.op == SFG_ST;
-                Report rep;
-                int hit = -1;
-                if (check_access(P, L, a, I.width, I.space, prov, rep, hit)) {
-                  fill_report(V, P, L, rep, op.kernel, pc, ctaid, tid, a, I.width, st, I.space, prov);
-                  stop = true;
-                  break;
-                }
-                const LRec& r = L.rec[hit];
-                const int64_t aa = (int64_t)a;
-                if (st) {
-                  uint64_t val;
-                  if (I.mode == SFG_MK_F32) val = (I.flags & SFG_F_S2_IMM) ? (uint64_t)(uint32_t)I.imm1 : s_f[I.s2 * 32 + lane];
-                  else if (I.mode == SFG_MK_B64) val = s_alo[I.s2 * 32 + lane];
-                  else val = (I.flags & SFG_F_S2_IMM) ? (uint64_t)I.imm1 : (uint64_t)s_r[I.s2 * 32 + lane];
-                  if (!mem_write(M, L, r, aa, I.width, val)) { V.status = SFG_ST_OVERLAY; stop = true; }
-                } else {
-                  const uint64_t val = mem_read(M, L, r, aa, I.width);
-                  switch (I.mode) {
-                    case SFG_MK_F32: s_f[I.dst * 32 + lane] = sfg_quiet((uint32_t)val); break;
-                    case SFG_MK_B64:
-                      s_alo[I.dst * 32 + lane] = val;
-                      s_ahi[I.dst * 32 + lane] = 0;
-                      s_ap[I.dst * 32 + lane] = 0;
-                      break;
-                    default: s_r[I.dst * 32 + lane] = (uint32_t)val; break;  // b8/b16 zero-extend, b32 bits
-                  }
-                }
-                break;
-              }
-              case SFG_MOV:
-                if (I.mode == SFG_CLS_R) {
-                  s_r[I.dst * 32 + lane] = (I.flags & SFG_F_S1_IMM) ? (uint32_t)I.imm1 : s_r[I.s1 * 32 + lane];
-                } else if (I.mode == SFG_CLS_F) {
-                  s_f[I.dst * 32 + lane] = (I.flags & SFG_F_S1_IMM) ? (uint32_t)I.imm1 : s_f[I.s1 * 32 + lane];
-                } else if (I.mode == SFG_CLS_A) {
-                  if (I.flags & SFG_F_S1_IMM) {
-                    s_alo[I.dst * 32 + lane] = (uint64_t)I.imm1;
-                    s_ahi[I.dst * 32 + lane] = (I.flags & SFG_F_U64IMM) ? 0 : (I.imm1 < 0 ? -1 : 0);
-                    s_ap[I.dst * 32 + lane] = 0;
-                  } else {
-                    s_alo[I.dst * 32 + lane] = s_alo[I.s1 * 32 + lane];
-                    s_ahi[I.dst * 32 + lane] = s_ahi[I.s1 * 32 + lane];
-                    s_ap[I.dst * 32 + lane] = s_ap[I.s1 * 32 + lane];
-                  }
-                } else {
-                  preds = (preds & ~(1u << I.dst)) | (((preds >> I.s1) & 1u) << I.dst);
-                }
-                break;
-              case SFG_ADD:
-              case SFG_SUB:
-              case SFG_MUL:
-                if (I.mode == SFG_CLS_A) {
-                  const i128 base = ((i128)s_ahi[I.s1 * 32 + lane] << 64) | (i128)s_alo[I.s1 * 32 + lane];
-                  const int64_t d = (I.flags & SFG_F_S2_IMM) ? I.imm2 : (int64_t)(int32_t)s_r[I.s2 * 32 + lane];
-                  const i128 res = I.op == SFG_ADD ? base + (i128)d : base - (i128)d;
-                  s_alo[I.dst * 32 + lane] = (uint64_t)res;
-                  s_ahi[I.dst * 32 + lane] = (int32_t)(int64_t)(res >> 64);
-                  s_ap[I.dst * 32 + lane] = s_ap[I.s1 * 32 + lane];
-                } else {
-                  const uint32_t x = (I.flags & SFG_F_S1_IMM) ? (uint32_t)I.imm1 : s_r[I.s1 * 32 + lane];
-                  const uint32_t y = (I.flags & SFG_F_S2_IMM) ? (uint32_t)I.imm2 : s_r[I.s2 * 32 + lane];
-                  s_r[I.dst * 32 + lane] = I.op == SFG_ADD ? x + y : (I.op == SFG_SUB ? x - y : x * y);
-                }
-                break;
-              case SFG_FADD:
-              case SFG_FSUB:
-              case SFG_FMUL: {
-                const uint32_t x = (I.flags & SFG_F_S1_IMM) ? (uint32_t)I.imm1 : s_f[I.s1 * 32 + lane];
-                const uint32_t y = (I.flags & SFG_F_S2_IMM) ? (uint32_t)I.imm2 : s_f[I.s2 * 32 + lane];
-                s_f[I.dst * 32 + lane] = sfg_fop(I.op, x, y);
-                break;
-              }
-              case SFG_SETP: {
-                bool res;
-                if (I.flags & SFG_F_FLOAT) {
-                  const float x = sfg_f((I.flags & SFG_F_S1_IMM) ? (uint32_t)I.imm1 : s_f[I.s1 * 32 + lane]);
-                  const float y = sfg_f((I.flags & SFG_F_S2_IMM) ? (uint32_t)I.imm2 : s_f[I.s2 * 32 + lane]);
-                  switch (I.mode) {
-                    case SFG_CMP_EQ: res = x == y; break;
-                    case SFG_CMP_NE: res = x != y; break;
-                    case SFG_CMP_LT: res = x < y; break;
-                    case SFG_CMP_LE: res = x <= y; break;
-                    case SFG_CMP_GT: res = x > y; break;
-                    default: res = x >= y; break;
-                  }
-                } else {
-                  const int64_t x = (I.flags & SFG_F_S1_IMM) ? I.imm1 : (int64_t)(int32_t)s_r[I.s1 * 32 + lane];
-                  const int64_t y = (I.flags & SFG_F_S2_IMM) ? I.imm2 : (int64_t)(int32_t)s_r[I.s2 * 32 + lane];
-                  switch (I.mode) {
-                    case SFG_CMP_EQ: res = x == y; break;
-                    case SFG_CMP_NE: res = x != y; break;
-                    case SFG_CMP_LT: res = x < y; break;
-                    case SFG_CMP_LE: res = x <= y; break;
-                    case SFG_CMP_GT: res = x > y; break;
-                    default: res = x >= y; break;
-                  }
-                }
-                preds = (preds & ~(1u << I.dst)) | ((uint32_t)res << I.dst);
-                break;
-              }
-              case SFG_CVT:
-                if (I.mode == SFG_CVT_F_FROM_I) {
-                  s_f[I.dst * 32 + lane] = (I.flags & SFG_F_S1_IMM)
-                                               ? (uint32_t)I.imm1
-                                               : sfg_b(__int2float_rn((int32_t)s_r[I.s1 * 32 + lane]));
-                } else if (I.flags & SFG_F_S1_IMM) {
-                  s_r[I.dst * 32 + lane] = (uint32_t)I.imm1;
-                } else {  // cvt_f32_to_i32 (executor.py:51-65)
-                  const uint32_t fb = s_f[I.s1 * 32 + lane];
-                  const float fv = sfg_f(fb);
-                  int32_t out;
-                  if (sfg_isnan_bits(fb)) out = 0;
-                  else if (fv >= 2147483647.0f) out = 2147483647;
-                  else if (fv <= -2147483648.0f) out = (int32_t)0x80000000u;
-                  else out = __float2int_rn(fv);
-                  s_r[I.dst * 32 + lane] = (uint32_t)out;
-                }
-                break;
-              default: {  // SREG
-                const int v = I.mode == SFG_SR_TID ? tid : I.mode == SFG_SR_NTID ? block
-                            : I.mode == SFG_SR_CTAID ? ctaid : grid;
-                s_r[I.dst * 32 + lane] = (uint32_t)v;
-                break;
-              }
-            }
-            if (stop) break;
-            if (I.edge_ft >= 0) edge_hit(s_ecnt, I.edge_ft, ecnt_overflow);
-            ++pc;
-            if (retired >= P.budget) { V.status = SFG_ST_BUDGET; stop = true; break; }
-          }
-          total_retired += retired;
-        }
-      }
-    }
-    if (ecnt_overflow && V.status < SFG_ST_OUT_OF_SPACE) V.status = SFG_ST_COUNTER;
-    V.retired = total_retired;
-    V.allocs = L.nalloc;
-    E.verdicts[i] = V;
-    uint32_t* erow = E.edge_counts + (size_t)i * P.n_edges;
-    for (int e = 0; e < P.n_edges; ++e) erow[e] = s_ecnt[e * 32 + lane];
+    if (i < E.n) run_input(P, E, i, R);
   }
 }

@@ -1,0 +1,445 @@
+// SIR -> CUDA C++ specialization of K3, compiled with NVRTC for sm_100a when a
+// program is created (the GPU analogue of the paper's instrument-at-load step,
+// PAPER.md §3; semantics of executor.py:210-424 preserved instruction by
+// instruction).
+//
+// Per simulated kernel the generator emits one device function in which
+//   * every simulated register is a C++ local (r/f: u32 bits, a: 128-bit signed
+//     value + provenance tag, p: bool) -> lives in hardware registers,
+//   * every basic block is a label; control flow is goto; each static edge's
+//     hit counter is a compile-time slot of the runner (registers),
+//   * the retired-instruction budget is charged once per block on the fast
+//     path; a block that could reach the budget branches to a slow copy that
+//     charges and checks per instruction (executor.py:411-415 exactly),
+//   * ld/st go through the exec_core sanitizer, with a fast path when static
+//     provenance analysis proves the base register carries a pointer
+//     parameter's tag and the access lies inside that record's live payload.
+// The host-op driver, allocator and sanitizer are exec_core.cuh, shared with
+// the generic interpreter (execute.cu).
+#include <nvrtc.h>
+
+#include <cstdio>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "embedded.inc"  // generated at build time: kEmbeddedNames / kEmbeddedSources / kEmbeddedCount
+
+namespace sfgjit {
+
+enum { TAG_BOT = -2, TAG_TOP = -1, TAG_NONE = 0 };  // q+1 = pointer param q
+
+struct KInfo {
+  int base, n, regs, nr, nf, na;
+};
+
+static std::string hex64(int64_t v) {
+  char b[40];
+  snprintf(b, sizeof b, "0x%llxull", (unsigned long long)v);
+  return b;
+}
+
+static std::string u32lit(int64_t v) {
+  char b[24];
+  snprintf(b, sizeof b, "0x%08xu", (unsigned)(uint32_t)v);
+  return b;
+}
+
+static std::string i64lit(int64_t v) {
+  char b[48];
+  if (v == INT64_MIN) return "(-9223372036854775807ll - 1)";
+  snprintf(b, sizeof b, "(%lldll)", (long long)v);
+  return b;
+}
+
+// blocks: leaders are 0, branch targets and successors of bra/exit (kernel_ir.py:364-401)
+static std::vector<int> block_starts(const sfg_ins* I, int n) {
+  std::vector<char> lead(n + 1, 0);
+  lead[0] = 1;
+  for (int i = 0; i < n; ++i) {
+    if (I[i].op == SFG_BRA) {
+      lead[I[i].target] = 1;
+      if (i + 1 < n) lead[i + 1] = 1;
+    } else if (I[i].op == SFG_EXIT && i + 1 < n) {
+      lead[i + 1] = 1;
+    }
+  }
+  std::vector<int> s;
+  for (int i = 0; i < n; ++i)
+    if (lead[i]) s.push_back(i);
+  return s;
+}
+
+static int meet(int a, int b) {
+  if (a == TAG_BOT) return b;
+  if (b == TAG_BOT) return a;
+  return a == b ? a : TAG_TOP;
+}
+
+// forward dataflow of a-register provenance tags (static when a param's tag reaches)
+static std::vector<std::vector<int>> tag_flow(const sfg_ins* I, int n, const KInfo& K,
+                                              const std::vector<int>& starts, std::vector<int>& blk_of) {
+  const int nb = (int)starts.size();
+  blk_of.assign(n, 0);
+  for (int b = 0; b < nb; ++b) {
+    const int e = b + 1 < nb ? starts[b + 1] : n;
+    for (int i = starts[b]; i < e; ++i) blk_of[i] = b;
+  }
+  std::vector<std::vector<int>> in(nb, std::vector<int>(K.regs, TAG_BOT));
+  for (int q = 0; q < K.regs; ++q) in[0][q] = q < K.na ? q + 1 : TAG_NONE;
+  std::vector<std::vector<int>> at(n, std::vector<int>(K.regs, TAG_BOT));  // state before instruction
+  bool changed = true;
+  while (changed) {
+    changed = false;
+    for (int b = 0; b < nb; ++b) {
+      std::vector<int> st = in[b];
+      const int e = b + 1 < nb ? starts[b + 1] : n;
+      for (int i = starts[b]; i < e; ++i) {
+        at[i] = st;
+        const sfg_ins& x = I[i];
+        if (x.op == SFG_MOV && x.mode == SFG_CLS_A) st[x.dst] = (x.flags & SFG_F_S1_IMM) ? TAG_NONE : st[x.s1];
+        else if ((x.op == SFG_ADD || x.op == SFG_SUB) && x.mode == SFG_CLS_A) st[x.dst] = st[x.s1];
+        else if (x.op == SFG_LD && x.mode == SFG_MK_B64) st[x.dst] = TAG_NONE;
+      }
+      auto flow = [&](int succ) {
+        for (int q = 0; q < K.regs; ++q) {
+          const int m = meet(in[succ][q], st[q]);
+          if (m != in[succ][q]) { in[succ][q] = m; changed = true; }
+        }
+      };
+      const sfg_ins& last = I[e - 1];
+      if (last.op == SFG_EXIT) continue;
+      if (last.op == SFG_BRA) {
+        flow(blk_of[last.target]);
+        if ((last.flags & SFG_F_PRED) && e < n) flow(blk_of[e]);
+      } else if (e < n) {
+        flow(blk_of[e]);
+      }
+    }
+  }
+  return at;
+}
+
+struct Gen {
+  const sfg_prog& P;
+  const sfg_ins* ins;
+  std::ostringstream o;
+  bool edge_ovf_checks;
+
+  explicit Gen(const sfg_prog& p, const sfg_ins* i) : P(p), ins(i) {}
+
+  std::string r(int i) { return "r" + std::to_string(i); }
+  std::string f(int i) { return "f" + std::to_string(i); }
+  std::string a(int i) { return "a" + std::to_string(i); }
+  std::string t(int i) { return "t" + std::to_string(i); }
+  std::string p(int i) { return "p" + std::to_string(i); }
+
+  std::string edge(int e) {
+    if (e < 0) return "";
+    if (edge_ovf_checks) return "if (++J.ec[" + std::to_string(e) + "] == 0u) J.ovf = true; ";
+    return "++J.ec[" + std::to_string(e) + "]; ";
+  }
+
+  // retire-adjust string for stops inside a block: fast path adds j+1, slow path already counted
+  static std::string radj(bool slow, int j) { return slow ? "" : "ret += " + std::to_string(j + 1) + "; "; }
+
+  void emit_mem(const sfg_ins& x, int kidx, int iid, int j, bool slow, int tag) {
+    const int W = x.width;
+    const bool st = x.op == SFG_ST;
+    o << "    { const i128 A_ = " << a(x.s1) << " + (i128)" << i64lit(x.imm2) << "; const int64_t lo_ = (int64_t)A_;\n";
+    std::string val;
+    if (st) {
+      if (x.mode == SFG_MK_F32) val = (x.flags & SFG_F_S2_IMM) ? std::string("(uint64_t)") + u32lit(x.imm1) : "(uint64_t)" + f(x.s2);
+      else if (x.mode == SFG_MK_B64) val = "(uint64_t)" + a(x.s2);
+      else val = (x.flags & SFG_F_S2_IMM) ? "(uint64_t)" + hex64(x.imm1) : "(uint64_t)" + r(x.s2);
+      o << "      const uint64_t sv_ = " << val << ";\n";
+    } else {
+      o << "      uint64_t v_;\n";
+    }
+    const std::string W_s = std::to_string(W), SP = std::to_string(x.space);
+    auto fast = [&](int q) {
+      const std::string Q = std::to_string(q);
+      return "(pok" + Q + " && psp" + Q + " == " + SP + " && (i128)lo_ == A_ && lo_ >= pb" + Q + " && lo_ + " + W_s +
+             " <= pe" + Q + ")";
+    };
+    auto fast_body = [&](int q) {
+      const std::string Q = std::to_string(q);
+      if (st) return "st_work(pp" + Q + " + (lo_ - pb" + Q + "), " + W_s + ", sv_);";
+      return "v_ = ld_work(pp" + Q + " + (lo_ - pb" + Q + "), " + W_s + ");";
+    };
+    std::string slow_path =
+        "{ Report rep_; int rh_ = -1;\n"
+        "        if (check_access(P, L, A_, " + W_s + ", " + SP + ", " + t(x.s1) + ", rep_, rh_)) { fill_report(V, P, L, rep_, " +
+        std::to_string(kidx) + ", " + std::to_string(iid) + ", ctaid, tid, A_, " + W_s + ", " + (st ? "true" : "false") +
+        ", " + SP + ", " + t(x.s1) + "); " + radj(slow, j) + "rc = RUN_FINDING; goto done; }\n";
+    if (st)
+      slow_path += "        if (!mem_write(M, L, L.rec[rh_], lo_, " + W_s + ", sv_)) { V.status = SFG_ST_OVERLAY; " +
+                   radj(slow, j) + "rc = RUN_FATAL; goto done; } }";
+    else
+      slow_path += "        v_ = mem_read(M, L, L.rec[rh_], lo_, " + W_s + "); }";
+    if (tag > 0) {
+      o << "      if " << fast(tag - 1) << " { " << fast_body(tag - 1) << " }\n      else " << slow_path << "\n";
+    } else if (tag == TAG_TOP) {
+      std::string pre = "      ";
+      for (int q = 0; q < cur_na; ++q) {
+        o << pre << "if (" << t(x.s1) << " == pt" << q << " && " << fast(q) << ") { " << fast_body(q) << " }\n";
+        pre = "      else ";
+      }
+      o << pre << slow_path << "\n";
+    } else {
+      o << "      " << slow_path << "\n";
+    }
+    if (!st) {
+      if (x.mode == SFG_MK_F32) o << "      " << f(x.dst) << " = sfg_quiet((uint32_t)v_);\n";
+      else if (x.mode == SFG_MK_B64) o << "      " << a(x.dst) << " = (i128)(uint64_t)v_; " << t(x.dst) << " = 0;\n";
+      else o << "      " << r(x.dst) << " = (uint32_t)v_;\n";
+    }
+    o << "    }\n";
+  }
+
+  int cur_na = 0;
+
+  std::string src_r(const sfg_ins& x, int slot) {
+    const bool imm = slot == 1 ? (x.flags & SFG_F_S1_IMM) : (x.flags & SFG_F_S2_IMM);
+    const int64_t v = slot == 1 ? x.imm1 : x.imm2;
+    return imm ? u32lit(v) : r(slot == 1 ? x.s1 : x.s2);
+  }
+  std::string src_f(const sfg_ins& x, int slot) {
+    const bool imm = slot == 1 ? (x.flags & SFG_F_S1_IMM) : (x.flags & SFG_F_S2_IMM);
+    const int64_t v = slot == 1 ? x.imm1 : x.imm2;
+    return imm ? u32lit(v) : f(slot == 1 ? x.s1 : x.s2);
+  }
+  std::string src_i64(const sfg_ins& x, int slot) {
+    const bool imm = slot == 1 ? (x.flags & SFG_F_S1_IMM) : (x.flags & SFG_F_S2_IMM);
+    const int64_t v = slot == 1 ? x.imm1 : x.imm2;
+    return imm ? i64lit(v) : "(int64_t)(int32_t)" + r(slot == 1 ? x.s1 : x.s2);
+  }
+
+  static const char* cmp(int m) {
+    static const char* c[] = {"==", "!=", "<", "<=", ">", ">="};
+    return c[m];
+  }
+
+  // one non-control instruction (everything except BRA/EXIT); j = index in block
+  void emit_plain(const sfg_ins& x, int kidx, int iid, int j, bool slow, int tag) {
+    switch (x.op) {
+      case SFG_MOV:
+        if (x.mode == SFG_CLS_R) o << "    " << r(x.dst) << " = " << src_r(x, 1) << ";\n";
+        else if (x.mode == SFG_CLS_F) o << "    " << f(x.dst) << " = " << src_f(x, 1) << ";\n";
+        else if (x.mode == SFG_CLS_A) {
+          if (x.flags & SFG_F_S1_IMM) {
+            if (x.flags & SFG_F_U64IMM) o << "    " << a(x.dst) << " = (i128)(uint64_t)" << hex64(x.imm1) << "; ";
+            else o << "    " << a(x.dst) << " = (i128)" << i64lit(x.imm1) << "; ";
+            o << t(x.dst) << " = 0;\n";
+          } else {
+            o << "    " << a(x.dst) << " = " << a(x.s1) << "; " << t(x.dst) << " = " << t(x.s1) << ";\n";
+          }
+        } else {
+          o << "    " << p(x.dst) << " = " << p(x.s1) << ";\n";
+        }
+        break;
+      case SFG_ADD:
+      case SFG_SUB:
+      case SFG_MUL: {
+        const char* opc = x.op == SFG_ADD ? "+" : x.op == SFG_SUB ? "-" : "*";
+        if (x.mode == SFG_CLS_A) {
+          o << "    " << a(x.dst) << " = " << a(x.s1) << " " << opc << " (i128)" << src_i64(x, 2) << "; " << t(x.dst)
+            << " = " << t(x.s1) << ";\n";
+        } else {
+          o << "    " << r(x.dst) << " = (uint32_t)(" << src_r(x, 1) << " " << opc << " " << src_r(x, 2) << ");\n";
+        }
+        break;
+      }
+      case SFG_FADD:
+      case SFG_FSUB:
+      case SFG_FMUL:
+        o << "    " << f(x.dst) << " = sfg_fop(" << (int)x.op << ", " << src_f(x, 1) << ", " << src_f(x, 2) << ");\n";
+        break;
+      case SFG_SETP:
+        if (x.flags & SFG_F_FLOAT)
+          o << "    " << p(x.dst) << " = sfg_f(" << src_f(x, 1) << ") " << cmp(x.mode) << " sfg_f(" << src_f(x, 2) << ");\n";
+        else
+          o << "    " << p(x.dst) << " = " << src_i64(x, 1) << " " << cmp(x.mode) << " " << src_i64(x, 2) << ";\n";
+        break;
+      case SFG_CVT:
+        if (x.mode == SFG_CVT_F_FROM_I) {
+          if (x.flags & SFG_F_S1_IMM) o << "    " << f(x.dst) << " = " << u32lit(x.imm1) << ";\n";
+          else o << "    " << f(x.dst) << " = sfg_b(__int2float_rn((int32_t)" << r(x.s1) << "));\n";
+        } else {
+          if (x.flags & SFG_F_S1_IMM) o << "    " << r(x.dst) << " = " << u32lit(x.imm1) << ";\n";
+          else o << "    " << r(x.dst) << " = sfg_cvt_f2i(" << f(x.s1) << ");\n";
+        }
+        break;
+      case SFG_SREG: {
+        static const char* names[] = {"tid", "block", "ctaid", "grid"};
+        o << "    " << r(x.dst) << " = (uint32_t)" << names[x.mode] << ";\n";
+        break;
+      }
+      case SFG_LD:
+      case SFG_ST:
+        emit_mem(x, kidx, iid, j, slow, tag);
+        break;
+      default:
+        break;
+    }
+  }
+
+  void emit_kernel(int kidx) {
+    const sfg_kernel& KD = P.kernels[kidx];
+    KInfo K{KD.ins_base, KD.n_ins, KD.regs, 0, 0, 0};
+    for (int q = 0; q < KD.n_params; ++q) {
+      if (KD.ptype[q] == 0) ++K.nr;
+      else if (KD.ptype[q] == 1) ++K.nf;
+      else ++K.na;
+    }
+    cur_na = K.na;
+    const sfg_ins* I = ins + K.base;
+    const std::vector<int> starts = block_starts(I, K.n);
+    std::vector<int> blk_of;
+    const auto tags = tag_flow(I, K.n, K, starts, blk_of);
+    const int nb = (int)starts.size();
+
+    o << "static __device__ __forceinline__ int sim_" << kidx
+      << "(JitRunner& J, const sfg_prog& P, Lane& L, Mem& M, sfg_verdict& V, const Pre& pre, int ctaid, int tid, "
+         "int grid, int block, uint64_t& total) {\n";
+    for (int q = 0; q < K.regs; ++q) {
+      o << "  uint32_t " << r(q) << " = " << (q < K.nr ? "pre.r[" + std::to_string(q) + "]" : std::string("0u"))
+        << ", " << f(q) << " = " << (q < K.nf ? "pre.f[" + std::to_string(q) + "]" : std::string("0u")) << ";\n";
+      o << "  i128 " << a(q) << " = " << (q < K.na ? "(i128)pre.a[" + std::to_string(q) + "]" : std::string("0"))
+        << "; int32_t " << t(q) << " = " << (q < K.na ? "pre.ap[" + std::to_string(q) + "]" : std::string("0"))
+        << "; bool " << p(q) << " = false;\n";
+    }
+    for (int q = 0; q < K.na; ++q) {
+      const std::string Q = std::to_string(q);
+      o << "  const int32_t pt" << Q << " = pre.ap[" << Q << "];\n";
+      o << "  int64_t pb" << Q << " = 0, pe" << Q << " = 0; int psp" << Q << " = -1; bool pok" << Q
+        << " = false; uint8_t* pp" << Q << " = M.work;\n";
+      o << "  if (pt" << Q << " > 0) { const LRec& R_ = L.rec[pt" << Q << " - 1]; pb" << Q << " = R_.base; pe" << Q
+        << " = R_.base + R_.size; psp" << Q << " = R_.space; pok" << Q
+        << " = (R_.flags & (R_RES | R_FREED | R_BASE)) == R_RES; pp" << Q << " = M.work + R_.phys; }\n";
+    }
+    o << "  uint64_t ret = 0; int rc = RUN_EXIT; const uint64_t BUD = P.budget;\n";
+    o << "  (void)grid; (void)block; (void)ctaid; (void)tid;\n";
+    for (int b = 0; b < nb; ++b) {
+      const int s0 = starts[b], e = b + 1 < nb ? starts[b + 1] : K.n;
+      const int len = e - s0;
+      const sfg_ins& last = I[e - 1];
+      const int checked = last.op == SFG_EXIT ? len - 1 : len;
+      for (int pass = 0; pass < 2; ++pass) {
+        const bool slow = pass == 1;
+        o << (slow ? "S" : "B") << b << ":\n";
+        if (!slow && checked > 0) o << "  if (ret + " << checked << "ull >= BUD) goto S" << b << ";\n";
+        if (!slow && checked == 0) {
+          // a lone exit: nothing to check, the slow copy is identical
+        }
+        for (int i = s0; i < e; ++i) {
+          const sfg_ins& x = I[i];
+          const int j = i - s0;
+          if (slow) o << "  ++ret;\n";
+          if (x.op == SFG_EXIT) {
+            if (!slow) o << "  ret += " << len << ";\n";
+            o << "  goto done;\n";
+            break;
+          }
+          if (x.op == SFG_BRA) {
+            const std::string tgt = std::to_string(blk_of[x.target]);
+            const std::string nxt = std::to_string(i + 1 < K.n ? blk_of[i + 1] : 0);
+            const std::string bud = slow ? "if (ret >= BUD) { rc = RUN_BUDGET; goto done; } " : "ret += " + std::to_string(len) + "; ";
+            if (x.flags & SFG_F_PRED) {
+              const std::string cond = std::string(x.flags & SFG_F_PNEG ? "!" : "") + p(x.s1);
+              o << "  if (" << cond << ") { " << edge(x.edge_tk) << bud << "goto B" << tgt << "; }\n";
+              o << "  else { " << edge(x.edge_ft) << bud << "goto B" << nxt << "; }\n";
+            } else {
+              o << "  " << edge(x.edge_tk) << bud << "goto B" << tgt << ";\n";
+            }
+            break;
+          }
+          emit_plain(x, kidx, i, j, slow, tags[i][x.op == SFG_LD || x.op == SFG_ST ? x.s1 : 0]);
+          if (i == e - 1) {  // block ends by falling through into the next leader
+            o << "  " << edge(x.edge_ft);
+            if (slow) o << "if (ret >= BUD) { rc = RUN_BUDGET; goto done; } ";
+            else o << "ret += " << len << "; ";
+            o << "goto B" << blk_of[i + 1] << ";\n";
+          } else if (slow) {
+            o << "  if (ret >= BUD) { rc = RUN_BUDGET; goto done; }\n";
+          }
+        }
+      }
+    }
+    o << "done:\n  total += ret;\n  return rc;\n}\n\n";
+  }
+
+  std::string run(int n_edges, uint64_t max_edge_events) {
+    edge_ovf_checks = max_edge_events >= 0xFFFFFFFFull;
+    const int NE = n_edges > 0 ? n_edges : 1;
+    o << "#include \"exec_core.cuh\"\n\nnamespace {\n\n";
+    o << "struct JitRunner {\n  uint32_t ec[" << NE << "];\n  bool ovf;\n"
+      << "  SFG_DEV void begin_input() {\n#pragma unroll\n    for (int e = 0; e < " << NE << "; ++e) ec[e] = 0u;\n    ovf = false;\n  }\n"
+      << "  SFG_DEV void flush(uint32_t* row, bool& o) {\n#pragma unroll\n    for (int e = 0; e < " << n_edges
+      << "; ++e) row[e] = ec[e];\n    o = ovf;\n  }\n"
+      << "  SFG_DEV int run_thread(const sfg_prog& P, int k, Lane& L, Mem& M, sfg_verdict& V, const Pre& pre, int ctaid, "
+         "int tid, int grid, int block, uint64_t& total);\n};\n\n";
+    for (int k = 0; k < P.n_kernels; ++k) emit_kernel(k);
+    o << "SFG_DEV int JitRunner::run_thread(const sfg_prog& P, int k, Lane& L, Mem& M, sfg_verdict& V, const Pre& pre, "
+         "int ctaid, int tid, int grid, int block, uint64_t& total) {\n  switch (k) {\n";
+    for (int k = 0; k < P.n_kernels; ++k)
+      o << "    case " << k << ": return sim_" << k << "(*this, P, L, M, V, pre, ctaid, tid, grid, block, total);\n";
+    o << "    default: return RUN_FATAL;\n  }\n}\n\n}  // namespace\n\n";
+    o << "extern \"C\" __global__ void __launch_bounds__(128) sfg_jit_execute(sfg_prog P, ExecView E) {\n"
+         "  JitRunner R;\n"
+         "  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < E.n; i += gridDim.x * blockDim.x) run_input(P, E, i, R);\n"
+         "}\n";
+    return o.str();
+  }
+};
+
+}  // namespace sfgjit
+
+// Generate and compile; on success `cubin` holds the sm_100a image.  Returns 0 on success.
+static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_edge_events, std::string& source,
+                           std::string& log, std::vector<char>& cubin) {
+  sfgjit::Gen g(P, ins);
+  source = g.run(P.n_edges, max_edge_events);
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, source.c_str(), "sfg_jit.cu", kEmbeddedCount, kEmbeddedSources, kEmbeddedNames) !=
+      NVRTC_SUCCESS) {
+    log = "nvrtcCreateProgram failed";
+    return 1;
+  }
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false", "-default-device",
+                        "-lineinfo", "-DSFG_JIT=1", "--device-int128"};
+  const nvrtcResult cr = nvrtcCompileProgram(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
+  size_t lsz = 0;
+  nvrtcGetProgramLogSize(prog, &lsz);
+  log.assign(lsz, '\0');
+  if (lsz) nvrtcGetProgramLog(prog, &log[0]);
+  if (cr != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    return 2;
+  }
+  size_t csz = 0;
+  nvrtcGetCUBINSize(prog, &csz);
+  cubin.resize(csz);
+  nvrtcGetCUBIN(prog, cubin.data());
+  nvrtcDestroyProgram(&prog);
+  return 0;
+}
+
+// Generate, compile and load the specialized execute kernel.  Returns 0 on success.
+static int sfg_jit_build(const sfg_prog& P, const sfg_ins* ins, uint64_t max_edge_events, std::string& source,
+                         std::string& log, cudaLibrary_t* lib_out, cudaKernel_t* kern_out) {
+  std::vector<char> cubin;
+  const int rc = sfg_jit_compile(P, ins, max_edge_events, source, log, cubin);
+  if (rc) return rc;
+  cudaError_t e = cudaLibraryLoadData(lib_out, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+  if (e != cudaSuccess) {
+    log += std::string("\ncudaLibraryLoadData: ") + cudaGetErrorString(e);
+    return 3;
+  }
+  e = cudaLibraryGetKernel(kern_out, *lib_out, "sfg_jit_execute");
+  if (e != cudaSuccess) {
+    log += std::string("\ncudaLibraryGetKernel: ") + cudaGetErrorString(e);
+    return 4;
+  }
+  return 0;
+}

@@ -4,7 +4,19 @@
 //
 // Everything is plain-old-data, little-endian, naturally aligned.
 #pragma once
+#ifdef __CUDACC_RTC__
+typedef signed char int8_t;
+typedef short int16_t;
+typedef int int32_t;
+typedef long long int64_t;
+typedef unsigned char uint8_t;
+typedef unsigned short uint16_t;
+typedef unsigned int uint32_t;
+typedef unsigned long long uint64_t;
+typedef unsigned long uintptr_t;
+#else
 #include <stdint.h>
+#endif
 
 #define SFG_ABI_VERSION 1
 

@@ -73,7 +73,7 @@ class DeviceCampaign:
     def __init__(self, manifest, *, master_seed=1, mem: MemConfig | None = None,
                  mutation: MutationConfig | None = None, budget=1_000_000, window=256, recent_weight=4.0,
                  diff_readback=False, stop_on_first_finding=False, stop_bug_class=None, device=None,
-                 extra_seeds=()):
+                 extra_seeds=(), ids_reset_per_input=False):
         if not torch.cuda.is_available():
             raise _native.NativeError("no CUDA device: the fuzzing inner loop runs only on the GPU")
         self.L = _native.lib()
@@ -113,6 +113,7 @@ class DeviceCampaign:
         self.entered = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.counts_base = torch.zeros(max(self.C, 1), dtype=torch.int64, device=self.dev)
         self.next_alloc_id = self.base.next_id
+        self.ids_reset = ids_reset_per_input   # reinit mode: every input gets a fresh image
         self.findings = FindingsLog()
         self.key_strings: dict[int, str] = {}
         # corpus (device) + host mirror
@@ -221,6 +222,15 @@ class DeviceCampaign:
                                           self.r_tmp.data_ptr(), self.r_tot.data_ptr() + 8 * total_slot,
                                           _stream()), "scan")
 
+    def new_worker(self):
+        """Reference workers (campaign.py:712-730) get a fresh MutationSchedule and a fresh
+        image: rotation counts and alloc ids restart; corpus/findings/coverage are shared."""
+        self.counts_base.zero_()
+        self.next_alloc_id = self.base.next_id
+
+    def _id_base(self, prefix: int) -> int:
+        return self.base.next_id if self.ids_reset else self._round_id0 + prefix
+
     # ---- one round ---------------------------------------------------------------------
     def run_round(self, it0: int, n: int) -> RoundResult:
         L, hp, s = self.L, self.h, _stream()
@@ -288,11 +298,11 @@ class DeviceCampaign:
             self._raise_fatal(fatal)
         executed = n if stop == U32_NONE else stop + 1
         n_adm = int(tot[2])
-        id_base = self.next_alloc_id
+        self._round_id0 = self.next_alloc_id
         if n_adm:
             self._admit(n, n_adm)
         _native.check(L.sfg_commit(hp, self.edge_total.data_ptr(), self.ghit.data_ptr(), s), "commit")
-        new_keys = self._absorb_findings(it0, id_base)
+        new_keys = self._absorb_findings(it0)
         self.next_alloc_id += int(tot[3])
         if stop == U32_NONE and self.C:
             self.counts_base[:self.C] += self.r_tot[8:8 + self.C]
@@ -349,7 +359,7 @@ class DeviceCampaign:
             tc = TestCase(args, int(meta[j]["rng_seed"]), parent_tc.id, ops)
             self.host_entries.append((tc, int(meta[j]["admitted_iteration"]), False))
 
-    def _absorb_findings(self, it0, id_base):
+    def _absorb_findings(self, it0):
         kc = self.r_kcount.cpu().numpy()
         hot = np.nonzero(kc)[0]
         if not len(hot):
@@ -369,7 +379,7 @@ class DeviceCampaign:
             vt = _np(self.r_verdicts.view(-1, VERDICT.itemsize)[idx].reshape(-1), VERDICT)
             ap = self.r_allocs_prefix[idx].cpu().numpy()
             for j, (i, k) in enumerate(fresh):
-                rep = decode_verdict(vt[j], self.low, it0 + i, id_base + int(ap[j]))
+                rep = decode_verdict(vt[j], self.low, it0 + i, self._id_base(int(ap[j])))
                 self.key_strings[k] = rep.dedupe_key
                 self.findings.add_many(rep, int(kc[k]))
                 out.append((i, rep))
@@ -428,40 +438,15 @@ class DeviceCampaign:
         ecnt = self.r_ecnt[:n * max(self.E, 1)].cpu().numpy().view(np.uint32).reshape(n, max(self.E, 1))
         admit = self.r_admit[:n].cpu().numpy()
         aprefix = self.r_allocs_prefix[:n].cpu().numpy()
-        # regenerate every child's pristine payload with the product kernel
-        sizes = [sum((int(v["nbytes"]) + 15) // 16 * 16 for v in vals[i * self.n_args:(i + 1) * self.n_args]
-                     if v["kind"] == 2) for i in range(n)]
-        offs = np.zeros(n * self.n_args, np.uint64)
-        cur = 0
-        for i in range(n):
-            for a in range(self.n_args):
-                v = vals[i * self.n_args + a]
-                if v["kind"] == 2:
-                    offs[i * self.n_args + a] = cur
-                    cur += (int(v["nbytes"]) + 15) // 16 * 16
-        dst = self._u8(cur + 16)
-        sel = torch.arange(n, dtype=torch.int32, device=self.dev)
-        doff = torch.from_numpy(offs.view(np.int64)).to(self.dev)
-        cd = self.corpus_dev()
-        _native.check(self.L.sfg_regen(self.h, ctypes.byref(cd), n, sel.data_ptr(), self.r_children.data_ptr(),
-                                       self.r_vals.data_ptr(), doff.data_ptr(), dst.data_ptr(), s), "regen")
-        data = dst.cpu().numpy().tobytes()
+        tcs = self.child_testcases(list(range(n)))
         recs = []
-        id_round = self.next_alloc_id - int(self.r_allocs[:n].sum().item())
         for i in range(n):
-            row = vals[i * self.n_args:(i + 1) * self.n_args].copy()
-            for a in range(self.n_args):
-                if row[a]["kind"] == 2:
-                    row[a]["data_off"] = offs[i * self.n_args + a]
-            args = unpack_values(row, data)
             c = chld[i]
             p = int(c["parent"])
-            parent_id = None if p < 0 else self.host_entries[p][0].id
-            tc = TestCase(args, int(c["rng_seed"]), parent_id,
-                          tuple(decode_op(c["ops"][k]) for k in range(int(c["n_ops"]))))
+            tc = tcs[i]
             v = verd[i]
             st = int(v["status"])
-            rep = decode_verdict(v, self.low, int(c["it"]), id_round + int(aprefix[i])) if st == ST_FINDING else None
+            rep = decode_verdict(v, self.low, int(c["it"]), self._id_base(int(aprefix[i]))) if st == ST_FINDING else None
             edges = {}
             for e in np.nonzero(ecnt[i][:self.E])[0]:
                 name, (a, b) = self.low.edge_names[e]
@@ -472,6 +457,49 @@ class DeviceCampaign:
                          "edges": {k: sorted(x) for k, x in edges.items()},
                          "report": rep.to_line() if rep else None, "admitted": bool(admit[i])})
         return recs
+
+    def child_testcases(self, idx):
+        """Reference TestCase objects for round inputs ``idx``: payloads regenerated
+        on the device from (parent, ops) with the product kernel, then decoded."""
+        n = len(idx)
+        if n == 0:
+            return []
+        s = _stream()
+        sel_np = np.asarray(idx, np.int32)
+        vals = _np(self.r_vals.view(-1, VAL.itemsize * self.n_args)[torch.from_numpy(sel_np).long().to(self.dev)]
+                   .reshape(-1), VAL)
+        chld = _np(self.r_children.view(-1, CHILD.itemsize)[torch.from_numpy(sel_np).long().to(self.dev)]
+                   .reshape(-1), CHILD)
+        offs = np.zeros(n * self.n_args, np.uint64)
+        cur = 0
+        for j in range(n):
+            for a in range(self.n_args):
+                v = vals[j * self.n_args + a]
+                if v["kind"] == 2:
+                    offs[j * self.n_args + a] = cur
+                    cur += (int(v["nbytes"]) + 15) // 16 * 16
+        dst = self._u8(cur + 16)
+        sel = torch.from_numpy(sel_np).to(self.dev)
+        doff = torch.from_numpy(offs.view(np.int64)).to(self.dev)
+        cd = self.corpus_dev()
+        self.launches += 1
+        _native.check(self.L.sfg_regen(self.h, ctypes.byref(cd), n, sel.data_ptr(), self.r_children.data_ptr(),
+                                       self.r_vals.data_ptr(), doff.data_ptr(), dst.data_ptr(), s), "regen")
+        data = dst.cpu().numpy().tobytes()
+        out = []
+        for j in range(n):
+            row = vals[j * self.n_args:(j + 1) * self.n_args].copy()
+            for a in range(self.n_args):
+                if row[a]["kind"] == 2:
+                    row[a]["data_off"] = offs[j * self.n_args + a]
+            c = chld[j]
+            p = int(c["parent"])
+            if p < 0:
+                out.append(self.seed_tc)
+                continue
+            out.append(TestCase(unpack_values(row, data), int(c["rng_seed"]), self.host_entries[p][0].id,
+                                tuple(decode_op(c["ops"][k]) for k in range(int(c["n_ops"])))))
+        return out
 
     # ---- one-shot execution of given test cases (execute_once analogue) -------------------
     def execute_testcases(self, tcs, iteration0: int = 0):
