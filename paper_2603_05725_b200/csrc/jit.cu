@@ -19,6 +19,8 @@
 #include <nvrtc.h>
 
 #include <cstdio>
+#include <map>
+#include <mutex>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -400,6 +402,17 @@ static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_e
                            std::string& log, std::vector<char>& cubin) {
   sfgjit::Gen g(P, ins);
   source = g.run(P.n_edges, max_edge_events);
+  // process-wide cache: identical programs (same generated source) compile once
+  static std::mutex mu;
+  static std::map<std::string, std::vector<char>> cache;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(source);
+    if (it != cache.end()) {
+      cubin = it->second;
+      return 0;
+    }
+  }
   nvrtcProgram prog;
   if (nvrtcCreateProgram(&prog, source.c_str(), "sfg_jit.cu", kEmbeddedCount, kEmbeddedSources, kEmbeddedNames) !=
       NVRTC_SUCCESS) {
@@ -422,6 +435,8 @@ static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_e
   cubin.resize(csz);
   nvrtcGetCUBIN(prog, cubin.data());
   nvrtcDestroyProgram(&prog);
+  std::lock_guard<std::mutex> lk(mu);
+  cache[source] = cubin;
   return 0;
 }
 

@@ -134,3 +134,20 @@ def _encode_for_test(o, op):
             o["imask"] = int(p["inner_mask"], 0)
         elif inner == "float_byte":
             o["ibyte"], o["imask"] = int(p["inner_byte"]), int(p["inner_mask"])
+
+
+@pytest.mark.parametrize("name", bench_names() + ["matmul", "vadd"])
+def test_jit_source_compiles_for_sm100a(name):
+    """The specialized execute kernel (SIR -> CUDA C++) NVRTC-compiles for sm_100a."""
+    import sys
+    sys.path.insert(0, str(_native.PKG.parent / "tools"))
+    from jit_check import check
+    if name in ("matmul", "vadd"):
+        from paper_2603_05725_b200.workloads import load
+        m = load(name)
+    else:
+        m = bench_manifest(name)
+    rc, cubin_bytes, text = check(m)
+    assert rc == 0, text[:2000]
+    assert cubin_bytes > 0
+    assert "sfg_jit_execute" in text
