@@ -13,6 +13,8 @@ struct sfg_program {
   sfg_prog P;
   cudaLibrary_t jit_lib = nullptr;    // specialized execute kernel (jit.cu), if built
   cudaKernel_t jit_kernel = nullptr;
+  int* jit_next = nullptr;            // persistent-kernel work counter
+  int jit_grid = 0;                   // resident CTAs (occupancy x SMs)
   std::string jit_source, jit_log;
   sfg_ins* ins;
   sfg_hostop* hostops;
@@ -156,6 +158,17 @@ int sfg_program_create(const void* prog, size_t prog_bytes, const void* ins, siz
       sfg_program_destroy(p);
       return 1;
     }
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)p->jit_kernel, 128, 0);
+    if (e != cudaSuccess || per_sm < 1) per_sm = 1;
+    p->jit_grid = sms * per_sm;
+    e = cudaMalloc((void**)&p->jit_next, sizeof(int));
+    if (e != cudaSuccess) {
+      sfg_program_destroy(p);
+      return fail("sfg_program_create: jit counter", e);
+    }
   }
   e = cudaFuncSetAttribute(sfg_execute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem);
   if (e != cudaSuccess) {
@@ -178,6 +191,7 @@ int sfg_program_update(sfg_program* p, const void* prog, size_t prog_bytes) {
 void sfg_program_destroy(sfg_program* p) {
   if (!p) return;
   if (p->jit_lib) cudaLibraryUnload(p->jit_lib);
+  if (p->jit_next) cudaFree(p->jit_next);
   cudaFree(p->ins);
   cudaFree(p->hostops);
   cudaFree(p->binds);
@@ -263,9 +277,12 @@ int sfg_execute(const sfg_program* p, int n, const void* children, const void* v
                 (const sfg_child*)children, (const sfg_val*)vals, work_base, work,
                 (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, overlay, n};
   if (p->jit_kernel) {
-    void* args[] = {(void*)&p->P, (void*)&E};
-    const cudaError_t e = cudaLaunchKernel((const void*)p->jit_kernel, dim3(blocks_for(n, 128)), dim3(128), args, 0,
-                                           S(stream));
+    cudaError_t e = cudaMemsetAsync(p->jit_next, 0, sizeof(int), S(stream));
+    if (e != cudaSuccess) return fail("sfg_execute (jit counter)", e);
+    int* next = p->jit_next;
+    void* args[] = {(void*)&p->P, (void*)&E, (void*)&next};
+    const unsigned grid = blocks_for(n, 128) < (unsigned)p->jit_grid ? blocks_for(n, 128) : (unsigned)p->jit_grid;
+    e = cudaLaunchKernel((const void*)p->jit_kernel, dim3(grid), dim3(128), args, 0, S(stream));
     if (e != cudaSuccess) return fail("sfg_execute (jit)", e);
     return 0;
   }

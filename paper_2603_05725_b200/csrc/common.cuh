@@ -11,24 +11,31 @@
 
 SFG_DEV float sfg_f(uint32_t b) { return __uint_as_float(b); }
 SFG_DEV uint32_t sfg_b(float f) { return __float_as_uint(f); }
-SFG_DEV bool sfg_isnan_bits(uint32_t b) { return (b & 0x7F800000u) == 0x7F800000u && (b & 0x007FFFFFu); }
+SFG_DEV bool sfg_isnan_bits(uint32_t b) { return (b & 0x7FFFFFFFu) > 0x7F800000u; }
+
+// NaN result of a binary32 op under the reference's host rules: the first NaN
+// operand wins and is quieted; an invalid op (inf-inf, 0*inf) gives 0xFFC00000.
+__device__ __noinline__ uint32_t sfg_fop_nan(uint32_t a, uint32_t b) {
+  if (sfg_isnan_bits(a)) return a | 0x00400000u;
+  if (sfg_isnan_bits(b)) return b | 0x00400000u;
+  return 0xFFC00000u;
+}
 
 // binary32 add/sub/mul with the reference's host semantics: the value equals
 // IEEE RNE (double rounding of a single f32 op is innocuous), NaN results
 // follow x86-64 SSE as exhibited through ctypes.c_float (executor.py:42-44,
-// 319-330): first NaN operand wins and is quieted, invalid ops give 0xFFC00000.
+// 319-330).  A non-NaN result implies non-NaN operands, so the common path is
+// one op and one compare.
 SFG_DEV uint32_t sfg_fop(int op, uint32_t a, uint32_t b) {
-  if (sfg_isnan_bits(a)) return a | 0x00400000u;
-  if (sfg_isnan_bits(b)) return b | 0x00400000u;
   float r;
   if (op == SFG_FADD) r = __fadd_rn(sfg_f(a), sfg_f(b));
   else if (op == SFG_FSUB) r = __fsub_rn(sfg_f(a), sfg_f(b));
   else r = __fmul_rn(sfg_f(a), sfg_f(b));
-  const uint32_t rb = sfg_b(r);
-  return sfg_isnan_bits(rb) ? 0xFFC00000u : rb;
+  if (r == r) return sfg_b(r);
+  return sfg_fop_nan(a, b);
 }
 
-SFG_DEV uint32_t sfg_quiet(uint32_t b) { return sfg_isnan_bits(b) ? (b | 0x00400000u) : b; }
+SFG_DEV uint32_t sfg_quiet(uint32_t b) { return b | (sfg_isnan_bits(b) ? 0x00400000u : 0u); }
 
 // read-only views of the device corpus (entries at round start)
 struct CorpusView {

@@ -159,15 +159,19 @@ struct Gen {
       o << "      uint64_t v_;\n";
     }
     const std::string W_s = std::to_string(W), SP = std::to_string(x.space);
+    // fast path: tagged live own record of the declared space, access inside its payload
+    // and naturally aligned in the work region (phys offsets are 16-aligned)
     auto fast = [&](int q) {
       const std::string Q = std::to_string(q);
-      return "(pok" + Q + " && psp" + Q + " == " + SP + " && (i128)lo_ == A_ && lo_ >= pb" + Q + " && lo_ + " + W_s +
-             " <= pe" + Q + ")";
+      return "(pk" + Q + "_" + SP + " && (i128)lo_ == A_ && (uint64_t)(lo_ - pb" + Q + ") <= (uint64_t)(psz" + Q + " - " +
+             W_s + ") && psz" + Q + " >= " + W_s + " && ((lo_ - pb" + Q + ") & " + std::to_string(W - 1) + ") == 0)";
     };
     auto fast_body = [&](int q) {
       const std::string Q = std::to_string(q);
-      if (st) return "st_work(pp" + Q + " + (lo_ - pb" + Q + "), " + W_s + ", sv_);";
-      return "v_ = ld_work(pp" + Q + " + (lo_ - pb" + Q + "), " + W_s + ");";
+      const char* T = W == 1 ? "uint8_t" : W == 2 ? "uint16_t" : W == 4 ? "uint32_t" : "uint64_t";
+      const std::string ptr = std::string("reinterpret_cast<") + (st ? "" : "const ") + T + "*>(pp" + Q + " + (lo_ - pb" + Q + "))";
+      if (st) return "*" + ptr + " = (" + T + ")sv_;";
+      return "v_ = *" + ptr + ";";
     };
     std::string slow_path =
         "{ Report rep_; int rh_ = -1;\n"
@@ -314,11 +318,13 @@ struct Gen {
     for (int q = 0; q < K.na; ++q) {
       const std::string Q = std::to_string(q);
       o << "  const int32_t pt" << Q << " = pre.ap[" << Q << "];\n";
-      o << "  int64_t pb" << Q << " = 0, pe" << Q << " = 0; int psp" << Q << " = -1; bool pok" << Q
+      o << "  int64_t pb" << Q << " = 0, psz" << Q << " = 0; int psp" << Q << " = -1; bool pok" << Q
         << " = false; uint8_t* pp" << Q << " = M.work;\n";
-      o << "  if (pt" << Q << " > 0) { const LRec& R_ = L.rec[pt" << Q << " - 1]; pb" << Q << " = R_.base; pe" << Q
-        << " = R_.base + R_.size; psp" << Q << " = R_.space; pok" << Q
+      o << "  if (pt" << Q << " > 0) { const LRec& R_ = L.rec[pt" << Q << " - 1]; pb" << Q << " = R_.base; psz" << Q
+        << " = R_.size; psp" << Q << " = R_.space; pok" << Q
         << " = (R_.flags & (R_RES | R_FREED | R_BASE)) == R_RES; pp" << Q << " = M.work + R_.phys; }\n";
+      o << "  const bool pk" << Q << "_0 = pok" << Q << " && psp" << Q << " == 0, pk" << Q << "_1 = pok" << Q << " && psp"
+        << Q << " == 1, pk" << Q << "_2 = pok" << Q << " && psp" << Q << " == 2;\n";
     }
     o << "  uint64_t ret = 0; int rc = RUN_EXIT; const uint64_t BUD = P.budget;\n";
     o << "  (void)grid; (void)block; (void)ctaid; (void)tid;\n";
@@ -387,9 +393,11 @@ struct Gen {
     for (int k = 0; k < P.n_kernels; ++k)
       o << "    case " << k << ": return sim_" << k << "(*this, P, L, M, V, pre, ctaid, tid, grid, block, total);\n";
     o << "    default: return RUN_FATAL;\n  }\n}\n\n}  // namespace\n\n";
-    o << "extern \"C\" __global__ void __launch_bounds__(128) sfg_jit_execute(sfg_prog P, ExecView E) {\n"
+    // persistent: every lane fetches its next input independently, so a long input
+    // never holds a whole block's resources while its warp-mates sit idle
+    o << "extern \"C\" __global__ void __launch_bounds__(128, 1) sfg_jit_execute(sfg_prog P, ExecView E, int* next) {\n"
          "  JitRunner R;\n"
-         "  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < E.n; i += gridDim.x * blockDim.x) run_input(P, E, i, R);\n"
+         "  for (int i = atomicAdd(next, 1); i < E.n; i = atomicAdd(next, 1)) run_input(P, E, i, R);\n"
          "}\n";
     return o.str();
   }
@@ -420,7 +428,7 @@ static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_e
     return 1;
   }
   const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false", "-default-device",
-                        "-lineinfo", "-DSFG_JIT=1", "--device-int128"};
+                        "-lineinfo", "-DSFG_JIT=1", "--device-int128", "--maxrregcount=255"};
   const nvrtcResult cr = nvrtcCompileProgram(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
   size_t lsz = 0;
   nvrtcGetProgramLogSize(prog, &lsz);
