@@ -71,6 +71,7 @@ class CampaignConfig:
     diff_readback: bool = False
     hooks: object = None
     round_size: int = 65536
+    pipeline_depth: int = 8
     device: str | None = None
 
 
@@ -158,31 +159,39 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
             dc.new_worker()   # fresh rotation counts + alloc ids (one image per worker)
             if config.mode == "amortized":
                 init_runs += 1
-            it = rng_.start
-            while it < rng_.stop:
-                if deadline is not None and time.perf_counter() > deadline:
-                    stop_reason = "wall_clock"
-                    break
-                n = min(config.round_size, rng_.stop - it)
-                before = len(dc.host_entries)
-                res = dc.run_round(it, n)
+            state = {"stop": None}
+
+            def on_round(res):
+                nonlocal executed, init_runs, term_runs
                 executed += res.executed
                 if config.mode == "reinit":
                     init_runs += res.executed
                     term_runs += res.executed
                 if out_dir is not None:
-                    for tc, _, _ in dc.host_entries[before:]:
+                    for tc, _, _ in dc.host_entries[on_round.mirrored:]:
                         _write_corpus_entry(out_dir, tc, specs)
+                    on_round.mirrored = len(dc.host_entries)
                     if res.new_keys:
-                        tcs = dc.child_testcases([i for i, _ in res.new_keys])
+                        tcs = dc.child_testcases([i for i, _ in res.new_keys], res.slot)
                         for (i, rep), tc in zip(res.new_keys, tcs):
                             _write_crash(out_dir, rep, tc, specs, manifest)
                 if res.stop is not None:
                     want = config.stop_bug_class
-                    stop_reason = ("first_finding" if config.stop_on_first_finding else
-                                   f"bug_class:{getattr(want, 'value', want)}")
+                    state["stop"] = ("first_finding" if config.stop_on_first_finding else
+                                     f"bug_class:{getattr(want, 'value', want)}")
+
+            on_round.mirrored = len(dc.host_entries)
+            it = rng_.start
+            while it < rng_.stop and state["stop"] is None:
+                if deadline is not None and time.perf_counter() > deadline:
+                    stop_reason = "wall_clock"
                     break
-                it += n
+                # bounded chunks so the wall-clock check runs between batches of rounds
+                chunk_stop = min(rng_.stop, it + config.round_size * config.pipeline_depth)
+                dc.run_rounds(it, chunk_stop, config.round_size, depth=config.pipeline_depth, on_round=on_round)
+                it = chunk_stop
+            if state["stop"] is not None:
+                stop_reason = state["stop"]
             if config.mode == "amortized":
                 term_runs += 1
     except CampaignFatalError:

@@ -1,19 +1,27 @@
-"""Device round driver: one batched round of the fuzzing inner loop on a GPU.
+"""Device round driver: batched rounds of the fuzzing inner loop on a GPU.
 
 A *round* is R consecutive fuzz inputs ``it0 .. it0+R-1`` of the batched-round
 contract: every input schedules a parent from the corpus as it
 stood at the round start, mutates with its own Philox stream, executes its
 COMPUTE phase on the post-INIT baseline, and is absorbed in ``it`` order.
 All of it runs as stream-ordered kernels from ``libsfg_b200.so``; torch only
-holds device memory and provides the stream.  Host work per round: three
-small device->host reads (work-arena size, stop/fatal/admission scalars,
-dedupe-key table) and building reference-typed objects for the (rare) new
-findings and admitted children.
+holds device memory and provides streams and events.
+
+Round pipelining.  A round's mutation depends on earlier rounds only through
+corpus admissions (rotation counts depend on draws only; alloc ids are
+applied on the host).  ``run_rounds`` therefore keeps ``depth`` rounds in
+flight on separate streams, each mutated from the corpus as of its
+submission; rounds are finalized (triaged) strictly in order, and when a
+round admits a child or stops the campaign every later in-flight round is
+re-submitted (or dropped).  The results are identical to running the rounds
+one after another; the long-running inputs of one round (the round time is
+bounded below by its longest input) overlap with the bulk of the next ones.
 """
 
 from __future__ import annotations
 
 import ctypes
+from collections import deque
 from dataclasses import dataclass
 
 import numpy as np
@@ -23,12 +31,13 @@ from . import _native
 from .baseline import MemConfig, OutOfSpaceError, build_baseline, record_table
 from .coverage import CoverageMap
 from .findings import FindingsLog
-from .lowering import (CHILD, ENTRY, KEYBASE, ST_COUNTER, ST_FINDING, ST_LANE_RECS, ST_OUT_OF_SPACE, ST_OVERLAY,
+from .lowering import (CHILD, ENTRY, ST_COUNTER, ST_FINDING, ST_LANE_RECS, ST_OUT_OF_SPACE, ST_OVERLAY,
                        ST_ZERO_ALLOC, VAL, VERDICT, Lowered, LoweringError, decode_op, decode_verdict,
                        pack_values, unpack_values)
 from .testcase import MutationError, TestCase
 
 U32_NONE = 0xFFFFFFFF
+STATUS = {0: "ok", 1: "finding", 2: "budget"}
 
 
 class CorpusDev(ctypes.Structure):
@@ -48,25 +57,63 @@ class DeviceFatal(Exception):
     pass
 
 
-def _ptr(t: torch.Tensor | None) -> int | None:
+def _ptr(t):
     return None if t is None else t.data_ptr()
-
-
-def _stream() -> int:
-    return torch.cuda.current_stream().cuda_stream
 
 
 def _np(t: torch.Tensor, dtype) -> np.ndarray:
     return t.detach().cpu().numpy().view(dtype)
 
 
-class RoundResult:
-    """Device buffers + host scalars of one executed round."""
+def _align16(n: int) -> int:
+    return (n + 15) // 16 * 16
 
-    def __init__(self, it0, n, stop, executed, admitted, new_keys):
+
+class RoundResult:
+    """Host-side outcome of one finalized round."""
+
+    def __init__(self, it0, n, stop, executed, admitted, new_keys, slot):
         self.it0, self.n, self.stop, self.executed = it0, n, stop, executed
         self.n_admitted = admitted
-        self.new_keys = new_keys
+        self.new_keys = new_keys          # [(round index, BugReport)] for keys first seen here
+        self.slot = slot
+
+
+class Slot:
+    """Device buffers + stream of one in-flight round."""
+
+    def __init__(self, dc: "DeviceCampaign", cap: int):
+        dev = dc.dev
+        C, E, A = max(dc.C, 1), max(dc.E, 1), dc.n_args
+        i64 = lambda m: torch.empty(max(m, 1), dtype=torch.int64, device=dev)  # noqa: E731
+        i32 = lambda m: torch.empty(max(m, 1), dtype=torch.int32, device=dev)  # noqa: E731
+        u8 = lambda m: torch.empty(max(m, 16), dtype=torch.uint8, device=dev)  # noqa: E731
+        self.cap = cap
+        self.stream = torch.cuda.Stream(device=dev)
+        self.parent, self.picks, self.flags, self.prefix = i32(cap), u8(cap * 3), i32(cap * C), i64(cap * C)
+        self.children, self.vals = u8(cap * CHILD.itemsize), u8(cap * A * VAL.itemsize)
+        self.work_base, self.ro_base = i64(cap), i64(cap)
+        self.verdicts, self.ecnt = u8(cap * VERDICT.itemsize), i32(cap * E)
+        self.overlay = i64(cap * 32) if dc.low.overlay else None
+        self.allocs, self.allocs_prefix, self.admit, self.pos = i64(cap), i64(cap), i64(cap), i64(cap)
+        self.bytes, self.boff, self.sel, self.dst_off = i64(cap), i64(cap), i32(cap), i64(cap * A)
+        self.tmp, self.tot, self.scalars = i64((cap + 2047) // 2048 + 8), i64(16), i32(2)
+        self.first, self.kfirst, self.kcount = i32(E), i32(dc.K), i64(dc.K)
+        self.counts_base = torch.zeros(C, dtype=torch.int64, device=dev)
+        self.pin_tot = torch.empty(16, dtype=torch.int64, pin_memory=True)
+        self.pin_sc = torch.empty(2, dtype=torch.int32, pin_memory=True)
+        self.work, self.work_cap = None, 0
+        self.readouts = None
+        self.ev_counts = torch.cuda.Event()
+        self.ev_done = torch.cuda.Event()
+        self.exec_ev = None
+        self.it0 = self.n = 0
+        self.round_index = -1
+
+    def ensure_work(self, nbytes: int, dev):
+        if nbytes > self.work_cap:
+            self.work_cap = int(nbytes * 1.1) + 4096
+            self.work = torch.empty(self.work_cap, dtype=torch.uint8, device=dev)
 
 
 class DeviceCampaign:
@@ -90,6 +137,7 @@ class DeviceCampaign:
         self.low = Lowered(manifest, self.base, mem=self.mem, mutation=self.mutation, master_seed=master_seed,
                            budget=budget, window=window, recent_weight=recent_weight,
                            diff_readback=diff_readback, stop_first=stop_on_first_finding, stop_class=stop_class)
+        self.diff = bool(diff_readback)
         self.specs = manifest.argspecs
         self.n_args = len(self.specs)
         self.C = len(self.low.int_args)
@@ -107,33 +155,32 @@ class DeviceCampaign:
             self.low.const_blob, len(self.low.const_blob), self.blob.data_ptr(), ctypes.byref(h)),
             "sfg_program_create")
         self.h = h
+        self.jit = self.L.sfg_program_jit_source(self.h, None, 0) > 0
         # global campaign state on device
         self.edge_total = torch.zeros(max(self.E, 1), dtype=torch.int64, device=self.dev)
         self.ghit = torch.zeros(max(self.E, 1), dtype=torch.uint8, device=self.dev)
         self.entered = torch.zeros(1, dtype=torch.int32, device=self.dev)
-        self.counts_base = torch.zeros(max(self.C, 1), dtype=torch.int64, device=self.dev)
+        self.counts_run = torch.zeros(max(self.C, 1), dtype=torch.int64, device=self.dev)
         self.next_alloc_id = self.base.next_id
         self.ids_reset = ids_reset_per_input   # reinit mode: every input gets a fresh image
         self.findings = FindingsLog()
-        self.key_strings: dict[int, str] = {}
+        self.key_strings: dict = {}
         # corpus (device) + host mirror
-        self.cap = 0
-        self.data_cap = 0
-        self.n_corpus = 0
-        self.corpus_bytes = 0
+        self.cap = self.data_cap = self.n_corpus = self.corpus_bytes = 0
+        self.max_entry_work = 0
         self.host_entries: list = []     # (TestCase, admitted_iteration, is_seed)
         seeds = [self.seed_tc] + list(extra_seeds)
-        self._grow_corpus(max(64, len(seeds) * 2), 1 << 16)
         self._upload_seeds(seeds)
         self.n_seeds = len(seeds)
-        self._round_cap = 0
-        self._work_cap = 0
+        self.slots: list[Slot] = []
+        self._last_done = None           # event: previous round finalized
+        self._last_counts = None         # event: counts_run valid for the next submission
         self.rounds = 0
-        self.launches = 0          # kernels launched through the C ABI (bench evidence)
-        self.timing = False        # record CUDA events around the execute kernel
-        self.last_exec_events = None
+        self.launches = 0                # kernels launched through the C ABI (bench evidence)
+        self.timing = False              # record CUDA events around each execute kernel
+        self.exec_events: list = []
 
-    # ---- buffers ---------------------------------------------------------------------
+    # ---- corpus ---------------------------------------------------------------------
     def _u8(self, n):
         return torch.empty(max(int(n), 16), dtype=torch.uint8, device=self.dev)
 
@@ -141,22 +188,32 @@ class DeviceCampaign:
         cap, data_cap = max(cap, self.cap), max(data_cap, self.data_cap)
         if cap == self.cap and data_cap == self.data_cap:
             return
-        meta = self._u8(cap * ENTRY.itemsize)
-        vals = self._u8(cap * self.n_args * VAL.itemsize)
-        chld = self._u8(cap * CHILD.itemsize)
-        data = self._u8(data_cap)
+        torch.cuda.synchronize(self.dev)  # in-flight rounds may still read the old buffers
+        meta, vals = self._u8(cap * ENTRY.itemsize), self._u8(cap * self.n_args * VAL.itemsize)
+        chld, data = self._u8(cap * CHILD.itemsize), self._u8(data_cap)
         if self.cap:
-            meta[:self.cap * ENTRY.itemsize].copy_(self.c_meta[:self.cap * ENTRY.itemsize])
-            vals[:self.cap * self.n_args * VAL.itemsize].copy_(self.c_vals[:self.cap * self.n_args * VAL.itemsize])
-            chld[:self.cap * CHILD.itemsize].copy_(self.c_child[:self.cap * CHILD.itemsize])
-            data[:self.data_cap].copy_(self.c_data[:self.data_cap])
+            for new, old, nb in ((meta, self.c_meta, self.cap * ENTRY.itemsize),
+                                 (vals, self.c_vals, self.cap * self.n_args * VAL.itemsize),
+                                 (chld, self.c_child, self.cap * CHILD.itemsize), (data, self.c_data, self.data_cap)):
+                new[:nb].copy_(old[:nb])
         self.c_meta, self.c_vals, self.c_child, self.c_data = meta, vals, chld, data
         self.cap, self.data_cap = cap, data_cap
 
+    def _entry_work_bound(self, vals) -> int:
+        """Upper bound of a child's work-region bytes given its parent's values: the
+        array mutations at most double an array (array_dim), or set 4*count
+        (array_extreme), so bound each array by max(2*nbytes, 8*count) + 16."""
+        b = 0
+        for v in vals:
+            if v["kind"] == 2:
+                ov = int(v["size_override"])
+                grow = max(2 * int(v["nbytes"]), 8 * int(v["count"])) + 16
+                b += _align16(max(grow, ov if ov != -(1 << 63) else 0))
+        return b + int(self.low.prog["named_work_bytes"])
+
     def _upload_seeds(self, seeds):
         metas = np.zeros(len(seeds), ENTRY)
-        allv = []
-        blob = bytearray()
+        allv, blob = [], bytearray()
         for j, tc in enumerate(seeds):
             vals, payload = pack_values(tc, self.specs)
             vals["data_off"] += np.where(vals["kind"] == 2, len(blob), 0).astype(np.uint64)
@@ -164,153 +221,147 @@ class DeviceCampaign:
             allv.append(vals)
             metas[j] = (0, tc.rng_seed & ((1 << 64) - 1), 1, -1, 0)
             self.host_entries.append((tc, 0, True))
-        self._grow_corpus(len(seeds) * 2, len(blob) * 2 + 4096)
+            self.max_entry_work = max(self.max_entry_work, self._entry_work_bound(vals))
+        self._grow_corpus(max(64, len(seeds) * 2), max(1 << 16, len(blob) * 2))
         v = np.concatenate(allv)
         self.c_meta[:metas.nbytes].copy_(torch.frombuffer(bytearray(metas.tobytes()), dtype=torch.uint8))
         self.c_vals[:v.nbytes].copy_(torch.frombuffer(bytearray(v.tobytes()), dtype=torch.uint8))
         if blob:
             self.c_data[:len(blob)].copy_(torch.frombuffer(blob, dtype=torch.uint8))
-        self.n_corpus = len(seeds)
-        self.corpus_bytes = len(blob)
-
-    def _ensure_round(self, n):
-        if n <= self._round_cap:
-            return
-        n = max(n, 1024)
-        C, E = max(self.C, 1), max(self.E, 1)
-        i64 = lambda m: torch.empty(max(m, 1), dtype=torch.int64, device=self.dev)  # noqa: E731
-        i32 = lambda m: torch.empty(max(m, 1), dtype=torch.int32, device=self.dev)  # noqa: E731
-        self.r_parent = i32(n)
-        self.r_picks = self._u8(n * 3)
-        self.r_flags = i32(n * C)
-        self.r_prefix = i64(n * C)
-        self.r_children = self._u8(n * CHILD.itemsize)
-        self.r_vals = self._u8(n * self.n_args * VAL.itemsize)
-        self.r_work_base = i64(n)
-        self.r_ro_base = i64(n)
-        self.r_verdicts = self._u8(n * VERDICT.itemsize)
-        self.r_ecnt = i32(n * E)
-        self.r_overlay = i64(n * 32) if self.low.overlay else None
-        self.r_allocs = i64(n)
-        self.r_allocs_prefix = i64(n)
-        self.r_admit = i64(n)
-        self.r_pos = i64(n)
-        self.r_bytes = i64(n)
-        self.r_boff = i64(n)
-        self.r_sel = i32(n)
-        self.r_dst_off = i64(n * self.n_args)
-        self.r_tmp = i64((n + 2047) // 2048 + 8)
-        self.r_tot = i64(16)
-        self.r_scalars = i32(2)
-        self.r_first = i32(E)
-        self.r_kfirst = i32(self.K)
-        self.r_kcount = i64(self.K)
-        self._round_cap = n
-
-    def _ensure_work(self, nbytes):
-        if nbytes > self._work_cap:
-            self._work_cap = int(nbytes * 1.25) + 4096
-            self.r_work = self._u8(self._work_cap)
+        self.n_corpus, self.corpus_bytes = len(seeds), len(blob)
 
     def corpus_dev(self) -> CorpusDev:
         return CorpusDev(self.c_meta.data_ptr(), self.c_vals.data_ptr(), self.c_data.data_ptr(),
                          self.n_corpus, self.n_seeds)
 
-    def _scan64(self, src, n, stride, col, out, out_stride, total_slot):
+    # ---- slots -----------------------------------------------------------------------
+    def _slot(self, k: int, n: int) -> Slot:
+        while len(self.slots) <= k:
+            self.slots.append(None)
+        s = self.slots[k]
+        if s is None or s.cap < n:
+            s = Slot(self, max(n, 1024))
+            self.slots[k] = s
+        return s
+
+    def _scan64(self, S: Slot, src, n, stride, col, out, total_slot):
         self.launches += 3
-        _native.check(self.L.sfg_scan_u64(src.data_ptr(), n, stride, col, out.data_ptr(), out_stride, 0,
-                                          self.r_tmp.data_ptr(), self.r_tot.data_ptr() + 8 * total_slot,
-                                          _stream()), "scan")
+        _native.check(self.L.sfg_scan_u64(src.data_ptr(), n, stride, col, out.data_ptr(), 1, 0, S.tmp.data_ptr(),
+                                          S.tot.data_ptr() + 8 * total_slot, S.stream.cuda_stream), "scan")
 
     def new_worker(self):
         """Reference workers (campaign.py:712-730) get a fresh MutationSchedule and a fresh
         image: rotation counts and alloc ids restart; corpus/findings/coverage are shared."""
-        self.counts_base.zero_()
+        self.drain()
+        self.counts_run.zero_()
+        self._last_counts = None
         self.next_alloc_id = self.base.next_id
 
-    def _id_base(self, prefix: int) -> int:
-        return self.base.next_id if self.ids_reset else self._round_id0 + prefix
+    def drain(self):
+        torch.cuda.synchronize(self.dev)
 
-    # ---- one round ---------------------------------------------------------------------
-    def run_round(self, it0: int, n: int) -> RoundResult:
-        L, hp, s = self.L, self.h, _stream()
-        self._ensure_round(n)
-        cd = self.corpus_dev()
+    # ---- submit: mutate + execute (speculative on the current corpus) -----------------
+    def _submit(self, S: Slot, it0: int, n: int, round_index: int, resubmit: bool = False):
+        L, hp = self.L, self.h
+        st = S.stream
+        s = st.cuda_stream
         if it0 + n - 1 >= 2 and self.low.prog["n_mutable"] == 0:
             raise MutationError("no mutable arguments")
+        S.it0, S.n, S.round_index = it0, n, round_index
+        cd = self.corpus_dev()
         C = self.C
-        self.launches += 3 + 3 * C
-        _native.check(L.sfg_plan(hp, ctypes.byref(cd), it0, n, self.r_parent.data_ptr(), self.r_picks.data_ptr(),
-                                 self.r_flags.data_ptr(), s), "plan")
+        self.launches += 2 + 3 * C
+        _native.check(L.sfg_plan(hp, ctypes.byref(cd), it0, n, S.parent.data_ptr(), S.picks.data_ptr(),
+                                 S.flags.data_ptr(), s), "plan")
         for c in range(C):
-            _native.check(L.sfg_scan_u32(self.r_flags.data_ptr(), n, C, c, self.r_prefix.data_ptr(), C, c,
-                                         self.r_tmp.data_ptr(), self.r_tot.data_ptr() + 8 * (8 + c % 8), s),
-                          "scan flags")
-        _native.check(L.sfg_mutate(hp, ctypes.byref(cd), it0, n, self.r_prefix.data_ptr(),
-                                   self.counts_base.data_ptr(), self.r_children.data_ptr(), self.r_vals.data_ptr(),
-                                   s), "mutate")
+            _native.check(L.sfg_scan_u32(S.flags.data_ptr(), n, C, c, S.prefix.data_ptr(), C, c, S.tmp.data_ptr(),
+                                         S.tot.data_ptr() + 8 * (8 + c), s), "scan flags")
+        with torch.cuda.stream(st):
+            if not resubmit:                   # a re-submitted round keeps its rotation base
+                if self._last_counts is not None:
+                    st.wait_event(self._last_counts)
+                S.counts_base.copy_(self.counts_run)
+                if C:
+                    self.counts_run[:C] = S.counts_base[:C] + S.tot[8:8 + C]
+                S.ev_counts.record(st)
+                self._last_counts = S.ev_counts
+        _native.check(L.sfg_mutate(hp, ctypes.byref(cd), it0, n, S.prefix.data_ptr(), S.counts_base.data_ptr(),
+                                   S.children.data_ptr(), S.vals.data_ptr(), s), "mutate")
         cw = CHILD.itemsize // 8
-        self._scan64(self.r_children.view(torch.int64), n, cw, CHILD.fields["work_bytes"][1] // 8,
-                     self.r_work_base, 1, 0)
-        if self.low.prog["diff_readback"]:
-            self._scan64(self.r_children.view(torch.int64), n, cw, CHILD.fields["readout_bytes"][1] // 8,
-                         self.r_ro_base, 1, 1)
-        tot = self.r_tot[:2].cpu()
-        self._ensure_work(int(tot[0]))
-        ro = self._u8(int(tot[1])) if self.low.prog["diff_readback"] else None
-        self.r_readouts = ro
-        _native.check(L.sfg_apply(hp, ctypes.byref(cd), n, self.r_children.data_ptr(), self.r_vals.data_ptr(),
-                                  self.r_work_base.data_ptr(), self.r_work.data_ptr(), s), "apply")
-        self._execute(n)
-        return self._triage(it0, n)
+        self._scan64(S, S.children.view(torch.int64), n, cw, CHILD.fields["work_bytes"][1] // 8, S.work_base, 0)
+        S.ensure_work(n * self.max_entry_work + 64, self.dev)
+        if self.diff:
+            self._scan64(S, S.children.view(torch.int64), n, cw, CHILD.fields["readout_bytes"][1] // 8, S.ro_base, 1)
+            with torch.cuda.stream(st):
+                S.tot[:2].cpu()  # host needs the readout size (diff mode only; tests)
+            S.readouts = self._u8(int(S.tot[1].item()) + 16)
+        else:
+            S.readouts = None
+        _native.check(L.sfg_apply(hp, ctypes.byref(cd), n, S.children.data_ptr(), S.vals.data_ptr(),
+                                  S.work_base.data_ptr(), S.work.data_ptr(), s), "apply")
+        self._execute(S, n)
 
-    def _execute(self, n):
+    def _execute(self, S: Slot, n: int):
         self.launches += 1
+        st = S.stream
         if self.timing:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-            ev[0].record()
+            ev[0].record(st)
         _native.check(self.L.sfg_execute(
-            self.h, n, self.r_children.data_ptr(), self.r_vals.data_ptr(), self.r_work_base.data_ptr(),
-            self.r_work.data_ptr(), self.r_verdicts.data_ptr(), self.r_ecnt.data_ptr(), _ptr(self.r_readouts),
-            self.r_ro_base.data_ptr(), _ptr(self.r_overlay), _stream()), "execute")
+            self.h, n, S.children.data_ptr(), S.vals.data_ptr(), S.work_base.data_ptr(), S.work.data_ptr(),
+            S.verdicts.data_ptr(), S.ecnt.data_ptr(), _ptr(S.readouts), S.ro_base.data_ptr(), _ptr(S.overlay),
+            st.cuda_stream), "execute")
         if self.timing:
-            ev[1].record()
-            self.last_exec_events = ev
+            ev[1].record(st)
+            S.exec_ev = ev
+            self.exec_events.append(ev)
 
-    def _triage(self, it0, n) -> RoundResult:
-        L, hp, s = self.L, self.h, _stream()
+    # ---- finalize: triage in order ------------------------------------------------------
+    def _finalize(self, S: Slot) -> RoundResult:
+        L, hp, st = self.L, self.h, S.stream
+        s = st.cuda_stream
+        n, it0 = S.n, S.it0
         self.launches += 4
-        self.r_scalars.fill_(-1)
-        self.r_first.fill_(-1)
-        self.r_kfirst.fill_(-1)
-        self.r_kcount.zero_()
-        _native.check(L.sfg_triage(hp, n, self.r_verdicts.data_ptr(), self.r_ecnt.data_ptr(),
-                                   self.r_children.data_ptr(), self.r_scalars.data_ptr(), self.r_first.data_ptr(),
-                                   self.edge_total.data_ptr(), self.r_kfirst.data_ptr(), self.r_kcount.data_ptr(),
-                                   self.entered.data_ptr(), self.r_allocs.data_ptr(), self.ghit.data_ptr(),
-                                   self.r_admit.data_ptr(), s), "triage")
-        self._scan64(self.r_admit, n, 1, 0, self.r_pos, 1, 2)
-        self._scan64(self.r_allocs, n, 1, 0, self.r_allocs_prefix, 1, 3)
-        sc = self.r_scalars.cpu().numpy().view(np.uint32)
-        tot = self.r_tot[:16].cpu().numpy().view(np.uint64)
+        with torch.cuda.stream(st):
+            if self._last_done is not None:
+                st.wait_event(self._last_done)
+            S.scalars.fill_(-1)
+            S.first.fill_(-1)
+            S.kfirst.fill_(-1)
+            S.kcount.zero_()
+        _native.check(L.sfg_triage(hp, n, S.verdicts.data_ptr(), S.ecnt.data_ptr(), S.children.data_ptr(),
+                                   S.scalars.data_ptr(), S.first.data_ptr(), self.edge_total.data_ptr(),
+                                   S.kfirst.data_ptr(), S.kcount.data_ptr(), self.entered.data_ptr(),
+                                   S.allocs.data_ptr(), self.ghit.data_ptr(), S.admit.data_ptr(), s), "triage")
+        self._scan64(S, S.admit, n, 1, 0, S.pos, 2)
+        self._scan64(S, S.allocs, n, 1, 0, S.allocs_prefix, 3)
+        with torch.cuda.stream(st):
+            S.pin_sc.copy_(S.scalars, non_blocking=True)
+            S.pin_tot.copy_(S.tot, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(st)
+        ev.synchronize()
+        sc = S.pin_sc.numpy().view(np.uint32)
+        tot = S.pin_tot.numpy().view(np.uint64)
         stop, fatal = int(sc[0]), int(sc[1])
         if fatal != U32_NONE and fatal <= stop:
-            self._raise_fatal(fatal)
+            self._raise_fatal(S, fatal)
         executed = n if stop == U32_NONE else stop + 1
         n_adm = int(tot[2])
         self._round_id0 = self.next_alloc_id
         if n_adm:
-            self._admit(n, n_adm)
+            self._admit(S, n_adm)
         _native.check(L.sfg_commit(hp, self.edge_total.data_ptr(), self.ghit.data_ptr(), s), "commit")
-        new_keys = self._absorb_findings(it0)
+        self.launches += 1
+        new_keys = self._absorb_findings(S)
         self.next_alloc_id += int(tot[3])
-        if stop == U32_NONE and self.C:
-            self.counts_base[:self.C] += self.r_tot[8:8 + self.C]
+        S.ev_done.record(st)
+        self._last_done = S.ev_done
         self.rounds += 1
-        return RoundResult(it0, n, None if stop == U32_NONE else stop, executed, n_adm, new_keys)
+        return RoundResult(it0, n, None if stop == U32_NONE else stop, executed, n_adm, new_keys, S)
 
-    def _raise_fatal(self, i):
-        v = _np(self.r_verdicts[i * VERDICT.itemsize:(i + 1) * VERDICT.itemsize], VERDICT)[0]
+    def _raise_fatal(self, S: Slot, i):
+        v = _np(S.verdicts[i * VERDICT.itemsize:(i + 1) * VERDICT.itemsize], VERDICT)[0]
         st = int(v["status"])
         if st == ST_OUT_OF_SPACE:
             raise OutOfSpaceError(f"input {i}: allocation does not fit its space")
@@ -320,28 +371,30 @@ class DeviceCampaign:
                            ST_OVERLAY: "per-input INIT-buffer write overlay overflow",
                            ST_COUNTER: "per-input edge counter overflow"}.get(st, f"status {st}"))
 
-    def _admit(self, n, n_adm):
-        L, hp, s = self.L, self.h, _stream()
+    def _admit(self, S: Slot, n_adm: int):
+        L, hp, st = self.L, self.h, S.stream
+        s = st.cuda_stream
+        n = S.n
         self.launches += 3
-        _native.check(L.sfg_child_bytes(hp, self.r_vals.data_ptr(), self.r_admit.data_ptr(), n,
-                                        self.r_bytes.data_ptr(), s), "child_bytes")
-        self._scan64(self.r_bytes, n, 1, 0, self.r_boff, 1, 4)
-        nbytes = int(self.r_tot[4].item())
+        _native.check(L.sfg_child_bytes(hp, S.vals.data_ptr(), S.admit.data_ptr(), n, S.bytes.data_ptr(), s),
+                      "child_bytes")
+        self._scan64(S, S.bytes, n, 1, 0, S.boff, 4)
+        with torch.cuda.stream(st):
+            nbytes = int(S.tot[4].item())
         self._grow_corpus(max(self.cap, (self.n_corpus + n_adm) * 2),
                           max(self.data_cap, (self.corpus_bytes + nbytes) * 2))
         cd = self.corpus_dev()
-        _native.check(L.sfg_compact(hp, self.r_children.data_ptr(), self.r_vals.data_ptr(), self.r_admit.data_ptr(),
-                                    self.r_pos.data_ptr(), self.r_boff.data_ptr(), n, self.n_corpus,
-                                    self.corpus_bytes, self.c_meta.data_ptr(), self.c_vals.data_ptr(),
-                                    self.c_child.data_ptr(), self.r_sel.data_ptr(), self.r_dst_off.data_ptr(), s),
-                      "compact")
-        _native.check(L.sfg_regen(hp, ctypes.byref(cd), n_adm, self.r_sel.data_ptr(), self.r_children.data_ptr(),
-                                  self.r_vals.data_ptr(), self.r_dst_off.data_ptr(), self.c_data.data_ptr(), s),
-                      "regen")
+        _native.check(L.sfg_compact(hp, S.children.data_ptr(), S.vals.data_ptr(), S.admit.data_ptr(),
+                                    S.pos.data_ptr(), S.boff.data_ptr(), n, self.n_corpus, self.corpus_bytes,
+                                    self.c_meta.data_ptr(), self.c_vals.data_ptr(), self.c_child.data_ptr(),
+                                    S.sel.data_ptr(), S.dst_off.data_ptr(), s), "compact")
+        _native.check(L.sfg_regen(hp, ctypes.byref(cd), n_adm, S.sel.data_ptr(), S.children.data_ptr(),
+                                  S.vals.data_ptr(), S.dst_off.data_ptr(), self.c_data.data_ptr(), s), "regen")
         first = self.n_corpus
         self.n_corpus += n_adm
         self.corpus_bytes += nbytes
-        self._mirror_entries(first, self.n_corpus)
+        with torch.cuda.stream(st):
+            self._mirror_entries(first, self.n_corpus)
 
     def _mirror_entries(self, lo, hi):
         """Build reference TestCase objects for corpus entries [lo, hi)."""
@@ -353,39 +406,97 @@ class DeviceCampaign:
         top = max([int(v["data_off"]) + int(v["nbytes"]) for v in vals if v["kind"] == 2] + [base])
         data = self.c_data[base:top].cpu().numpy().tobytes() if top > base else b""
         for j in range(hi - lo):
-            args = unpack_values(vals[j * self.n_args:(j + 1) * self.n_args], data, base)
+            row = vals[j * self.n_args:(j + 1) * self.n_args]
+            args = unpack_values(row, data, base)
             parent_tc = self.host_entries[int(meta[j]["parent"])][0]
             ops = tuple(decode_op(chld[j]["ops"][k]) for k in range(int(chld[j]["n_ops"])))
-            tc = TestCase(args, int(meta[j]["rng_seed"]), parent_tc.id, ops)
-            self.host_entries.append((tc, int(meta[j]["admitted_iteration"]), False))
+            self.host_entries.append((TestCase(args, int(meta[j]["rng_seed"]), parent_tc.id, ops),
+                                      int(meta[j]["admitted_iteration"]), False))
+            self.max_entry_work = max(self.max_entry_work, self._entry_work_bound(row))
 
-    def _absorb_findings(self, it0):
-        kc = self.r_kcount.cpu().numpy()
-        hot = np.nonzero(kc)[0]
-        if not len(hot):
-            return []
-        kf = self.r_kfirst.cpu().numpy().view(np.uint32)
-        fresh = []
-        for k in hot:
-            ks = self.key_strings.get(int(k))
-            if ks is not None and ks in self.findings:
-                self.findings.bump(ks, int(kc[k]))
-            else:
-                fresh.append((int(kf[k]), int(k)))
-        fresh.sort()
-        out = []
-        if fresh:
-            idx = [i for i, _ in fresh]
-            vt = _np(self.r_verdicts.view(-1, VERDICT.itemsize)[idx].reshape(-1), VERDICT)
-            ap = self.r_allocs_prefix[idx].cpu().numpy()
-            for j, (i, k) in enumerate(fresh):
-                rep = decode_verdict(vt[j], self.low, it0 + i, self._id_base(int(ap[j])))
-                self.key_strings[k] = rep.dedupe_key
-                self.findings.add_many(rep, int(kc[k]))
-                out.append((i, rep))
-        return out
+    def _id_base(self, prefix: int) -> int:
+        return self.base.next_id if self.ids_reset else self._round_id0 + prefix
 
-    # ---- bench / e2e helpers ----------------------------------------------------------
+    def _absorb_findings(self, S: Slot):
+        with torch.cuda.stream(S.stream):
+            kc = S.kcount.cpu().numpy()
+            hot = np.nonzero(kc)[0]
+            if not len(hot):
+                return []
+            kf = S.kfirst.cpu().numpy().view(np.uint32)
+            fresh = []
+            for k in hot:
+                ks = self.key_strings.get(int(k))
+                if ks is not None and ks in self.findings:
+                    self.findings.bump(ks, int(kc[k]))
+                else:
+                    fresh.append((int(kf[k]), int(k)))
+            fresh.sort()
+            out = []
+            if fresh:
+                idx = torch.tensor([i for i, _ in fresh], dtype=torch.long, device=self.dev)
+                vt = _np(S.verdicts.view(-1, VERDICT.itemsize)[idx].reshape(-1), VERDICT)
+                ap = S.allocs_prefix[idx].cpu().numpy()
+                for j, (i, k) in enumerate(fresh):
+                    rep = decode_verdict(vt[j], self.low, S.it0 + i, self._id_base(int(ap[j])))
+                    self.key_strings[k] = rep.dedupe_key
+                    self.findings.add_many(rep, int(kc[k]))
+                    out.append((i, rep))
+            return out
+
+    # ---- public round API --------------------------------------------------------------
+    def run_round(self, it0: int, n: int) -> RoundResult:
+        """Submit and finalize one round (no pipelining)."""
+        S = self._slot(0, n)
+        self._submit(S, it0, n, self.rounds)
+        return self._finalize(S)
+
+    def run_rounds(self, it0: int, it_stop: int, round_size: int, depth: int = 8, on_round=None):
+        """Rounds covering iterations [it0, it_stop) with up to ``depth`` rounds in
+        flight.  ``on_round(result)`` runs after each round is finalized (before its
+        slot is reused).  Returns the list of RoundResults (stops early on a stop)."""
+        plan = []
+        it = it0
+        while it < it_stop:
+            n = min(round_size, it_stop - it)
+            plan.append((it, n))
+            it += n
+        results = []
+        inflight = deque()
+        base_round = self.rounds
+        nxt = 0
+
+        def submit(k):
+            it_k, n_k = plan[k]
+            S = self._slot(k % depth, n_k)
+            self._submit(S, it_k, n_k, base_round + k)
+            inflight.append((k, S))
+
+        while nxt < len(plan) and len(inflight) < depth:
+            submit(nxt)
+            nxt += 1
+        while inflight:
+            k, S = inflight.popleft()
+            res = self._finalize(S)
+            results.append(res)
+            if on_round is not None:
+                on_round(res)
+            if res.stop is not None:
+                self.drain()
+                break
+            if res.n_admitted:
+                # later in-flight rounds were mutated from the pre-admission corpus: redo them
+                redo = list(inflight)
+                inflight.clear()
+                for kk, SS in redo:
+                    self._submit(SS, SS.it0, SS.n, SS.round_index, resubmit=True)
+                    inflight.append((kk, SS))
+            if nxt < len(plan):
+                submit(nxt)
+                nxt += 1
+        return results
+
+    # ---- bench / e2e helpers ------------------------------------------------------------
     def corpus_host_pinned(self):
         """Pinned host copies of the device corpus (meta, vals, child records, payload)."""
         out = []
@@ -397,25 +508,28 @@ class DeviceCampaign:
             out.append(h)
         return out
 
-    def load_corpus_from_host(self, host):
+    def load_corpus_from_host(self, host, stream=None):
         """Re-upload the corpus from pinned host buffers (stream-ordered H2D copies)."""
-        for t, h in zip((self.c_meta, self.c_vals, self.c_child, self.c_data), host):
-            t[:h.numel()].copy_(h, non_blocking=True)
+        with torch.cuda.stream(stream or torch.cuda.current_stream()):
+            for t, h in zip((self.c_meta, self.c_vals, self.c_child, self.c_data), host):
+                t[:h.numel()].copy_(h, non_blocking=True)
 
     def algorithmic_exec_bytes(self) -> int:
         """Unavoidable off-chip bytes of one exec in the execute kernel: the child's
-        argument payload read once (SURVEY.md §8(d) C_write counterpart), its 64-byte
-        verdict and a 4*ceil(E/32)-byte edge-hit bitmap written."""
+        argument payload read once, its 64-byte verdict and a 4*ceil(E/32)-byte
+        edge-hit bitmap written."""
         seed = self.host_entries[0][0]
         payload = sum(len(v.data) if hasattr(v, "data") else 4 for v in seed.args)
         return payload + 64 + 4 * ((self.E + 31) // 32)
 
-    def retired_mean(self, n: int) -> float:
-        v = _np(self.r_verdicts[:n * VERDICT.itemsize], VERDICT)
+    def retired_mean(self, S: Slot | None = None) -> float:
+        S = S or self.slots[0]
+        v = _np(S.verdicts[:S.n * VERDICT.itemsize], VERDICT)
         return float(v["retired"].astype(np.float64).mean())
 
     # ---- views for tests / reporting ----------------------------------------------------
     def coverage_map(self) -> CoverageMap:
+        self.drain()
         cov = CoverageMap.for_program(self.manifest.program)
         tot = self.edge_total[:self.E].cpu().numpy().view(np.uint64) if self.E else []
         for e, c in enumerate(tot):
@@ -428,48 +542,48 @@ class DeviceCampaign:
                 cov.entered[name] = True
         return cov
 
+    def _edges_row(self, row):
+        edges = {}
+        for e in np.nonzero(row[:self.E])[0]:
+            name, (a, b) = self.low.edge_names[e]
+            edges.setdefault(name, []).append([a, b, int(row[e])])
+        return {k: sorted(x) for k, x in edges.items()}
+
     def round_records(self, res: RoundResult):
-        """Per-input records of the last round (same shape as oracle.loop records)."""
+        """Per-input records of a finalized round (same shape as oracle.loop records)."""
+        S = res.slot
         n = res.executed
-        s = _stream()
-        vals = _np(self.r_vals[:n * self.n_args * VAL.itemsize], VAL)
-        chld = _np(self.r_children[:n * CHILD.itemsize], CHILD)
-        verd = _np(self.r_verdicts[:n * VERDICT.itemsize], VERDICT)
-        ecnt = self.r_ecnt[:n * max(self.E, 1)].cpu().numpy().view(np.uint32).reshape(n, max(self.E, 1))
-        admit = self.r_admit[:n].cpu().numpy()
-        aprefix = self.r_allocs_prefix[:n].cpu().numpy()
-        tcs = self.child_testcases(list(range(n)))
+        self.drain()
+        chld = _np(S.children[:n * CHILD.itemsize], CHILD)
+        verd = _np(S.verdicts[:n * VERDICT.itemsize], VERDICT)
+        E1 = max(self.E, 1)
+        ecnt = S.ecnt[:n * E1].cpu().numpy().view(np.uint32).reshape(n, E1)
+        admit = S.admit[:n].cpu().numpy()
+        aprefix = S.allocs_prefix[:n].cpu().numpy()
+        tcs = self.child_testcases(list(range(n)), S)
         recs = []
         for i in range(n):
-            c = chld[i]
-            p = int(c["parent"])
-            tc = tcs[i]
-            v = verd[i]
+            c, v = chld[i], verd[i]
             st = int(v["status"])
             rep = decode_verdict(v, self.low, int(c["it"]), self._id_base(int(aprefix[i]))) if st == ST_FINDING else None
-            edges = {}
-            for e in np.nonzero(ecnt[i][:self.E])[0]:
-                name, (a, b) = self.low.edge_names[e]
-                edges.setdefault(name, []).append([a, b, int(ecnt[i][e])])
-            recs.append({"it": int(c["it"]), "parent": p, "child": tc,
-                         "status": {0: "ok", 1: "finding", 2: "budget"}.get(st, f"fatal{st}"),
-                         "retired": int(v["retired"]), "allocs": int(v["allocs"]),
-                         "edges": {k: sorted(x) for k, x in edges.items()},
+            recs.append({"it": int(c["it"]), "parent": int(c["parent"]), "child": tcs[i],
+                         "status": STATUS.get(st, f"fatal{st}"), "retired": int(v["retired"]),
+                         "allocs": int(v["allocs"]), "edges": self._edges_row(ecnt[i]),
                          "report": rep.to_line() if rep else None, "admitted": bool(admit[i])})
         return recs
 
-    def child_testcases(self, idx):
+    def child_testcases(self, idx, S: Slot | None = None):
         """Reference TestCase objects for round inputs ``idx``: payloads regenerated
         on the device from (parent, ops) with the product kernel, then decoded."""
+        S = S or self.slots[0]
         n = len(idx)
         if n == 0:
             return []
-        s = _stream()
-        sel_np = np.asarray(idx, np.int32)
-        vals = _np(self.r_vals.view(-1, VAL.itemsize * self.n_args)[torch.from_numpy(sel_np).long().to(self.dev)]
-                   .reshape(-1), VAL)
-        chld = _np(self.r_children.view(-1, CHILD.itemsize)[torch.from_numpy(sel_np).long().to(self.dev)]
-                   .reshape(-1), CHILD)
+        st = S.stream
+        sel = torch.tensor(list(idx), dtype=torch.int32, device=self.dev)
+        with torch.cuda.stream(st):
+            vals = _np(S.vals.view(-1, VAL.itemsize * self.n_args)[sel.long()].reshape(-1), VAL)
+            chld = _np(S.children.view(-1, CHILD.itemsize)[sel.long()].reshape(-1), CHILD)
         offs = np.zeros(n * self.n_args, np.uint64)
         cur = 0
         for j in range(n):
@@ -477,14 +591,15 @@ class DeviceCampaign:
                 v = vals[j * self.n_args + a]
                 if v["kind"] == 2:
                     offs[j * self.n_args + a] = cur
-                    cur += (int(v["nbytes"]) + 15) // 16 * 16
+                    cur += _align16(int(v["nbytes"]))
         dst = self._u8(cur + 16)
-        sel = torch.from_numpy(sel_np).to(self.dev)
         doff = torch.from_numpy(offs.view(np.int64)).to(self.dev)
         cd = self.corpus_dev()
         self.launches += 1
-        _native.check(self.L.sfg_regen(self.h, ctypes.byref(cd), n, sel.data_ptr(), self.r_children.data_ptr(),
-                                       self.r_vals.data_ptr(), doff.data_ptr(), dst.data_ptr(), s), "regen")
+        torch.cuda.synchronize(self.dev)
+        _native.check(self.L.sfg_regen(self.h, ctypes.byref(cd), n, sel.data_ptr(), S.children.data_ptr(),
+                                       S.vals.data_ptr(), doff.data_ptr(), dst.data_ptr(),
+                                       torch.cuda.current_stream().cuda_stream), "regen")
         data = dst.cpu().numpy().tobytes()
         out = []
         for j in range(n):
@@ -505,13 +620,14 @@ class DeviceCampaign:
     def execute_testcases(self, tcs, iteration0: int = 0):
         """Run COMPUTE for explicit inputs (no mutation); returns per-input dicts."""
         n = len(tcs)
-        self._ensure_round(n)
+        S = self._slot(0, n)
+        self.drain()
         vals_all = np.zeros(n * self.n_args, VAL)
         chld = np.zeros(n, CHILD)
         work = bytearray()
         ro_base = np.zeros(n, np.uint64)
-        ro_total = 0
         wbase = np.zeros(n, np.uint64)
+        ro_total = 0
         for i, tc in enumerate(tcs):
             vals, _ = pack_values(tc, self.specs)
             wbase[i] = len(work)
@@ -520,46 +636,44 @@ class DeviceCampaign:
             for a, v in enumerate(tc.args):
                 if vals[a]["kind"] != 2:
                     continue
-                size = v.size_override if v.size_override is not None else len(v.data)
-                size = max(size, 0)
+                size = max(v.size_override if v.size_override is not None else len(v.data), 0)
                 chunk = v.data[:size] + bytes(max(0, size - len(v.data)))
                 vals[a]["data_off"] = off
                 region += chunk + bytes((-len(chunk)) % 16)
-                off += (size + 15) // 16 * 16
+                off += _align16(size)
             region += bytes(int(self.low.prog["named_work_bytes"]))
             work += region
-            chld[i]["it"] = iteration0 + i
-            chld[i]["parent"] = -1
-            chld[i]["work_bytes"] = len(region)
+            chld[i]["it"], chld[i]["parent"], chld[i]["work_bytes"] = iteration0 + i, -1, len(region)
             ro = int(self.low.prog["readout_bytes_fixed"])
             for k in range(int(self.low.prog["n_copyout_arg"])):
-                ro += (int(vals[int(self.low.prog["copyout_arg"][k])]["nbytes"]) + 15) // 16 * 16
+                ro += _align16(int(vals[int(self.low.prog["copyout_arg"][k])]["nbytes"]))
             ro_base[i] = ro_total
             ro_total += ro
             chld[i]["readout_bytes"] = ro
             vals_all[i * self.n_args:(i + 1) * self.n_args] = vals
-        self._ensure_work(len(work) + 16)
-        self.r_work[:len(work)].copy_(torch.frombuffer(work, dtype=torch.uint8)) if work else None
-        self.r_children[:chld.nbytes].copy_(torch.frombuffer(bytearray(chld.tobytes()), dtype=torch.uint8))
-        self.r_vals[:vals_all.nbytes].copy_(torch.frombuffer(bytearray(vals_all.tobytes()), dtype=torch.uint8))
-        self.r_work_base[:n].copy_(torch.from_numpy(wbase.view(np.int64)))
-        self.r_ro_base[:n].copy_(torch.from_numpy(ro_base.view(np.int64)))
-        self.r_readouts = self._u8(ro_total + 16) if self.low.prog["diff_readback"] else None
-        self._execute(n)
-        verd = _np(self.r_verdicts[:n * VERDICT.itemsize], VERDICT)
-        ecnt = self.r_ecnt[:n * max(self.E, 1)].cpu().numpy().view(np.uint32).reshape(n, max(self.E, 1))
-        rod = self.r_readouts.cpu().numpy().tobytes() if self.r_readouts is not None else b""
+        S.ensure_work(len(work) + 16, self.dev)
+        if work:
+            S.work[:len(work)].copy_(torch.frombuffer(work, dtype=torch.uint8))
+        S.children[:chld.nbytes].copy_(torch.frombuffer(bytearray(chld.tobytes()), dtype=torch.uint8))
+        S.vals[:vals_all.nbytes].copy_(torch.frombuffer(bytearray(vals_all.tobytes()), dtype=torch.uint8))
+        S.work_base[:n].copy_(torch.from_numpy(wbase.view(np.int64)))
+        S.ro_base[:n].copy_(torch.from_numpy(ro_base.view(np.int64)))
+        S.readouts = self._u8(ro_total + 16) if self.diff else None
+        S.n = n
+        torch.cuda.synchronize(self.dev)
+        self._execute(S, n)
+        self.drain()
+        verd = _np(S.verdicts[:n * VERDICT.itemsize], VERDICT)
+        E1 = max(self.E, 1)
+        ecnt = S.ecnt[:n * E1].cpu().numpy().view(np.uint32).reshape(n, E1)
+        rod = S.readouts.cpu().numpy().tobytes() if S.readouts is not None else b""
         out = []
         for i in range(n):
             v = verd[i]
             st = int(v["status"])
             rep = decode_verdict(v, self.low, iteration0 + i, self.base.next_id) if st == ST_FINDING else None
-            edges = {}
-            for e in np.nonzero(ecnt[i][:self.E])[0]:
-                name, (a, b) = self.low.edge_names[e]
-                edges.setdefault(name, []).append([a, b, int(ecnt[i][e])])
             readouts = {}
-            if self.r_readouts is not None and st == 0:
+            if S.readouts is not None and st == 0:
                 cur = int(ro_base[i])
                 for op in self.manifest.phases["compute"]:
                     if op.kind != "copy_out":
@@ -573,15 +687,18 @@ class DeviceCampaign:
                     else:
                         ln = op.size
                         readouts[op.name] = rod[cur:cur + ln]
-                    cur += (ln + 15) // 16 * 16
-            out.append({"status": {0: "ok", 1: "finding", 2: "budget"}.get(st, f"fatal{st}"),
-                        "report": rep, "retired": int(v["retired"]), "allocs": int(v["allocs"]),
-                        "edges": {k: sorted(x) for k, x in edges.items()}, "readouts": readouts,
+                    cur += _align16(ln)
+            out.append({"status": STATUS.get(st, f"fatal{st}"), "report": rep, "retired": int(v["retired"]),
+                        "allocs": int(v["allocs"]), "edges": self._edges_row(ecnt[i]), "readouts": readouts,
                         "entered": int(v["entered"])})
         return out
 
     def close(self):
         if getattr(self, "h", None):
+            try:
+                self.drain()
+            except Exception:
+                pass
             self.L.sfg_program_destroy(self.h)
             self.h = None
 

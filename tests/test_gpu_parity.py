@@ -88,3 +88,45 @@ def test_batched_rounds_match_reference(engine_cls, name):
     assert report_to_rec(build_report(dc.coverage_map())) == ref["coverage"]
     assert [_digest(e[0]) for e in dc.host_entries] == ref["corpus"]
     dc.close()
+
+
+@pytest.mark.parametrize("name", ["amax", "amin", "rotm", "dot"])
+def test_pipelined_rounds_equal_sequential(engine_cls, name):
+    """Speculative round pipelining (depth 4) reproduces the reference's batched
+    records exactly, including rounds that admit children (re-submission path)."""
+    data = golden("ref_batched.json")
+    cfg = data["config"]
+    ref = data["runs"][name]
+    m = bench_manifest(name)
+    dc = engine_cls(m, master_seed=cfg["master_seed"])
+    got = []
+    dc.run_rounds(1, cfg["iterations"] + 1, cfg["round_size"], depth=4,
+                  on_round=lambda res: got.extend(dc.round_records(res)))
+    assert len(got) == len(ref["records"])
+    for g, w in zip(got, ref["records"]):
+        assert _digest(g["child"]) == w["child"], g["it"]
+        assert g["report"] == w["report"], g["it"]
+        assert g["edges"] == w["edges"], g["it"]
+        assert g["admitted"] == w["admitted"], g["it"]
+    assert dc.findings.render_text() == ref["findings"]
+    assert report_to_rec(build_report(dc.coverage_map())) == ref["coverage"]
+    assert [_digest(e[0]) for e in dc.host_entries] == ref["corpus"]
+    dc.close()
+
+
+def test_fuzz_loop_api_matches_batched_reference(engine_cls, tmp_path):
+    """The reference-shaped fuzz_loop (public API) over the same contract."""
+    from paper_2603_05725_b200.campaign import CampaignConfig, fuzz_loop
+    data = golden("ref_batched.json")
+    cfg = data["config"]
+    ref = data["runs"]["amax"]
+    m = bench_manifest("amax")
+    s = fuzz_loop(m, CampaignConfig(master_seed=cfg["master_seed"], iterations=cfg["iterations"],
+                                    round_size=cfg["round_size"], pipeline_depth=3, out_dir=tmp_path / "out"))
+    assert s.findings.render_text() == ref["findings"]
+    assert report_to_rec(build_report(s.coverage)) == ref["coverage"]
+    assert [_digest(e.tc) for e in s.corpus.entries] == ref["corpus"]
+    assert s.compute_runs == cfg["iterations"]
+    assert (tmp_path / "out" / "findings.txt").read_text() == ref["findings"]
+    crashes = sorted(p.name for p in (tmp_path / "out" / "crashes").iterdir())
+    assert len(crashes) == len(s.findings)

@@ -18,10 +18,10 @@ for R in [int(x) for x in (sys.argv[2:] or ["4096", "16384", "65536", "262144", 
     times = []
     for _ in range(3):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record(); dc.run_round(it, R); e.record(); torch.cuda.synchronize()
+        s.record(); res = dc.run_round(it, R); e.record(); torch.cuda.synchronize()
         it += R
-        times.append((s.elapsed_time(e), dc.last_exec_events[0].elapsed_time(dc.last_exec_events[1])))
-    v = dc.r_verdicts[:R * VERDICT.itemsize].cpu().numpy().view(VERDICT)
+        times.append((s.elapsed_time(e), res.slot.exec_ev[0].elapsed_time(res.slot.exec_ev[1])))
+    v = res.slot.verdicts[:R * VERDICT.itemsize].cpu().numpy().view(VERDICT)
     ret = v["retired"].astype(np.int64)
     q = np.percentile(ret, [50, 90, 99, 99.9, 100])
     print(f"R={R:8d} step_ms={[round(t[0],2) for t in times]} k3_ms={[round(t[1],2) for t in times]} "
