@@ -83,9 +83,12 @@ int sfg_apply(const sfg_program* p, const sfg_corpus_dev* c, int n, const void* 
 int sfg_regen(const sfg_program* p, const sfg_corpus_dev* c, int n_sel, const int32_t* sel,
               const void* children, const void* vals, const uint64_t* dst_off, uint8_t* dst,
               void* stream);
+/* work_counter: 4-byte device scratch private to this launch (the persistent
+ * specialized kernel hands out inputs from it; concurrent launches need their own). */
 int sfg_execute(const sfg_program* p, int n, const void* children, const void* vals,
                 const uint64_t* work_base, uint8_t* work, void* verdicts, uint32_t* edge_counts,
-                uint8_t* readouts, const uint64_t* readout_base, uint64_t* overlay, void* stream);
+                uint8_t* readouts, const uint64_t* readout_base, uint64_t* overlay, int* work_counter,
+                void* stream);
 int sfg_triage(const sfg_program* p, int n, const void* verdicts, const uint32_t* edge_counts,
                const void* children, uint32_t* scalars, uint32_t* first_hit, uint64_t* edge_total,
                uint32_t* key_first, uint64_t* key_count, uint32_t* entered, uint64_t* allocs,

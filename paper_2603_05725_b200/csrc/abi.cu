@@ -13,8 +13,9 @@ struct sfg_program {
   sfg_prog P;
   cudaLibrary_t jit_lib = nullptr;    // specialized execute kernel (jit.cu), if built
   cudaKernel_t jit_kernel = nullptr;
-  int* jit_next = nullptr;            // persistent-kernel work counter
   int jit_grid = 0;                   // resident CTAs (occupancy x SMs)
+  int jit_block = 128;                // CTA size of the persistent kernel
+  int jit_mode = 1;                   // 0 per-lane fetch, 1 per-warp batches
   std::string jit_source, jit_log;
   sfg_ins* ins;
   sfg_hostop* hostops;
@@ -161,14 +162,12 @@ int sfg_program_create(const void* prog, size_t prog_bytes, const void* ins, siz
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)p->jit_kernel, 128, 0);
+    if (const char* b = getenv("SFG_EXEC_BLOCK")) p->jit_block = atoi(b) >= 32 ? atoi(b) : 128;
+    if (const char* md = getenv("SFG_EXEC_MODE")) p->jit_mode = atoi(md);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)p->jit_kernel, p->jit_block, 0);
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
     p->jit_grid = sms * per_sm;
-    e = cudaMalloc((void**)&p->jit_next, sizeof(int));
-    if (e != cudaSuccess) {
-      sfg_program_destroy(p);
-      return fail("sfg_program_create: jit counter", e);
-    }
+
   }
   e = cudaFuncSetAttribute(sfg_execute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem);
   if (e != cudaSuccess) {
@@ -191,7 +190,6 @@ int sfg_program_update(sfg_program* p, const void* prog, size_t prog_bytes) {
 void sfg_program_destroy(sfg_program* p) {
   if (!p) return;
   if (p->jit_lib) cudaLibraryUnload(p->jit_lib);
-  if (p->jit_next) cudaFree(p->jit_next);
   cudaFree(p->ins);
   cudaFree(p->hostops);
   cudaFree(p->binds);
@@ -271,18 +269,24 @@ int sfg_regen(const sfg_program* p, const sfg_corpus_dev* c, int n_sel, const in
 
 int sfg_execute(const sfg_program* p, int n, const void* children, const void* vals, const uint64_t* work_base,
                 uint8_t* work, void* verdicts, uint32_t* edge_counts, uint8_t* readouts,
-                const uint64_t* readout_base, uint64_t* overlay, void* stream) {
+                const uint64_t* readout_base, uint64_t* overlay, int* work_counter, void* stream) {
   if (n <= 0) return 0;
   ExecView E{p->ins, p->hostops, p->binds, p->recs, p->base_blob, p->const_blob,
                 (const sfg_child*)children, (const sfg_val*)vals, work_base, work,
                 (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, overlay, n};
   if (p->jit_kernel) {
-    cudaError_t e = cudaMemsetAsync(p->jit_next, 0, sizeof(int), S(stream));
+    if (work_counter == nullptr) {
+      g_err = "sfg_execute: the specialized kernel needs a per-launch work counter";
+      return 1;
+    }
+    cudaError_t e = cudaMemsetAsync(work_counter, 0, sizeof(int), S(stream));
     if (e != cudaSuccess) return fail("sfg_execute (jit counter)", e);
-    int* next = p->jit_next;
-    void* args[] = {(void*)&p->P, (void*)&E, (void*)&next};
-    const unsigned grid = blocks_for(n, 128) < (unsigned)p->jit_grid ? blocks_for(n, 128) : (unsigned)p->jit_grid;
-    e = cudaLaunchKernel((const void*)p->jit_kernel, dim3(grid), dim3(128), args, 0, S(stream));
+    int* next = work_counter;
+    int mode = p->jit_mode;
+    void* args[] = {(void*)&p->P, (void*)&E, (void*)&next, (void*)&mode};
+    const unsigned want = blocks_for(n, p->jit_block);
+    const unsigned grid = want < (unsigned)p->jit_grid ? want : (unsigned)p->jit_grid;
+    e = cudaLaunchKernel((const void*)p->jit_kernel, dim3(grid), dim3(p->jit_block), args, 0, S(stream));
     if (e != cudaSuccess) return fail("sfg_execute (jit)", e);
     return 0;
   }

@@ -393,11 +393,25 @@ struct Gen {
     for (int k = 0; k < P.n_kernels; ++k)
       o << "    case " << k << ": return sim_" << k << "(*this, P, L, M, V, pre, ctaid, tid, grid, block, total);\n";
     o << "    default: return RUN_FATAL;\n  }\n}\n\n}  // namespace\n\n";
-    // persistent: every lane fetches its next input independently, so a long input
-    // never holds a whole block's resources while its warp-mates sit idle
-    o << "extern \"C\" __global__ void __launch_bounds__(128, 1) sfg_jit_execute(sfg_prog P, ExecView E, int* next) {\n"
+    // persistent kernel.  mode 0: every lane fetches its next input independently
+    // (a long input never idles its warp-mates); mode 1: a warp fetches 32 consecutive
+    // inputs and re-fetches after all 32 finished (lanes stay in SIMT lockstep while
+    // their inputs follow the same path).
+    o << "extern \"C\" __global__ void __launch_bounds__(128, 1) sfg_jit_execute(sfg_prog P, ExecView E, int* next, int mode) {\n"
          "  JitRunner R;\n"
-         "  for (int i = atomicAdd(next, 1); i < E.n; i = atomicAdd(next, 1)) run_input(P, E, i, R);\n"
+         "  if (mode == 0) {\n"
+         "    for (int i = atomicAdd(next, 1); i < E.n; i = atomicAdd(next, 1)) run_input(P, E, i, R);\n"
+         "    return;\n"
+         "  }\n"
+         "  const int lane = threadIdx.x & 31;\n"
+         "  while (true) {\n"
+         "    int b = 0;\n"
+         "    if (lane == 0) b = atomicAdd(next, 32);\n"
+         "    b = __shfl_sync(0xffffffffu, b, 0);\n"
+         "    if (b >= E.n) break;\n"
+         "    if (b + lane < E.n) run_input(P, E, b + lane, R);\n"
+         "    __syncwarp();\n"
+         "  }\n"
          "}\n";
     return o.str();
   }

@@ -98,6 +98,7 @@ class Slot:
         self.allocs, self.allocs_prefix, self.admit, self.pos = i64(cap), i64(cap), i64(cap), i64(cap)
         self.bytes, self.boff, self.sel, self.dst_off = i64(cap), i64(cap), i32(cap), i64(cap * A)
         self.tmp, self.tot, self.scalars = i64((cap + 2047) // 2048 + 8), i64(16), i32(2)
+        self.counter = i32(1)            # work counter of this slot's execute launch
         self.first, self.kfirst, self.kcount = i32(E), i32(dc.K), i64(dc.K)
         self.counts_base = torch.zeros(C, dtype=torch.int64, device=dev)
         self.pin_tot = torch.empty(16, dtype=torch.int64, pin_memory=True)
@@ -310,7 +311,7 @@ class DeviceCampaign:
         _native.check(self.L.sfg_execute(
             self.h, n, S.children.data_ptr(), S.vals.data_ptr(), S.work_base.data_ptr(), S.work.data_ptr(),
             S.verdicts.data_ptr(), S.ecnt.data_ptr(), _ptr(S.readouts), S.ro_base.data_ptr(), _ptr(S.overlay),
-            st.cuda_stream), "execute")
+            S.counter.data_ptr(), st.cuda_stream), "execute")
         if self.timing:
             ev[1].record(st)
             S.exec_ev = ev

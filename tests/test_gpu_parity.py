@@ -130,3 +130,36 @@ def test_fuzz_loop_api_matches_batched_reference(engine_cls, tmp_path):
     assert (tmp_path / "out" / "findings.txt").read_text() == ref["findings"]
     crashes = sorted(p.name for p in (tmp_path / "out" / "crashes").iterdir())
     assert len(crashes) == len(s.findings)
+
+
+def test_pipelined_equals_sequential_under_overlap(engine_cls):
+    """Rounds of the matmul target run long enough to overlap on the device; the
+    pipelined campaign must equal the one-round-at-a-time campaign bit for bit."""
+    import numpy as np
+    from conftest import workload_manifest
+    from paper_2603_05725_b200.lowering import VERDICT
+    m = workload_manifest("matmul")
+
+    def campaign(depth):
+        dc = engine_cls(m, master_seed=3)
+        digests = []
+
+        def keep(res):
+            v = res.slot.verdicts[:res.executed * VERDICT.itemsize].cpu().numpy()
+            e = res.slot.ecnt[:res.executed * max(dc.E, 1)].cpu().numpy()
+            digests.append(hashlib.sha256(v.tobytes() + e.tobytes()).hexdigest())
+
+        if depth == 1:
+            for k in range(6):
+                keep(dc.run_round(1 + k * 4096, 4096))
+        else:
+            dc.run_rounds(1, 1 + 6 * 4096, 4096, depth=depth, on_round=keep)
+        out = (digests, dc.findings.render_text(), report_to_rec(build_report(dc.coverage_map())),
+               [e[0].id for e in dc.host_entries])
+        dc.close()
+        return out
+
+    seq = campaign(1)
+    pip = campaign(6)
+    assert seq[0] == pip[0]
+    assert seq[1:] == pip[1:]
