@@ -163,3 +163,29 @@ def test_pipelined_equals_sequential_under_overlap(engine_cls):
     pip = campaign(6)
     assert seq[0] == pip[0]
     assert seq[1:] == pip[1:]
+
+
+@pytest.mark.parametrize("stem", ["matmul", "vadd"])
+@pytest.mark.parametrize("depth", [1, 3])
+def test_workloads_match_reference(engine_cls, stem, depth):
+    """C1 (vadd, off-by-one OOB write) and C2 (matmul, stride/size OOB) on the
+    device vs the reference's batched records (tests/golden/ref_workloads.json)."""
+    from conftest import workload_manifest
+    ref = golden("ref_workloads.json")[stem]
+    dc = engine_cls(workload_manifest(stem), master_seed=11)
+    got = []
+    dc.run_rounds(1, 301, 100, depth=depth, on_round=lambda res: got.extend(dc.round_records(res)))
+    assert len(got) == len(ref["records"])
+    for g, w in zip(got, ref["records"]):
+        assert g["parent"] == w["parent"], g["it"]
+        assert _digest(g["child"]) == w["child"], g["it"]
+        assert g["status"] == w["status"], g["it"]
+        assert g["report"] == w["report"], g["it"]
+        assert g["retired"] == w["retired"], g["it"]
+        assert g["allocs"] == w["allocs"], g["it"]
+        assert g["edges"] == w["edges"], g["it"]
+        assert g["admitted"] == w["admitted"], g["it"]
+    assert dc.findings.render_text() == ref["findings"]
+    assert report_to_rec(build_report(dc.coverage_map())) == ref["coverage"]
+    assert [_digest(e[0]) for e in dc.host_entries] == ref["corpus"]
+    dc.close()

@@ -119,3 +119,22 @@ def test_sequential_loop_matches_reference_fuzz_loop(key):
     assert sorted(f"{e.tc.id}.tc" for e in res.corpus) == want["corpus"]
     assert f"stop={res.stop_reason}" in want["summary"]
     assert f"compute_runs={res.executed}" in want["summary"]
+
+
+@pytest.mark.parametrize("stem", ["matmul", "vadd"])
+def test_workloads_batched_matches_reference(stem):
+    """C1/C2 synthetic targets (workloads/*.man): the oracle's batched driver vs
+    the reference's own functions driven the same way (make_golden.py workloads)."""
+    from conftest import workload_manifest
+    ref = golden("ref_workloads.json")[stem]
+    m = workload_manifest(stem)
+    res = ol.batched_loop(m, master_seed=11, iterations=300, round_size=100)
+    assert len(res.records) == len(ref["records"])
+    for got, want in zip(res.records, ref["records"]):
+        assert _digest(got["child"]) == want["child"], got["it"]
+        assert got["report"] == want["report"], got["it"]
+        assert got["retired"] == want["retired"], got["it"]
+        assert got["edges"] == want["edges"], got["it"]
+        assert got["admitted"] == want["admitted"], got["it"]
+    assert res.findings.render_text() == ref["findings"]
+    assert report_to_rec(build_report(res.coverage)) == ref["coverage"]
