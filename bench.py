@@ -145,10 +145,15 @@ def run_ours(a):
     from paper_2603_05725_b200.engine import DeviceCampaign
     from paper_2603_05725_b200.workloads import load
 
+    from paper_2603_05725_b200.shard import RoundComm
+
     m = load(a.workload)
-    R = a.round
     D = a.depth
-    dc = DeviceCampaign(m, master_seed=11 + rank)  # weak scaling: one campaign shard per GPU
+    # one campaign, each global round sharded over the ranks (R inputs per GPU per
+    # round, weak scaling); per-round merge over NCCL
+    comm = RoundComm()
+    R = a.round * world
+    dc = DeviceCampaign(m, master_seed=11, comm=comm)
     dc.timing = True
 
     def all_streams_done(ev):
@@ -182,7 +187,7 @@ def run_ours(a):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max = float(t.item())
-    value = world * executed / t_max
+    value = executed / t_max
     ms = [t_max * 1000 / a.steps]
 
     # ---- end to end through the public round API with host buffers
@@ -193,16 +198,17 @@ def run_ours(a):
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     k3_avg_s = statistics.mean(k3_ms) / 1000.0
     bytes_exec = dc.algorithmic_exec_bytes()
-    achieved = bytes_exec * R / k3_avg_s / 1e9
+    achieved = bytes_exec * a.round / k3_avg_s / 1e9
     retired = dc.retired_mean(results[-1].slot)
+    collectives = comm.calls
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
             "traffic": None, "kernel": "sfg_execute_kernel", "bytes_per_exec": bytes_exec,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
             "note": "execute is SM-issue bound (interpreter); see issue_roofline"}
     sm_mhz = clk.summary().get("sm_mhz") or 1965.0
-    issue = {"sim_instr_per_s": retired * R / k3_avg_s, "sim_instr_per_exec": retired,
+    issue = {"sim_instr_per_s": retired * a.round / k3_avg_s, "sim_instr_per_exec": retired,
              "k3_ms_per_launch": statistics.mean(k3_ms),
-             "rounds_in_flight": D,
+             "rounds_in_flight": D, "soft_cap": dc.soft_cap,
              "lane_instr_peak_per_s": 148 * 4 * 32 * sm_mhz * 1e6}
 
     if rank == 0:
@@ -214,10 +220,12 @@ def run_ours(a):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": t_max * 1000 / a.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "i32/f32", "data": "synthetic",
-                "config": {"workload": WORKLOAD, "round_size": R, "execs_per_step": world * R,
+                "config": {"workload": WORKLOAD, "round_size": R, "execs_per_step": R,
                            "rounds_in_flight": D, "engine": "jit" if dc.jit else "interpreter",
                            "l2": f"inputs larger than L2: {D} rounds in flight hold ~{D * R * 1900 >> 20} MiB of "
-                                 "round buffers (126 MB L2)", "parallelism": f"shard{world}"},
+                                 "round buffers (126 MB L2)", "parallelism": f"shard{world}",
+                           "merge": f"per-round NCCL MIN/SUM all-reduce + all-gather ({collectives} collectives)"
+                           if world > 1 else "none (1 GPU)"},
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(), "roofline": roof,
                 "issue_roofline": issue, "cpu_baseline": cpu}
         print(json.dumps(line))
@@ -230,13 +238,14 @@ def run_e2e(a, dc, torch, R, it, all_streams_done):
     uploaded from pinned host memory before the run and every round's verdict
     records are copied back to pinned host memory as the round is finalized."""
     host = dc.corpus_host_pinned()
-    vers = [torch.empty(R * 112, dtype=torch.uint8, pin_memory=True) for _ in range(a.depth)]
+    r_loc = a.round
+    vers = [torch.empty(r_loc * 112, dtype=torch.uint8, pin_memory=True) for _ in range(a.depth)]
     h2d = sum(t.numel() for t in host)
-    d2h = R * 112
+    d2h = r_loc * 112
 
     def on_round(res):
         with torch.cuda.stream(res.slot.stream):
-            vers[dc.rounds % a.depth].copy_(res.slot.verdicts[:R * 112], non_blocking=True)
+            vers[dc.rounds % a.depth].copy_(res.slot.verdicts[:res.slot.n * 112], non_blocking=True)
 
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
@@ -257,7 +266,7 @@ def main():
     p.add_argument("--steps", type=int, default=16)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--round", type=int, default=65536)
-    p.add_argument("--depth", type=int, default=8, help="rounds in flight (speculative pipelining)")
+    p.add_argument("--depth", type=int, default=16, help="rounds in flight (speculative pipelining)")
     p.add_argument("--workload", default="matmul")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--cpu-seconds", type=float, default=15.0)

@@ -14,7 +14,7 @@
  *          executor.launch / _exec_one     executor.py:390-424, 210-377
  *          sanitizer.check_access          sanitizer.py:145-187
  *          CoverageMap.record_launch/edge  coverage.py:59-71
- *   sfg_triage + sfg_commit
+ *   sfg_triage_stop/absorb/admit + sfg_commit
  *       <- _absorb_iteration    campaign.py:825-846
  *          new_edges_since / merge_from    coverage.py:85-113
  *          FindingsLog.add      sanitizer.py:216-225
@@ -83,17 +83,58 @@ int sfg_apply(const sfg_program* p, const sfg_corpus_dev* c, int n, const void* 
 int sfg_regen(const sfg_program* p, const sfg_corpus_dev* c, int n_sel, const int32_t* sel,
               const void* children, const void* vals, const uint64_t* dst_off, uint8_t* dst,
               void* stream);
-/* work_counter: 4-byte device scratch private to this launch (the persistent
- * specialized kernel hands out inputs from it; concurrent launches need their own). */
+/* work_counter: 4 ints of device scratch private to this launch pair (the
+ * persistent specialized kernel hands out inputs from it; [1] = number of
+ * deferred inputs; concurrent launches need their own).
+ * soft_cap != 0 (specialized kernel only): an input whose retired-instruction
+ * count would reach soft_cap is abandoned and listed in deferred[n]; it is
+ * finished by sfg_execute_deferred, which re-materializes its payload and runs
+ * it from scratch with the real budget.  Results are identical to soft_cap 0;
+ * long inputs then share warps instead of pinning one warp each. */
 int sfg_execute(const sfg_program* p, int n, const void* children, const void* vals,
                 const uint64_t* work_base, uint8_t* work, void* verdicts, uint32_t* edge_counts,
                 uint8_t* readouts, const uint64_t* readout_base, uint64_t* overlay, int* work_counter,
-                void* stream);
-int sfg_triage(const sfg_program* p, int n, const void* verdicts, const uint32_t* edge_counts,
-               const void* children, uint32_t* scalars, uint32_t* first_hit, uint64_t* edge_total,
-               uint32_t* key_first, uint64_t* key_count, uint32_t* entered, uint64_t* allocs,
-               const uint8_t* ghit, uint64_t* admit, void* stream);
-int sfg_commit(const sfg_program* p, const uint64_t* edge_total, uint8_t* ghit, void* stream);
+                uint64_t soft_cap, int32_t* deferred, void* stream);
+int sfg_execute_deferred(const sfg_program* p, const sfg_corpus_dev* c, int n, const void* children,
+                         const void* vals, const uint64_t* work_base, uint8_t* work, void* verdicts,
+                         uint32_t* edge_counts, uint8_t* readouts, const uint64_t* readout_base,
+                         uint64_t* overlay, int* work_counter, int32_t* deferred, void* stream);
+/* Triage in three stream-ordered phases so that a multi-GPU campaign can merge
+ * the per-rank partials between them: a rank owns the global
+ * round indices [i_base, i_base + n).  All indices written are GLOBAL round
+ * indices; "none" is INT32_MAX, so the merge is a signed MIN all-reduce.
+ *   stop:   scalars[0] = min stop-rule finding, scalars[1] = min fatal     -> MIN
+ *   absorb: first_hit[E], key_first[K]                                     -> MIN
+ *           edge_delta[E], key_count[K], entered_cnt[n_kernels]            -> SUM
+ *           allocs[n] (per input, 0 past the stop)   (local; exclusive-scanned)
+ *   admit:  admit[n] = no finding, it != 1, first hitter of an edge unseen
+ *           at the round start (ghit)                                       (local)
+ * sfg_commit folds the merged delta into the campaign map (edge_total,
+ * ghit, entered mask).  Callers fill scalars/first_hit/key_first with
+ * INT32_MAX and zero the SUM buffers before the stop phase. */
+int sfg_triage_stop(const sfg_program* p, int n, int i_base, const void* verdicts, int32_t* scalars,
+                    void* stream);
+int sfg_triage_absorb(const sfg_program* p, int n, int i_base, const void* verdicts,
+                      const uint32_t* edge_counts, const int32_t* scalars, int32_t* first_hit,
+                      uint64_t* edge_delta, int32_t* key_first, uint64_t* key_count,
+                      uint64_t* entered_cnt, uint64_t* allocs, void* stream);
+int sfg_triage_admit(const sfg_program* p, int n, int i_base, const void* verdicts,
+                     const uint32_t* edge_counts, const void* children, const int32_t* scalars,
+                     const int32_t* first_hit, const uint8_t* ghit, uint64_t* admit, void* stream);
+int sfg_commit(const sfg_program* p, const uint64_t* edge_delta, const uint64_t* entered_cnt,
+               uint64_t* edge_total, uint8_t* ghit, uint32_t* entered, void* stream);
+/* Context-sensitive hashed coverage map (derived view; admission stays on exact
+ * edges): every live input (round index <= scalars[0]) sets, per hit edge e, the
+ * byte slot fmix64(edge_ctx[e] ^ bucket(count) * 0x9E3779B97F4A7C15) & (2^map_bits - 1)
+ * of map (2^map_bits bytes, 4-byte aligned); new_slots[0] += slots turned on.
+ * Byte flags: the cross-GPU merge is a MAX all-reduce of map. */
+int sfg_ctxmap(int n, int n_edges, int i_base, const uint32_t* edge_counts, const int32_t* scalars,
+               const uint64_t* edge_ctx, uint8_t* map, int map_bits, uint64_t* new_slots, void* stream);
+/* admitted children (admit/pos from the admit phase + scan) -> contiguous staging
+ * rows (sfg_child, n_args x sfg_val): the records ranks exchange on admission */
+int sfg_select(const sfg_program* p, const void* children, const void* vals, const uint64_t* admit,
+               const uint64_t* pos, int n, void* stage_children, void* stage_vals, void* stream);
+/* admit == NULL: every row counts (staged rows); compact then appends rows 0..n-1 in order */
 int sfg_child_bytes(const sfg_program* p, const void* vals, const uint64_t* admit, int n,
                     uint64_t* bytes, void* stream);
 int sfg_compact(const sfg_program* p, const void* children, const void* vals, const uint64_t* admit,

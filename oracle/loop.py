@@ -204,7 +204,7 @@ def _edges_of(delta: CoverageMap):
 def run_loop(manifest, *, master_seed=1, iterations=1000, batched=True, round_size=256,
              stop_on_first_finding=False, stop_bug_class=None, budget=1_000_000,
              mem_cfg: MemCfg | None = None, max_ops=3, granule=4, redzone=32,
-             window=256, weight=4.0, keep_records=True, extra_seeds=()):
+             window=256, weight=4.0, keep_records=True, extra_seeds=(), fanout=0):
     """Shared body of ``sequential_loop`` / ``batched_loop``."""
     specs = manifest.argspecs
     res = OracleCampaign()
@@ -238,8 +238,13 @@ def run_loop(manifest, *, master_seed=1, iterations=1000, batched=True, round_si
         else:
             s = OracleStream(master_seed, KEYBASE + it) if batched else worker
             pool = round_entries if batched else corpus
-            parent = schedule_next(pool, s, it, window, weight)
-            rec["parent"] = next(i for i, e in enumerate(pool) if e.tc is parent)
+            if fanout:   # fixed fan-out (BASELINE.json configs[3]): no scheduling draw
+                pidx = ((it - 1) // fanout) % len(pool)
+                parent = pool[pidx].tc
+            else:
+                parent = schedule_next(pool, s, it, window, weight)
+                pidx = next(i for i, e in enumerate(pool) if e.tc is parent)
+            rec["parent"] = pidx
             picks = draw_picks(specs, s, max_ops)
             child = finish_child(parent, picks, counts, s, granule, redzone)
         delta = gcov.fresh()

@@ -42,6 +42,7 @@ static_assert(sizeof(sfg_prog) < 4096, "sfg_prog must fit the kernel parameter s
 #include "mutate.cu"
 #include "execute.cu"
 #include "triage.cu"
+#include "ctxmap.cu"
 #include "jit.cu"
 
 static thread_local std::string g_err;
@@ -253,7 +254,7 @@ int sfg_apply(const sfg_program* p, const sfg_corpus_dev* c, int n, const void* 
               const uint64_t* work_base, uint8_t* work, void* stream) {
   if (n <= 0) return 0;
   sfg_apply_kernel<<<blocks_for((int64_t)n * 32, 256), 256, 0, S(stream)>>>(
-      p->P, CV(c), n, (const sfg_child*)children, (const sfg_val*)vals, work_base, work);
+      p->P, CV(c), n, (const sfg_child*)children, (const sfg_val*)vals, work_base, work, nullptr, nullptr);
   SFG_CHECK_LAUNCH("sfg_apply");
   return 0;
 }
@@ -269,17 +270,27 @@ int sfg_regen(const sfg_program* p, const sfg_corpus_dev* c, int n_sel, const in
 
 int sfg_execute(const sfg_program* p, int n, const void* children, const void* vals, const uint64_t* work_base,
                 uint8_t* work, void* verdicts, uint32_t* edge_counts, uint8_t* readouts,
-                const uint64_t* readout_base, uint64_t* overlay, int* work_counter, void* stream) {
-  if (n <= 0) return 0;
+                const uint64_t* readout_base, uint64_t* overlay, int* work_counter, uint64_t soft_cap,
+                int32_t* deferred, void* stream) {
+  if (n <= 0) {
+    if (work_counter) cudaMemsetAsync(work_counter, 0, 4 * sizeof(int), S(stream));
+    return 0;
+  }
   ExecView E{p->ins, p->hostops, p->binds, p->recs, p->base_blob, p->const_blob,
-                (const sfg_child*)children, (const sfg_val*)vals, work_base, work,
-                (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, overlay, n};
+             (const sfg_child*)children, (const sfg_val*)vals, work_base, work,
+             (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, overlay, n,
+             0ull, deferred, work_counter ? work_counter + 1 : nullptr};
   if (p->jit_kernel) {
     if (work_counter == nullptr) {
       g_err = "sfg_execute: the specialized kernel needs a per-launch work counter";
       return 1;
     }
-    cudaError_t e = cudaMemsetAsync(work_counter, 0, sizeof(int), S(stream));
+    if (soft_cap && deferred == nullptr) {
+      g_err = "sfg_execute: soft_cap needs a deferred list";
+      return 1;
+    }
+    E.soft_cap = soft_cap;
+    cudaError_t e = cudaMemsetAsync(work_counter, 0, 4 * sizeof(int), S(stream));
     if (e != cudaSuccess) return fail("sfg_execute (jit counter)", e);
     int* next = work_counter;
     int mode = p->jit_mode;
@@ -290,33 +301,99 @@ int sfg_execute(const sfg_program* p, int n, const void* children, const void* v
     if (e != cudaSuccess) return fail("sfg_execute (jit)", e);
     return 0;
   }
+  if (work_counter) cudaMemsetAsync(work_counter, 0, 4 * sizeof(int), S(stream));
   sfg_execute_kernel<<<blocks_for(n, 128), 128, p->smem, S(stream)>>>(p->P, E);
   SFG_CHECK_LAUNCH("sfg_execute");
   return 0;
 }
 
-int sfg_triage(const sfg_program* p, int n, const void* verdicts, const uint32_t* edge_counts, const void* children,
-               uint32_t* scalars, uint32_t* first_hit, uint64_t* edge_total, uint32_t* key_first,
-               uint64_t* key_count, uint32_t* entered, uint64_t* allocs, const uint8_t* ghit, uint64_t* admit,
-               void* stream) {
-  if (n <= 0) return 0;
-  const sfg_verdict* V = (const sfg_verdict*)verdicts;
-  sfg_stop_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(p->P, V, n, scalars);
-  SFG_CHECK_LAUNCH("sfg_triage/stop");
-  sfg_absorb_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(p->P, V, edge_counts, n, scalars, first_hit,
-                                                              (unsigned long long*)edge_total, key_first,
-                                                              (unsigned long long*)key_count, entered, allocs);
-  SFG_CHECK_LAUNCH("sfg_triage/absorb");
-  sfg_admit_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(p->P, V, edge_counts, (const sfg_child*)children, n,
-                                                             scalars, first_hit, ghit, admit);
-  SFG_CHECK_LAUNCH("sfg_triage/admit");
+int sfg_execute_deferred(const sfg_program* p, const sfg_corpus_dev* c, int n, const void* children,
+                         const void* vals, const uint64_t* work_base, uint8_t* work, void* verdicts,
+                         uint32_t* edge_counts, uint8_t* readouts, const uint64_t* readout_base, uint64_t* overlay,
+                         int* work_counter, int32_t* deferred, void* stream) {
+  if (n <= 0 || !p->jit_kernel) return 0;  // the interpreter never defers
+  // pristine payloads again (the first attempt's stores landed in the work regions)
+  sfg_apply_kernel<<<p->jit_grid, 256, 0, S(stream)>>>(p->P, CV(c), n, (const sfg_child*)children,
+                                                      (const sfg_val*)vals, work_base, work, deferred,
+                                                      work_counter + 1);
+  SFG_CHECK_LAUNCH("sfg_execute_deferred/apply");
+  ExecView E{p->ins, p->hostops, p->binds, p->recs, p->base_blob, p->const_blob,
+             (const sfg_child*)children, (const sfg_val*)vals, work_base, work,
+             (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, overlay, n,
+             0ull, deferred, work_counter + 1};
+  int* next = work_counter + 2;
+  int mode = 2;
+  void* args[] = {(void*)&p->P, (void*)&E, (void*)&next, (void*)&mode};
+  // one-warp CTAs: a warp that holds long inputs pins only its own slot
+  const unsigned grid = (unsigned)p->jit_grid * (unsigned)(p->jit_block / 32);
+  cudaError_t e = cudaLaunchKernel((const void*)p->jit_kernel, dim3(grid), dim3(32), args, 0, S(stream));
+  if (e != cudaSuccess) return fail("sfg_execute_deferred (jit)", e);
   return 0;
 }
 
-int sfg_commit(const sfg_program* p, const uint64_t* edge_total, uint8_t* ghit, void* stream) {
-  sfg_commit_kernel<<<blocks_for(p->P.n_edges, 256), 256, 0, S(stream)>>>(
-      p->P.n_edges, (const unsigned long long*)edge_total, ghit);
+int sfg_triage_stop(const sfg_program* p, int n, int i_base, const void* verdicts, int32_t* scalars,
+                    void* stream) {
+  if (n <= 0) return 0;
+  sfg_stop_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(p->P, (const sfg_verdict*)verdicts, n, i_base, scalars);
+  SFG_CHECK_LAUNCH("sfg_triage_stop");
+  return 0;
+}
+
+int sfg_triage_absorb(const sfg_program* p, int n, int i_base, const void* verdicts, const uint32_t* edge_counts,
+                      const int32_t* scalars, int32_t* first_hit, uint64_t* edge_delta, int32_t* key_first,
+                      uint64_t* key_count, uint64_t* entered_cnt, uint64_t* allocs, void* stream) {
+  if (n <= 0) return 0;
+  sfg_absorb_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(
+      p->P, (const sfg_verdict*)verdicts, edge_counts, n, i_base, scalars, first_hit,
+      (unsigned long long*)edge_delta, key_first, (unsigned long long*)key_count,
+      (unsigned long long*)entered_cnt, allocs);
+  SFG_CHECK_LAUNCH("sfg_triage_absorb");
+  return 0;
+}
+
+int sfg_triage_admit(const sfg_program* p, int n, int i_base, const void* verdicts, const uint32_t* edge_counts,
+                     const void* children, const int32_t* scalars, const int32_t* first_hit, const uint8_t* ghit,
+                     uint64_t* admit, void* stream) {
+  if (n <= 0) return 0;
+  sfg_admit_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(p->P, (const sfg_verdict*)verdicts, edge_counts,
+                                                             (const sfg_child*)children, n, i_base, scalars,
+                                                             first_hit, ghit, admit);
+  SFG_CHECK_LAUNCH("sfg_triage_admit");
+  return 0;
+}
+
+int sfg_commit(const sfg_program* p, const uint64_t* edge_delta, const uint64_t* entered_cnt, uint64_t* edge_total,
+               uint8_t* ghit, uint32_t* entered, void* stream) {
+  const int ne = p->P.n_edges > 0 ? p->P.n_edges : 1;
+  sfg_commit_kernel<<<blocks_for(ne, 256), 256, 0, S(stream)>>>(
+      p->P.n_edges, p->P.n_kernels, (const unsigned long long*)edge_delta, (const unsigned long long*)entered_cnt,
+      (unsigned long long*)edge_total, ghit, entered);
   SFG_CHECK_LAUNCH("sfg_commit");
+  return 0;
+}
+
+int sfg_select(const sfg_program* p, const void* children, const void* vals, const uint64_t* admit,
+               const uint64_t* pos, int n, void* stage_children, void* stage_vals, void* stream) {
+  if (n <= 0) return 0;
+  sfg_select_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(p->P, (const sfg_child*)children,
+                                                              (const sfg_val*)vals, admit, pos, n,
+                                                              (sfg_child*)stage_children, (sfg_val*)stage_vals);
+  SFG_CHECK_LAUNCH("sfg_select");
+  return 0;
+}
+
+int sfg_ctxmap(int n, int n_edges, int i_base, const uint32_t* edge_counts, const int32_t* scalars,
+               const uint64_t* edge_ctx, uint8_t* map, int map_bits, uint64_t* new_slots, void* stream) {
+  if (n <= 0 || n_edges <= 0) return 0;
+  if (map_bits < 2 || map_bits > 34) {
+    g_err = "sfg_ctxmap: map_bits out of range";
+    return 1;
+  }
+  const int64_t total = (int64_t)n * n_edges;
+  sfg_ctxmap_kernel<<<blocks_for(total, 256), 256, 0, S(stream)>>>(
+      n, n_edges, i_base, edge_counts, scalars, edge_ctx, (uint32_t*)map, (1ull << map_bits) - 1,
+      (unsigned long long*)new_slots);
+  SFG_CHECK_LAUNCH("sfg_ctxmap");
   return 0;
 }
 

@@ -74,6 +74,13 @@ struct ExecView {
   const uint64_t* readout_base;
   uint64_t* overlay;           // [n][SFG_OVERLAY] packed (addr << 8 | byte)
   int n;
+  // long-input deferral (specialized kernel only): an input whose retired count
+  // would reach soft_cap is abandoned and appended to deferred[] (count in
+  // *n_deferred); the tail pass re-materializes and re-runs it from scratch with
+  // the real budget, 32 long inputs per warp.  soft_cap 0 = off.
+  uint64_t soft_cap;
+  int32_t* deferred;
+  int* n_deferred;
 };
 
 namespace {
@@ -386,7 +393,7 @@ struct Pre {
   int nr, nf, na;
 };
 
-enum { RUN_EXIT = 0, RUN_FINDING = 1, RUN_BUDGET = 2, RUN_FATAL = 3 };
+enum { RUN_EXIT = 0, RUN_FINDING = 1, RUN_BUDGET = 2, RUN_FATAL = 3, RUN_DEFER = 4 };
 
 // One input's COMPUTE phase (campaign.py:483-561).  Runner supplies the simulated
 // thread execution: begin_input(), run_thread(...) -> RUN_*, flush(row).
@@ -394,6 +401,8 @@ template <class Runner>
 SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R) {
   const sfg_child& ch = E.children[i];
   const sfg_val* cv = E.vals + (size_t)i * P.n_args;
+  uint64_t t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   Lane L;
   Mem M{&E, E.work + E.work_base[i], E.base_blob, E.overlay ? E.overlay + (size_t)i * SFG_OVERLAY : nullptr};
   sfg_verdict V{};
@@ -529,9 +538,14 @@ SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R) {
       for (int tid = 0; tid < op.block && !stop; ++tid) {
         const int rc = R.run_thread(P, op.kernel, L, M, V, pre, ctaid, tid, op.grid, op.block, total_retired);
         if (rc == RUN_BUDGET) { V.status = SFG_ST_BUDGET; stop = true; }
+        else if (rc == RUN_DEFER) { V.status = SFG_ST_DEFERRED; stop = true; }
         else if (rc != RUN_EXIT) stop = true;  // finding (V filled) or fatal (V.status set)
       }
     }
+  }
+  if (V.status == SFG_ST_DEFERRED) {  // nothing of this attempt is kept
+    E.deferred[atomicAdd(E.n_deferred, 1)] = i;
+    return;
   }
   V.retired = total_retired;
   V.allocs = L.nalloc;
@@ -539,6 +553,11 @@ SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R) {
   bool overflow = false;
   R.flush(erow, overflow);
   if (overflow && V.status < SFG_ST_OUT_OF_SPACE) V.status = SFG_ST_COUNTER;
+  uint64_t t_end;
+  uint32_t smid;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  V.where = (uint64_t)(smid & 0xff) | ((t_end - t_start) << 8);
   E.verdicts[i] = V;
 }
 

@@ -327,6 +327,9 @@ struct Gen {
         << Q << " == 1, pk" << Q << "_2 = pok" << Q << " && psp" << Q << " == 2;\n";
     }
     o << "  uint64_t ret = 0; int rc = RUN_EXIT; const uint64_t BUD = P.budget;\n";
+    // fast-path limit: the budget, or the remaining soft cap of the input (deferral)
+    o << "  const uint64_t SOFT = J.soft_cap; const bool SFT = SOFT != 0ull && (SOFT <= total || SOFT - total < BUD);\n";
+    o << "  const uint64_t LIM = SFT ? (SOFT > total ? SOFT - total : 0ull) : BUD;\n";
     o << "  (void)grid; (void)block; (void)ctaid; (void)tid;\n";
     for (int b = 0; b < nb; ++b) {
       const int s0 = starts[b], e = b + 1 < nb ? starts[b + 1] : K.n;
@@ -336,7 +339,8 @@ struct Gen {
       for (int pass = 0; pass < 2; ++pass) {
         const bool slow = pass == 1;
         o << (slow ? "S" : "B") << b << ":\n";
-        if (!slow && checked > 0) o << "  if (ret + " << checked << "ull >= BUD) goto S" << b << ";\n";
+        if (!slow && checked > 0)
+          o << "  if (ret + " << checked << "ull >= LIM) { if (SFT) { rc = RUN_DEFER; goto done; } goto S" << b << "; }\n";
         if (!slow && checked == 0) {
           // a lone exit: nothing to check, the slow copy is identical
         }
@@ -381,7 +385,7 @@ struct Gen {
     edge_ovf_checks = max_edge_events >= 0xFFFFFFFFull;
     const int NE = n_edges > 0 ? n_edges : 1;
     o << "#include \"exec_core.cuh\"\n\nnamespace {\n\n";
-    o << "struct JitRunner {\n  uint32_t ec[" << NE << "];\n  bool ovf;\n"
+    o << "struct JitRunner {\n  uint32_t ec[" << NE << "];\n  bool ovf;\n  uint64_t soft_cap;\n"
       << "  SFG_DEV void begin_input() {\n#pragma unroll\n    for (int e = 0; e < " << NE << "; ++e) ec[e] = 0u;\n    ovf = false;\n  }\n"
       << "  SFG_DEV void flush(uint32_t* row, bool& o) {\n#pragma unroll\n    for (int e = 0; e < " << n_edges
       << "; ++e) row[e] = ec[e];\n    o = ovf;\n  }\n"
@@ -399,6 +403,13 @@ struct Gen {
     // their inputs follow the same path).
     o << "extern \"C\" __global__ void __launch_bounds__(128, 1) sfg_jit_execute(sfg_prog P, ExecView E, int* next, int mode) {\n"
          "  JitRunner R;\n"
+         "  R.soft_cap = E.soft_cap;\n"
+         "  if (mode == 2) {  // tail pass over the deferred inputs, real budget\n"
+         "    R.soft_cap = 0;\n"
+         "    const int nd = *E.n_deferred;\n"
+         "    for (int j = atomicAdd(next, 1); j < nd; j = atomicAdd(next, 1)) run_input(P, E, E.deferred[j], R);\n"
+         "    return;\n"
+         "  }\n"
          "  if (mode == 0) {\n"
          "    for (int i = atomicAdd(next, 1); i < E.n; i = atomicAdd(next, 1)) run_input(P, E, i, R);\n"
          "    return;\n"

@@ -29,6 +29,7 @@ __constant__ uint32_t kArith[6] = {0x3F800000u, 0xBF800000u, 0x3F000000u,
 
 // Stream::weighted_choice over schedule_next's weights (rng.py:61-71).
 __device__ int pick_parent(SfgStream& s, const sfg_prog& P, const CorpusView& C, int64_t it) {
+  if (P.fanout > 0) return (int)(((it - 1) / P.fanout) % C.n);  // fixed fan-out: no draw
   const double x0 = s.random();
   // recent entries are a suffix of the non-seed entries (appended in admission order)
   int lo = C.n_seeds, hi = C.n;
@@ -388,12 +389,17 @@ extern "C" __global__ void sfg_mutate_kernel(sfg_prog P, CorpusView C, int64_t i
 }
 
 // warp per input: parent payloads -> child work region (materialized contents)
+// (sel != nullptr: only the inputs sel[0 .. *sel_n) -- the deferred long inputs
+// re-materialized for the tail pass)
 extern "C" __global__ void sfg_apply_kernel(sfg_prog P, CorpusView C, int n, const sfg_child* children,
-                                            const sfg_val* vals, const uint64_t* work_base, uint8_t* work) {
+                                            const sfg_val* vals, const uint64_t* work_base, uint8_t* work,
+                                            const int32_t* sel, const int* sel_n) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int i = warp; i < n; i += nwarps) {
+  if (sel) n = *sel_n;
+  for (int j = warp; j < n; j += nwarps) {
+    const int i = sel ? sel[j] : j;
     const sfg_child& ch = children[i];
     const int parent = ch.parent < 0 ? 0 : ch.parent;
     const sfg_val* pv = C.vals + (size_t)parent * P.n_args;

@@ -18,7 +18,7 @@ typedef unsigned long uintptr_t;
 #include <stdint.h>
 #endif
 
-#define SFG_ABI_VERSION 1
+#define SFG_ABI_VERSION 2
 
 #define SFG_MAX_ARGS 16      // argspecs per harness
 #define SFG_MAX_OPS 3        // MutationConfig.max_ops ceiling (reference default 3)
@@ -149,7 +149,7 @@ typedef struct sfg_entry {   // 32 bytes: corpus entry metadata
 } sfg_entry;
 
 // execution status
-enum { SFG_ST_OK = 0, SFG_ST_FINDING = 1, SFG_ST_BUDGET = 2,
+enum { SFG_ST_OK = 0, SFG_ST_FINDING = 1, SFG_ST_BUDGET = 2, SFG_ST_DEFERRED = 3,
        SFG_ST_OUT_OF_SPACE = 16, SFG_ST_ZERO_ALLOC = 17, SFG_ST_LANE_RECS = 18,
        SFG_ST_OVERLAY = 19, SFG_ST_COUNTER = 20 };
 enum { SFG_C_SPATIAL_OOB = 0, SFG_C_TEMPORAL_UAF, SFG_C_SPACE_MISMATCH, SFG_C_PROVENANCE_ESCAPE,
@@ -169,7 +169,7 @@ typedef struct sfg_verdict { // 112 bytes
   int32_t launches, allocs;
   uint32_t entered;                           // bit k: kernel k launched
   int32_t key;                                // dedupe slot, -1 none
-  int64_t pad;
+  uint64_t where;                             // diagnostics: SM id (bits 0-7), ns spent (bits 8-63)
 } sfg_verdict;
 
 // program-wide scalars passed by value to every kernel
@@ -202,4 +202,8 @@ typedef struct sfg_prog {
   int32_t diff_readback, stop_first, stop_class, n_copyout_arg;  // stop_class -1: none
   int64_t readout_bytes_fixed;     // sum of named copy_out sizes in COMPUTE
   int8_t copyout_arg[SFG_MAX_ARGS];  // arg refs of COMPUTE `copy_out arg:k`, in script order
+  // parent scheduling: 0 = schedule_next (campaign.py:593-603, one random() draw);
+  // k > 0 = fixed fan-out, input it mutates corpus entry ((it - 1) / k) mod n (no draw;
+  // BASELINE.json configs[3]: k children per seed of a large seed corpus)
+  int32_t fanout;
 } sfg_prog;

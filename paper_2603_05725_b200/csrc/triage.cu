@@ -103,47 +103,57 @@ template __global__ void sfg_scan_apply<uint32_t>(const uint32_t*, int64_t, int,
 template __global__ void sfg_scan_apply<uint64_t>(const uint64_t*, int64_t, int, int, const uint64_t*, uint64_t*, int, int);
 
 // ---- triage
-// stop/fatal: scalars[0] = stop index (UINT32_MAX none), scalars[1] = fatal index
-extern "C" __global__ void sfg_stop_kernel(sfg_prog P, const sfg_verdict* V, int n, uint32_t* scalars) {
+// Indices are GLOBAL round indices g = i_base + i (a rank owns the contiguous
+// slice [i_base, i_base + n) of the round), so the per-rank partials below
+// merge across GPUs with plain MIN / SUM all-reduces; with
+// one GPU i_base = 0 and the reductions are the identity.  "None" is
+// INT32_MAX so that a signed MIN all-reduce is the merge.
+constexpr int32_t kNone = 0x7fffffff;
+
+// scalars[0] = stop index, scalars[1] = first fatal index
+extern "C" __global__ void sfg_stop_kernel(sfg_prog P, const sfg_verdict* V, int n, int i_base, int32_t* scalars) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const sfg_verdict& v = V[i];
-  if (v.status >= SFG_ST_OUT_OF_SPACE) atomicMin(&scalars[1], (uint32_t)i);
-  if (v.status == SFG_ST_FINDING && (P.stop_first || v.bug_class == P.stop_class))
-    atomicMin(&scalars[0], (uint32_t)i);
+  if (v.status >= SFG_ST_OUT_OF_SPACE) atomicMin(&scalars[1], i_base + i);
+  if (v.status == SFG_ST_FINDING && (P.stop_first || v.bug_class == P.stop_class)) atomicMin(&scalars[0], i_base + i);
 }
 
+// per-round partials: first_hit[e] (MIN), edge_delta[e] (SUM), key_first/key_count
+// (MIN/SUM), entered_cnt[kernel] (SUM; > 0 <=> entered), allocs per input
 extern "C" __global__ void sfg_absorb_kernel(sfg_prog P, const sfg_verdict* V, const uint32_t* ecnt, int n,
-                                             const uint32_t* scalars, uint32_t* first_hit,
-                                             unsigned long long* edge_total, uint32_t* key_first,
-                                             unsigned long long* key_count, uint32_t* entered,
+                                             int i_base, const int32_t* scalars, int32_t* first_hit,
+                                             unsigned long long* edge_delta, int32_t* key_first,
+                                             unsigned long long* key_count, unsigned long long* entered_cnt,
                                              uint64_t* allocs_out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;  // every lane stays for the warp collectives
-  const uint32_t stop = scalars[0];
+  const int32_t stop = scalars[0];
   const bool valid = i < n;
-  const bool live = valid && (uint32_t)i <= stop;
+  const int32_t g = i_base + i;
+  const bool live = valid && g <= stop;
   const int lane = threadIdx.x & 31;
   const uint32_t* row = ecnt + (size_t)(valid ? i : 0) * P.n_edges;
   for (int e = 0; e < P.n_edges; ++e) {
     const uint32_t c = valid ? row[e] : 0;
-    const uint32_t fh = __reduce_min_sync(0xffffffffu, c ? (uint32_t)i : 0xffffffffu);
+    const int32_t fh = __reduce_min_sync(0xffffffffu, c ? g : kNone);
     uint64_t s = live ? c : 0;
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) {
-      if (fh != 0xffffffffu) atomicMin(&first_hit[e], fh);
-      if (s) atomicAdd(&edge_total[e], (unsigned long long)s);
+      if (fh != kNone) atomicMin(&first_hit[e], fh);
+      if (s) atomicAdd(&edge_delta[e], (unsigned long long)s);
     }
   }
   uint32_t ent = live ? V[i].entered : 0;
   ent = __reduce_or_sync(0xffffffffu, ent);
-  if (lane == 0 && ent) atomicOr(entered, ent);
+  if (lane == 0)
+    for (uint32_t m = ent; m; m &= m - 1) atomicAdd(&entered_cnt[__ffs(m) - 1], 1ull);
   const int key = live ? V[i].key : -1;
   const unsigned mask = __ballot_sync(0xffffffffu, key >= 0);
   if (key >= 0) {
     const unsigned peers = __match_any_sync(mask, key);
     if (lane == __ffs(peers) - 1) {
-      atomicMin(&key_first[key], (uint32_t)i);
+      atomicMin(&key_first[key], g);
       atomicAdd(&key_count[key], (unsigned long long)__popc(peers));
     }
   }
@@ -151,22 +161,50 @@ extern "C" __global__ void sfg_absorb_kernel(sfg_prog P, const sfg_verdict* V, c
 }
 
 extern "C" __global__ void sfg_admit_kernel(sfg_prog P, const sfg_verdict* V, const uint32_t* ecnt,
-                                            const sfg_child* ch, int n, const uint32_t* scalars,
-                                            const uint32_t* first_hit, const uint8_t* ghit, uint64_t* admit) {
+                                            const sfg_child* ch, int n, int i_base, const int32_t* scalars,
+                                            const int32_t* first_hit, const uint8_t* ghit, uint64_t* admit) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const int32_t g = i_base + i;
   uint64_t a = 0;
-  if ((uint32_t)i <= scalars[0] && V[i].status != SFG_ST_FINDING && ch[i].it != 1) {
+  if (g <= scalars[0] && V[i].status != SFG_ST_FINDING && ch[i].it != 1) {
     const uint32_t* row = ecnt + (size_t)i * P.n_edges;
     for (int e = 0; e < P.n_edges; ++e)
-      if (row[e] && !ghit[e] && first_hit[e] == (uint32_t)i) { a = 1; break; }
+      if (row[e] && !ghit[e] && first_hit[e] == g) { a = 1; break; }
   }
   admit[i] = a;
 }
 
-extern "C" __global__ void sfg_commit_kernel(int n_edges, const unsigned long long* edge_total, uint8_t* ghit) {
+// fold the (merged) round delta into the campaign map: saturating u64 counters
+// (coverage.py:62-71), hit flags, entered-kernel mask
+extern "C" __global__ void sfg_commit_kernel(int n_edges, int n_kernels, const unsigned long long* edge_delta,
+                                             const unsigned long long* entered_cnt, unsigned long long* edge_total,
+                                             uint8_t* ghit, uint32_t* entered) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < n_edges) ghit[e] = edge_total[e] ? 1 : 0;
+  if (e < n_edges) {
+    const unsigned long long t = edge_total[e], d = edge_delta[e];
+    const unsigned long long s = t + d < t ? ~0ull : t + d;
+    edge_total[e] = s;
+    ghit[e] = s ? 1 : 0;
+  }
+  if (e == 0) {
+    uint32_t m = *entered;
+    for (int k = 0; k < n_kernels; ++k)
+      if (entered_cnt[k]) m |= 1u << k;
+    *entered = m;
+  }
+}
+
+// admitted children of this rank, in order, into contiguous staging rows
+// (the rows every rank exchanges when a round admits)
+extern "C" __global__ void sfg_select_kernel(sfg_prog P, const sfg_child* ch, const sfg_val* vals,
+                                             const uint64_t* admit, const uint64_t* pos, int n, sfg_child* st_child,
+                                             sfg_val* st_vals) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || !admit[i]) return;
+  const int j = (int)pos[i];
+  st_child[j] = ch[i];
+  for (int a = 0; a < P.n_args; ++a) st_vals[(size_t)j * P.n_args + a] = vals[(size_t)i * P.n_args + a];
 }
 
 // sizes of admitted children's pristine payloads (per input, 16-aligned per array)
@@ -175,7 +213,7 @@ extern "C" __global__ void sfg_child_bytes_kernel(sfg_prog P, const sfg_val* val
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   uint64_t b = 0;
-  if (admit[i]) {
+  if (!admit || admit[i]) {
     const sfg_val* v = vals + (size_t)i * P.n_args;
     for (int a = 0; a < P.n_args; ++a)
       if (v[a].kind == SFG_V_ARR) b += sfg_align16(v[a].nbytes);
@@ -190,8 +228,8 @@ extern "C" __global__ void sfg_compact_kernel(sfg_prog P, const sfg_child* ch, c
                                               int n, int n_corpus, uint64_t corpus_bytes, sfg_entry* cmeta,
                                               sfg_val* cvals, sfg_child* cchild, int32_t* sel, uint64_t* dst_off) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || !admit[i]) return;
-  const int j = (int)pos[i];
+  if (i >= n || (admit && !admit[i])) return;
+  const int j = admit ? (int)pos[i] : i;
   const int e = n_corpus + j;
   sfg_entry m;
   m.admitted_iteration = ch[i].it;

@@ -21,6 +21,7 @@ bounded below by its longest input) overlap with the bulk of the next ones.
 from __future__ import annotations
 
 import ctypes
+import os
 from collections import deque
 from dataclasses import dataclass
 
@@ -31,13 +32,15 @@ from . import _native
 from .baseline import MemConfig, OutOfSpaceError, build_baseline, record_table
 from .coverage import CoverageMap
 from .findings import FindingsLog
-from .lowering import (CHILD, ENTRY, ST_COUNTER, ST_FINDING, ST_LANE_RECS, ST_OUT_OF_SPACE, ST_OVERLAY,
+from .lowering import (CHILD, ENTRY, ST_COUNTER, MAX_KERNELS, ctx_edge_hashes, ST_FINDING, ST_LANE_RECS, ST_OUT_OF_SPACE, ST_OVERLAY,
                        ST_ZERO_ALLOC, VAL, VERDICT, Lowered, LoweringError, decode_op, decode_verdict,
                        pack_values, unpack_values)
+from .shard import RoundComm, owner_of
 from .testcase import MutationError, TestCase
 
-U32_NONE = 0xFFFFFFFF
+NONE = 0x7FFFFFFF   # "no index" in the triage MIN buffers (sfg.h)
 STATUS = {0: "ok", 1: "finding", 2: "budget"}
+DEFAULT_SOFT_CAP = 1 << 15   # retired instructions before an input moves to the tail pass
 
 
 class CorpusDev(ctypes.Structure):
@@ -73,6 +76,7 @@ class RoundResult:
     """Host-side outcome of one finalized round."""
 
     def __init__(self, it0, n, stop, executed, admitted, new_keys, slot):
+        # global round: inputs it0 .. it0+n-1; stop / executed over all ranks
         self.it0, self.n, self.stop, self.executed = it0, n, stop, executed
         self.n_admitted = admitted
         self.new_keys = new_keys          # [(round index, BugReport)] for keys first seen here
@@ -97,18 +101,31 @@ class Slot:
         self.overlay = i64(cap * 32) if dc.low.overlay else None
         self.allocs, self.allocs_prefix, self.admit, self.pos = i64(cap), i64(cap), i64(cap), i64(cap)
         self.bytes, self.boff, self.sel, self.dst_off = i64(cap), i64(cap), i32(cap), i64(cap * A)
-        self.tmp, self.tot, self.scalars = i64((cap + 2047) // 2048 + 8), i64(16), i32(2)
-        self.counter = i32(1)            # work counter of this slot's execute launch
-        self.first, self.kfirst, self.kcount = i32(E), i32(dc.K), i64(dc.K)
+        self.tmp, self.tot = i64((cap + 2047) // 2048 + 8), i64(16)
+        self.counter = i32(4)            # work counters of this slot's execute launches
+        self.deferred = i32(cap)         # long inputs handed to the tail pass
+        # triage partials (merged across ranks between the phases, sfg.h):
+        # MIN: [stop, fatal, first_hit[E], key_first[K]]; SUM: [edge_delta[E], key_count[K], entered[16]]
+        E0, K0 = dc.E, dc.K
+        self.mins = i32(2 + E0 + K0)
+        self.scalars, self.first, self.kfirst = self.mins[:2], self.mins[2:2 + E0], self.mins[2 + E0:2 + E0 + K0]
+        self.sums = i64(E0 + K0 + MAX_KERNELS)
+        self.edelta, self.kcount, self.ent = self.sums[:E0], self.sums[E0:E0 + K0], self.sums[E0 + K0:]
+        self.small = i64(2)              # [admitted, allocs] of this rank, all-gathered
         self.counts_base = torch.zeros(C, dtype=torch.int64, device=dev)
         self.pin_tot = torch.empty(16, dtype=torch.int64, pin_memory=True)
         self.pin_sc = torch.empty(2, dtype=torch.int32, pin_memory=True)
+        self.pin_gath = torch.empty((dc.comm.world, 2), dtype=torch.int64, pin_memory=True)
         self.work, self.work_cap = None, 0
         self.readouts = None
         self.ev_counts = torch.cuda.Event()
         self.ev_done = torch.cuda.Event()
         self.exec_ev = None
-        self.it0 = self.n = 0
+        self.it0 = self.n = 0            # this rank's slice: global ids it0 .. it0+n-1
+        self.round_it0 = self.round_n = 0  # the whole (global) round
+        self.i_base = 0                  # round index of this rank's first input
+        self.executed = 0                # this rank's inputs at or before the stop
+        self.alloc_base = 0              # alloc id of this rank's first allocation
         self.round_index = -1
 
     def ensure_work(self, nbytes: int, dev):
@@ -121,11 +138,16 @@ class DeviceCampaign:
     def __init__(self, manifest, *, master_seed=1, mem: MemConfig | None = None,
                  mutation: MutationConfig | None = None, budget=1_000_000, window=256, recent_weight=4.0,
                  diff_readback=False, stop_on_first_finding=False, stop_bug_class=None, device=None,
-                 extra_seeds=(), ids_reset_per_input=False):
+                 extra_seeds=(), ids_reset_per_input=False, comm: RoundComm | None = None,
+                 soft_cap: int | None = None, ctx_map_bits: int = 0, fanout: int = 0):
         if not torch.cuda.is_available():
             raise _native.NativeError("no CUDA device: the fuzzing inner loop runs only on the GPU")
         self.L = _native.lib()
         self.dev = torch.device(device or "cuda")
+        self.comm = comm or RoundComm()
+        if soft_cap is None:
+            soft_cap = int(os.environ.get("SFG_SOFT_CAP", DEFAULT_SOFT_CAP))
+        self.soft_cap = soft_cap
         self.manifest = manifest
         self.mem = mem or MemConfig()
         self.mutation = mutation or MutationConfig()
@@ -137,7 +159,8 @@ class DeviceCampaign:
             stop_class = getattr(stop_bug_class, "value", str(stop_bug_class))
         self.low = Lowered(manifest, self.base, mem=self.mem, mutation=self.mutation, master_seed=master_seed,
                            budget=budget, window=window, recent_weight=recent_weight,
-                           diff_readback=diff_readback, stop_first=stop_on_first_finding, stop_class=stop_class)
+                           diff_readback=diff_readback, stop_first=stop_on_first_finding, stop_class=stop_class,
+                           fanout=fanout)
         self.diff = bool(diff_readback)
         self.specs = manifest.argspecs
         self.n_args = len(self.specs)
@@ -162,6 +185,12 @@ class DeviceCampaign:
         self.ghit = torch.zeros(max(self.E, 1), dtype=torch.uint8, device=self.dev)
         self.entered = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.counts_run = torch.zeros(max(self.C, 1), dtype=torch.int64, device=self.dev)
+        # context-sensitive hashed coverage map (derived view, csrc/ctxmap.cu)
+        self.ctx_bits = int(ctx_map_bits)
+        if self.ctx_bits:
+            self.ctx_map = torch.zeros(max(1 << self.ctx_bits, 4), dtype=torch.uint8, device=self.dev)
+            self.edge_ctx = torch.from_numpy(ctx_edge_hashes(self.low, manifest).view(np.int64)).to(self.dev)
+            self.ctx_new = torch.zeros(1, dtype=torch.int64, device=self.dev)
         self.next_alloc_id = self.base.next_id
         self.ids_reset = ids_reset_per_input   # reinit mode: every input gets a fresh image
         self.findings = FindingsLog()
@@ -263,12 +292,16 @@ class DeviceCampaign:
 
     # ---- submit: mutate + execute (speculative on the current corpus) -----------------
     def _submit(self, S: Slot, it0: int, n: int, round_index: int, resubmit: bool = False):
-        L, hp = self.L, self.h
+        """Round ``it0 .. it0+n-1`` (global); this rank mutates and executes its slice."""
+        L, hp, comm = self.L, self.h, self.comm
         st = S.stream
         s = st.cuda_stream
         if it0 + n - 1 >= 2 and self.low.prog["n_mutable"] == 0:
             raise MutationError("no mutable arguments")
-        S.it0, S.n, S.round_index = it0, n, round_index
+        lo, hi = comm.bounds(n)
+        S.round_it0, S.round_n, S.i_base = it0, n, lo
+        S.it0, S.n, S.round_index = it0 + lo, hi - lo, round_index
+        it0, n = S.it0, S.n
         cd = self.corpus_dev()
         C = self.C
         self.launches += 2 + 3 * C
@@ -283,7 +316,10 @@ class DeviceCampaign:
                     st.wait_event(self._last_counts)
                 S.counts_base.copy_(self.counts_run)
                 if C:
-                    self.counts_run[:C] = S.counts_base[:C] + S.tot[8:8 + C]
+                    # rotation counts: picks of earlier slices of the round come first
+                    g = comm.all_gather(S.tot[8:8 + C], st)
+                    S.counts_base[:C] += g[:comm.rank].sum(0)
+                    self.counts_run[:C] += g.sum(0)
                 S.ev_counts.record(st)
                 self._last_counts = S.ev_counts
         _native.check(L.sfg_mutate(hp, ctypes.byref(cd), it0, n, S.prefix.data_ptr(), S.counts_base.data_ptr(),
@@ -300,18 +336,32 @@ class DeviceCampaign:
             S.readouts = None
         _native.check(L.sfg_apply(hp, ctypes.byref(cd), n, S.children.data_ptr(), S.vals.data_ptr(),
                                   S.work_base.data_ptr(), S.work.data_ptr(), s), "apply")
-        self._execute(S, n)
+        self._execute(S, n, self.soft_cap, cd)
 
-    def _execute(self, S: Slot, n: int):
+    def _execute(self, S: Slot, n: int, soft_cap: int = 0, cd=None):
+        """K3: bulk pass (long inputs deferred at ``soft_cap`` retired instructions)
+        then the tail pass over the deferred inputs; results equal soft_cap = 0."""
         self.launches += 1
         st = S.stream
         if self.timing:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             ev[0].record(st)
+        soft = soft_cap if (self.jit and cd is not None) else 0
         _native.check(self.L.sfg_execute(
             self.h, n, S.children.data_ptr(), S.vals.data_ptr(), S.work_base.data_ptr(), S.work.data_ptr(),
             S.verdicts.data_ptr(), S.ecnt.data_ptr(), _ptr(S.readouts), S.ro_base.data_ptr(), _ptr(S.overlay),
-            S.counter.data_ptr(), st.cuda_stream), "execute")
+            S.counter.data_ptr(), soft, S.deferred.data_ptr(), st.cuda_stream), "execute")
+        if soft:
+            if self.timing:
+                evb = torch.cuda.Event(enable_timing=True)
+                evb.record(st)
+                S.bulk_ev = evb
+            self.launches += 2
+            _native.check(self.L.sfg_execute_deferred(
+                self.h, ctypes.byref(cd), n, S.children.data_ptr(), S.vals.data_ptr(), S.work_base.data_ptr(),
+                S.work.data_ptr(), S.verdicts.data_ptr(), S.ecnt.data_ptr(), _ptr(S.readouts),
+                S.ro_base.data_ptr(), _ptr(S.overlay), S.counter.data_ptr(), S.deferred.data_ptr(),
+                st.cuda_stream), "execute_deferred")
         if self.timing:
             ev[1].record(st)
             S.exec_ev = ev
@@ -319,84 +369,129 @@ class DeviceCampaign:
 
     # ---- finalize: triage in order ------------------------------------------------------
     def _finalize(self, S: Slot) -> RoundResult:
-        L, hp, st = self.L, self.h, S.stream
+        """Triage one round: stop -> [MIN] -> absorb -> [MIN, SUM] -> admit ->
+        scans -> [gather] -> corpus append, map commit, findings (sfg.h)."""
+        L, hp, st, comm = self.L, self.h, S.stream, self.comm
         s = st.cuda_stream
-        n, it0 = S.n, S.it0
-        self.launches += 4
+        n, ib = S.n, S.i_base
+        self.launches += 7
         with torch.cuda.stream(st):
             if self._last_done is not None:
                 st.wait_event(self._last_done)
-            S.scalars.fill_(-1)
-            S.first.fill_(-1)
-            S.kfirst.fill_(-1)
-            S.kcount.zero_()
-        _native.check(L.sfg_triage(hp, n, S.verdicts.data_ptr(), S.ecnt.data_ptr(), S.children.data_ptr(),
-                                   S.scalars.data_ptr(), S.first.data_ptr(), self.edge_total.data_ptr(),
-                                   S.kfirst.data_ptr(), S.kcount.data_ptr(), self.entered.data_ptr(),
-                                   S.allocs.data_ptr(), self.ghit.data_ptr(), S.admit.data_ptr(), s), "triage")
+            S.mins.fill_(NONE)
+            S.sums.zero_()
+        vp, ep = S.verdicts.data_ptr(), S.ecnt.data_ptr()
+        _native.check(L.sfg_triage_stop(hp, n, ib, vp, S.scalars.data_ptr(), s), "triage_stop")
+        comm.all_reduce(S.scalars, "min", st)
+        _native.check(L.sfg_triage_absorb(hp, n, ib, vp, ep, S.scalars.data_ptr(), S.first.data_ptr(),
+                                          S.edelta.data_ptr(), S.kfirst.data_ptr(), S.kcount.data_ptr(),
+                                          S.ent.data_ptr(), S.allocs.data_ptr(), s), "triage_absorb")
+        comm.all_reduce(S.mins[2:], "min", st)
+        comm.all_reduce(S.sums, "sum", st)
+        if self.ctx_bits:
+            self.launches += 1
+            _native.check(L.sfg_ctxmap(n, self.E, ib, ep, S.scalars.data_ptr(), self.edge_ctx.data_ptr(),
+                                       self.ctx_map.data_ptr(), self.ctx_bits, self.ctx_new.data_ptr(), s), "ctxmap")
+            comm.all_reduce(self.ctx_map, "max", st)
+        _native.check(L.sfg_triage_admit(hp, n, ib, vp, ep, S.children.data_ptr(), S.scalars.data_ptr(),
+                                         S.first.data_ptr(), self.ghit.data_ptr(), S.admit.data_ptr(), s),
+                      "triage_admit")
         self._scan64(S, S.admit, n, 1, 0, S.pos, 2)
         self._scan64(S, S.allocs, n, 1, 0, S.allocs_prefix, 3)
         with torch.cuda.stream(st):
+            S.small.copy_(S.tot[2:4])
+            gath = comm.all_gather(S.small, st)
             S.pin_sc.copy_(S.scalars, non_blocking=True)
             S.pin_tot.copy_(S.tot, non_blocking=True)
+            S.pin_gath.copy_(gath, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(st)
         ev.synchronize()
-        sc = S.pin_sc.numpy().view(np.uint32)
-        tot = S.pin_tot.numpy().view(np.uint64)
-        stop, fatal = int(sc[0]), int(sc[1])
-        if fatal != U32_NONE and fatal <= stop:
+        stop, fatal = (int(x) for x in S.pin_sc.numpy())
+        gathered = S.pin_gath.numpy().copy()
+        if fatal != NONE and fatal <= stop:
             self._raise_fatal(S, fatal)
-        executed = n if stop == U32_NONE else stop + 1
-        n_adm = int(tot[2])
+        N = S.round_n
+        executed = N if stop == NONE else stop + 1
+        S.executed = max(0, min(S.n, executed - ib))
+        n_adm = int(gathered[:, 0].sum())
         self._round_id0 = self.next_alloc_id
+        S.alloc_base = self.next_alloc_id + int(gathered[:comm.rank, 1].sum())
         if n_adm:
-            self._admit(S, n_adm)
-        _native.check(L.sfg_commit(hp, self.edge_total.data_ptr(), self.ghit.data_ptr(), s), "commit")
-        self.launches += 1
+            self._admit(S, gathered[:, 0])
+        _native.check(L.sfg_commit(hp, S.edelta.data_ptr(), S.ent.data_ptr(), self.edge_total.data_ptr(),
+                                   self.ghit.data_ptr(), self.entered.data_ptr(), s), "commit")
         new_keys = self._absorb_findings(S)
-        self.next_alloc_id += int(tot[3])
+        self.next_alloc_id += int(gathered[:, 1].sum())
         S.ev_done.record(st)
         self._last_done = S.ev_done
         self.rounds += 1
-        return RoundResult(it0, n, None if stop == U32_NONE else stop, executed, n_adm, new_keys, S)
+        return RoundResult(S.round_it0, N, None if stop == NONE else stop, executed, n_adm, new_keys, S)
 
-    def _raise_fatal(self, S: Slot, i):
-        v = _np(S.verdicts[i * VERDICT.itemsize:(i + 1) * VERDICT.itemsize], VERDICT)[0]
-        st = int(v["status"])
+    def _raise_fatal(self, S: Slot, g):
+        """The first fatal input (global round index g) raises the reference's
+        exception on every rank; its owner reads the status."""
+        st = None
+        if S.i_base <= g < S.i_base + S.n:
+            i = g - S.i_base
+            st = int(_np(S.verdicts[i * VERDICT.itemsize:(i + 1) * VERDICT.itemsize], VERDICT)[0]["status"])
+        st = next(x for x in self.comm.all_gather_object(st) if x is not None)
         if st == ST_OUT_OF_SPACE:
-            raise OutOfSpaceError(f"input {i}: allocation does not fit its space")
+            raise OutOfSpaceError(f"input {g}: allocation does not fit its space")
         if st == ST_ZERO_ALLOC:
             raise ValueError("allocation size must be positive")
         raise DeviceFatal({ST_LANE_RECS: "per-input allocation table overflow",
                            ST_OVERLAY: "per-input INIT-buffer write overlay overflow",
                            ST_COUNTER: "per-input edge counter overflow"}.get(st, f"status {st}"))
 
-    def _admit(self, S: Slot, n_adm: int):
-        L, hp, st = self.L, self.h, S.stream
+    def _admit(self, S: Slot, per_rank):
+        """Append the round's admitted children (all ranks, in id order) to the
+        corpus: each rank stages its own rows, the rows are all-gathered, and
+        every rank regenerates the payloads from (parent, ops) on its device."""
+        L, hp, st, comm = self.L, self.h, S.stream, self.comm
         s = st.cuda_stream
-        n = S.n
-        self.launches += 3
-        _native.check(L.sfg_child_bytes(hp, S.vals.data_ptr(), S.admit.data_ptr(), n, S.bytes.data_ptr(), s),
-                      "child_bytes")
-        self._scan64(S, S.bytes, n, 1, 0, S.boff, 4)
+        A = self.n_args
+        CB, VB = CHILD.itemsize, A * VAL.itemsize
+        mine = int(per_rank[comm.rank])
+        T = int(per_rank.sum())
+        mx = int(per_rank.max())
+        self.launches += 1
+        stage = self._u8(max(mx, 1) * (CB + VB))
+        _native.check(L.sfg_select(hp, S.children.data_ptr(), S.vals.data_ptr(), S.admit.data_ptr(),
+                                   S.pos.data_ptr(), S.n, stage.data_ptr(), stage.data_ptr() + max(mx, 1) * CB, s),
+                      "select")
+        with torch.cuda.stream(st):
+            if comm.world > 1:
+                g = comm.all_gather(stage[:max(mx, 1) * (CB + VB)], st)
+                off = max(mx, 1) * CB
+                gch = torch.cat([g[r, :int(c) * CB] for r, c in enumerate(per_rank)])
+                gva = torch.cat([g[r, off:off + int(c) * VB] for r, c in enumerate(per_rank)])
+            else:
+                gch, gva = stage[:mine * CB], stage[max(mx, 1) * CB:max(mx, 1) * CB + mine * VB]
+            gch, gva = gch.contiguous(), gva.contiguous()
+        nb = self._u8(T * 8)
+        boff = torch.empty(max(T, 1), dtype=torch.int64, device=self.dev)
+        self.launches += 1
+        _native.check(L.sfg_child_bytes(hp, gva.data_ptr(), None, T, nb.data_ptr(), s), "child_bytes")
+        self._scan64(S, nb.view(torch.int64), T, 1, 0, boff, 4)
         with torch.cuda.stream(st):
             nbytes = int(S.tot[4].item())
-        self._grow_corpus(max(self.cap, (self.n_corpus + n_adm) * 2),
+        self._grow_corpus(max(self.cap, (self.n_corpus + T) * 2),
                           max(self.data_cap, (self.corpus_bytes + nbytes) * 2))
         cd = self.corpus_dev()
-        _native.check(L.sfg_compact(hp, S.children.data_ptr(), S.vals.data_ptr(), S.admit.data_ptr(),
-                                    S.pos.data_ptr(), S.boff.data_ptr(), n, self.n_corpus, self.corpus_bytes,
-                                    self.c_meta.data_ptr(), self.c_vals.data_ptr(), self.c_child.data_ptr(),
-                                    S.sel.data_ptr(), S.dst_off.data_ptr(), s), "compact")
-        _native.check(L.sfg_regen(hp, ctypes.byref(cd), n_adm, S.sel.data_ptr(), S.children.data_ptr(),
-                                  S.vals.data_ptr(), S.dst_off.data_ptr(), self.c_data.data_ptr(), s), "regen")
+        sel = torch.empty(max(T, 1), dtype=torch.int32, device=self.dev)
+        dst_off = torch.empty(max(T, 1) * A, dtype=torch.int64, device=self.dev)
+        self.launches += 2
+        _native.check(L.sfg_compact(hp, gch.data_ptr(), gva.data_ptr(), None, None, boff.data_ptr(), T,
+                                    self.n_corpus, self.corpus_bytes, self.c_meta.data_ptr(), self.c_vals.data_ptr(),
+                                    self.c_child.data_ptr(), sel.data_ptr(), dst_off.data_ptr(), s), "compact")
+        _native.check(L.sfg_regen(hp, ctypes.byref(cd), T, sel.data_ptr(), gch.data_ptr(), gva.data_ptr(),
+                                  dst_off.data_ptr(), self.c_data.data_ptr(), s), "regen")
         first = self.n_corpus
-        self.n_corpus += n_adm
+        self.n_corpus += T
         self.corpus_bytes += nbytes
         with torch.cuda.stream(st):
             self._mirror_entries(first, self.n_corpus)
-
     def _mirror_entries(self, lo, hi):
         """Build reference TestCase objects for corpus entries [lo, hi)."""
         meta = _np(self.c_meta[lo * ENTRY.itemsize:hi * ENTRY.itemsize], ENTRY)
@@ -415,16 +510,19 @@ class DeviceCampaign:
                                       int(meta[j]["admitted_iteration"]), False))
             self.max_entry_work = max(self.max_entry_work, self._entry_work_bound(row))
 
-    def _id_base(self, prefix: int) -> int:
-        return self.base.next_id if self.ids_reset else self._round_id0 + prefix
+    def _id_base(self, S: Slot, prefix: int) -> int:
+        return self.base.next_id if self.ids_reset else S.alloc_base + prefix
 
     def _absorb_findings(self, S: Slot):
+        """FindingsLog updates of a round: hit counts of known keys; new keys are
+        decoded by the rank owning their first input and shared with all ranks."""
+        comm = self.comm
         with torch.cuda.stream(S.stream):
             kc = S.kcount.cpu().numpy()
             hot = np.nonzero(kc)[0]
             if not len(hot):
                 return []
-            kf = S.kfirst.cpu().numpy().view(np.uint32)
+            kf = S.kfirst.cpu().numpy()
             fresh = []
             for k in hot:
                 ks = self.key_strings.get(int(k))
@@ -433,16 +531,22 @@ class DeviceCampaign:
                 else:
                     fresh.append((int(kf[k]), int(k)))
             fresh.sort()
-            out = []
-            if fresh:
-                idx = torch.tensor([i for i, _ in fresh], dtype=torch.long, device=self.dev)
+            mine = [(g, k) for g, k in fresh if S.i_base <= g < S.i_base + S.n]
+            reps = []
+            if mine:
+                idx = torch.tensor([g - S.i_base for g, _ in mine], dtype=torch.long, device=self.dev)
                 vt = _np(S.verdicts.view(-1, VERDICT.itemsize)[idx].reshape(-1), VERDICT)
                 ap = S.allocs_prefix[idx].cpu().numpy()
-                for j, (i, k) in enumerate(fresh):
-                    rep = decode_verdict(vt[j], self.low, S.it0 + i, self._id_base(int(ap[j])))
-                    self.key_strings[k] = rep.dedupe_key
-                    self.findings.add_many(rep, int(kc[k]))
-                    out.append((i, rep))
+                for j, (g, k) in enumerate(mine):
+                    reps.append((g, k, decode_verdict(vt[j], self.low, S.round_it0 + g,
+                                                      self._id_base(S, int(ap[j])))))
+            if comm.world > 1:
+                reps = sorted(r for part in comm.all_gather_object(reps) for r in part)
+            out = []
+            for g, k, rep in reps:
+                self.key_strings[k] = rep.dedupe_key
+                self.findings.add_many(rep, int(kc[k]))
+                out.append((g, rep))
             return out
 
     # ---- public round API --------------------------------------------------------------
@@ -490,7 +594,7 @@ class DeviceCampaign:
                 redo = list(inflight)
                 inflight.clear()
                 for kk, SS in redo:
-                    self._submit(SS, SS.it0, SS.n, SS.round_index, resubmit=True)
+                    self._submit(SS, SS.round_it0, SS.round_n, SS.round_index, resubmit=True)
                     inflight.append((kk, SS))
             if nxt < len(plan):
                 submit(nxt)
@@ -529,6 +633,11 @@ class DeviceCampaign:
         return float(v["retired"].astype(np.float64).mean())
 
     # ---- views for tests / reporting ----------------------------------------------------
+    def ctx_map_slots(self) -> np.ndarray:
+        """Set slots of the context-sensitive hashed map (sorted indices)."""
+        self.drain()
+        return torch.nonzero(self.ctx_map).flatten().cpu().numpy()
+
     def coverage_map(self) -> CoverageMap:
         self.drain()
         cov = CoverageMap.for_program(self.manifest.program)
@@ -553,7 +662,7 @@ class DeviceCampaign:
     def round_records(self, res: RoundResult):
         """Per-input records of a finalized round (same shape as oracle.loop records)."""
         S = res.slot
-        n = res.executed
+        n = S.executed                    # this rank's inputs up to the stop
         self.drain()
         chld = _np(S.children[:n * CHILD.itemsize], CHILD)
         verd = _np(S.verdicts[:n * VERDICT.itemsize], VERDICT)
@@ -566,7 +675,7 @@ class DeviceCampaign:
         for i in range(n):
             c, v = chld[i], verd[i]
             st = int(v["status"])
-            rep = decode_verdict(v, self.low, int(c["it"]), self._id_base(int(aprefix[i]))) if st == ST_FINDING else None
+            rep = decode_verdict(v, self.low, int(c["it"]), self._id_base(S, int(aprefix[i]))) if st == ST_FINDING else None
             recs.append({"it": int(c["it"]), "parent": int(c["parent"]), "child": tcs[i],
                          "status": STATUS.get(st, f"fatal{st}"), "retired": int(v["retired"]),
                          "allocs": int(v["allocs"]), "edges": self._edges_row(ecnt[i]),

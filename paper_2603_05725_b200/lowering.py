@@ -72,7 +72,7 @@ VERDICT = np.dtype([("status", "<i4"), ("bug_class", "<i4"), ("kernel", "<i4"), 
                     ("addr_lo", "<i8"), ("addr_hi", "<i8"), ("is_store", "u1"), ("space", "u1"), ("mech", "u1"),
                     ("alloc_state", "u1"), ("prov", "<i4"), ("alloc", "<i4"), ("label", "<i4"),
                     ("alloc_base", "<i8"), ("alloc_size", "<i8"), ("retired", "<u8"), ("launches", "<i4"),
-                    ("allocs", "<i4"), ("entered", "<u4"), ("key", "<i4"), ("pad", "<i8")], align=True)
+                    ("allocs", "<i4"), ("entered", "<u4"), ("key", "<i4"), ("where", "<u8")], align=True)
 PROG = np.dtype([
     ("space_size", "<i8", (3,)), ("scope_size", "<i8", (3,)), ("qcap", "<i8", (3,)),
     ("granule", "<i4"), ("redzone", "<i4"), ("cursor", "<i8", (3,)), ("qbytes", "<i8", (3,)),
@@ -87,7 +87,7 @@ PROG = np.dtype([
     ("max_ops", "<i4"), ("mut_granule", "<i4"), ("mut_redzone", "<i4"), ("window", "<i4"),
     ("recent_weight", "<f8"), ("master_seed", "<u8"), ("keybase", "<u8"), ("budget", "<u8"),
     ("diff_readback", "<i4"), ("stop_first", "<i4"), ("stop_class", "<i4"), ("n_copyout_arg", "<i4"),
-    ("readout_bytes_fixed", "<i8"), ("copyout_arg", "i1", (MAX_ARGS,))], align=True)
+    ("readout_bytes_fixed", "<i8"), ("copyout_arg", "i1", (MAX_ARGS,)), ("fanout", "<i4")], align=True)
 
 LAYOUTS = {"ins": INS, "kernel": KERNEL, "hostop": HOSTOP, "binding": BINDING, "rec": REC, "val": VAL,
            "op": OP, "child": CHILD, "entry": ENTRY, "verdict": VERDICT, "prog": PROG}
@@ -289,7 +289,7 @@ class Lowered:
     """Everything the device needs for one harness + campaign configuration."""
 
     def __init__(self, manifest, baseline, *, mem, mutation, master_seed, budget, window, recent_weight,
-                 diff_readback=False, stop_first=False, stop_class=None):
+                 diff_readback=False, stop_first=False, stop_class=None, fanout=0):
         self.manifest = manifest
         prog = manifest.program
         specs = manifest.argspecs
@@ -439,6 +439,7 @@ class Lowered:
         if mutation.max_ops > MAX_OPS:
             raise LoweringError(f"max_ops > {MAX_OPS}")
         P["window"], P["recent_weight"] = window, float(recent_weight)
+        P["fanout"] = int(fanout)
         P["master_seed"], P["keybase"], P["budget"] = master_seed & ((1 << 64) - 1), KEYBASE, budget
         P["diff_readback"], P["stop_first"] = int(diff_readback), int(stop_first)
         P["stop_class"] = -1 if stop_class is None else [c.value for c in CLASS_BY_CODE].index(stop_class)
@@ -595,3 +596,48 @@ def decode_verdict(v, low: Lowered, iteration: int, id_base: int) -> BugReport:
                      int(v["alloc_base"]) if alloc is not None else 0,
                      int(v["alloc_size"]) if alloc is not None else 0,
                      ("LIVE", "FREED")[state] if (alloc is not None and state < 2) else "", iteration)
+
+
+# ---- context-sensitive hashed coverage map (csrc/ctxmap.cu) ----
+
+CTX_GOLDEN = 0x9E3779B97F4A7C15
+_M64 = (1 << 64) - 1
+
+
+def fmix64(k: int) -> int:
+    k &= _M64
+    k ^= k >> 33
+    k = (k * 0xFF51AFD7ED558CCD) & _M64
+    k ^= k >> 33
+    k = (k * 0xC4CEB9FE1A85EC53) & _M64
+    return k ^ (k >> 33)
+
+
+def hit_bucket(c: int) -> int:
+    """AFL hit-count class: 1, 2, 3, 4-7, 8-15, 16-31, 32-127, 128+ -> 1..8."""
+    if c <= 3:
+        return c
+    for b, hi in ((4, 8), (5, 16), (6, 32), (7, 128)):
+        if c < hi:
+            return b
+    return 8
+
+
+def ctx_edge_hashes(low: "Lowered", manifest) -> np.ndarray:
+    """Per dense edge: hash of (calling context, kernel, src, dst).  The calling
+    context of a kernel is the launch chain of the COMPUTE phase up to its first
+    launch (SIR has no call instruction)."""
+    import hashlib
+    chain = [op.kernel for op in manifest.phases[COMPUTE] if op.kind == "launch"]
+    out = np.zeros(max(len(low.edge_names), 1), np.uint64)
+    for e, (name, (a, b)) in enumerate(low.edge_names):
+        ctx = chain[:chain.index(name) + 1] if name in chain else [name]
+        h = 0x6A09E667F3BCC908
+        for k in ctx:
+            h = fmix64(h ^ int.from_bytes(hashlib.sha256(k.encode()).digest()[:8], "little"))
+        out[e] = fmix64(h ^ (((a & 0xFFFFFFFF) << 32) | (b & 0xFFFFFFFF)))
+    return out
+
+
+def ctx_slot(edge_hash: int, count: int, bits: int) -> int:
+    return fmix64(int(edge_hash) ^ ((hit_bucket(count) * CTX_GOLDEN) & _M64)) & ((1 << bits) - 1)

@@ -276,3 +276,49 @@ def parse_testcase(text: str, specs=None):
     if "id" in meta and meta["id"] != tc.id:
         raise MutationError("testcase id does not match its content")
     return tc, extra
+
+
+# ---- seed corpora ------------------------------------------------------------------------
+
+
+class Stream:
+    """Keyed random stream with the reference's semantics (rng.py:20-117: numpy's
+    ``Generator`` over ``Philox`` keyed ``(seed, stream_id)``).  Host-side only
+    (seed corpora); the device restates the same generator in csrc/philox.cuh."""
+
+    def __init__(self, seed: int, stream_id: int = 0):
+        import numpy as np
+        self._gen = np.random.Generator(np.random.Philox(
+            key=np.array([seed & 0xFFFFFFFFFFFFFFFF, stream_id & 0xFFFFFFFFFFFFFFFF], dtype=np.uint64)))
+
+    def integers(self, lo: int, hi: int) -> int:
+        return int(self._gen.integers(lo, hi))
+
+    def random(self) -> float:
+        return float(self._gen.random())
+
+    def u64(self) -> int:
+        import numpy as np
+        return int(self._gen.integers(0, 1 << 64, dtype=np.uint64))
+
+
+def sample_valid_testcase(specs, rng: Stream) -> TestCase:
+    """Uniform draw from every argument's declared valid domain, draw for draw
+    as the reference (mutation.py:533-554); used to build large seed corpora
+    (BASELINE.json configs[3])."""
+    import struct
+    args = []
+    for spec in specs:
+        if spec.kind == ScalarType.I32:
+            args.append(IntValue(rng.integers(spec.lo, spec.hi + 1)))
+        elif spec.kind == ScalarType.F32:
+            args.append(FloatValue.from_float(spec.flo + rng.random() * (spec.fhi - spec.flo)))
+        else:
+            if spec.elem == "f32":
+                span = spec.fhi - spec.flo
+                data = b"".join(struct.pack("<I", f32_bits(spec.flo + rng.random() * span))
+                                for _ in range(spec.count))
+            else:
+                data = b"".join(struct.pack("<i", rng.integers(spec.lo, spec.hi + 1)) for _ in range(spec.count))
+            args.append(ArrayValue(data, spec.elem, spec.extents or (spec.count,), spec.space))
+    return TestCase(tuple(args), rng.u64())

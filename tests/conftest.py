@@ -54,3 +54,17 @@ def cuda_ok():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return True
+
+
+WORKLOADS = ("matmul", "vadd", "ctxchain", "structcfg")
+
+
+def workload_case(stem: str):
+    """(manifest, campaign kwargs, round size, iterations) of a golden workload
+    campaign (tests/golden/make_golden.py workloads)."""
+    from paper_2603_05725_b200.testcase import parse_testcase
+    m = workload_manifest(stem)
+    if stem == "structcfg":
+        seeds = tuple(parse_testcase(t)[0] for t in golden("ref_workloads.json")[stem]["seeds"])
+        return m, {"extra_seeds": seeds, "fanout": 8}, 1600, 3200
+    return m, {}, 100, 300

@@ -126,12 +126,15 @@ def sampled():
 
 
 def batched(m, *, master_seed, iterations, round_size, stop_bug_class=None,
-            stop_on_first_finding=False):
-    """Batched-round contract on the reference's own functions."""
+            stop_on_first_finding=False, extra_seeds=(), fanout=0):
+    """Batched-round contract on the reference's own functions.  fanout > 0: input
+    it mutates round-corpus entry ((it - 1) // fanout) % len (no scheduling draw)."""
     specs = m.argspecs
     seed_tc = m.seed(master_seed)
     corpus = rc.Corpus()
     corpus.add_seed(seed_tc)
+    for tc in extra_seeds:
+        corpus.add_seed(tc)
     findings = rc.FindingsLog()
     gcov = CoverageMap.for_program(m.program)
     sched = MutationSchedule()
@@ -153,8 +156,12 @@ def batched(m, *, master_seed, iterations, round_size, stop_bug_class=None,
             child, pidx = seed_tc, -1
         else:
             s = Stream(master_seed, KEYBASE + it)
-            parent = rc.schedule_next(round_corpus, s, it)
-            pidx = next(i for i, e in enumerate(round_corpus.entries) if e.tc is parent)
+            if fanout:
+                pidx = ((it - 1) // fanout) % len(round_corpus.entries)
+                parent = round_corpus.entries[pidx].tc
+            else:
+                parent = rc.schedule_next(round_corpus, s, it)
+                pidx = next(i for i, e in enumerate(round_corpus.entries) if e.tc is parent)
             child = mutate_testcase(parent, specs, sched, s)
         delta = gcov.fresh()
         first = image._next_alloc_id
@@ -212,12 +219,26 @@ def fuzzloops(tmp):
     return out
 
 
+STRUCT_SEEDS = 199          # + the manifest seed = 200 corpus entries
+STRUCT_SEED_KEY = 7 << 40   # sample_valid_testcase(specs, Stream(11, STRUCT_SEED_KEY + k))
+
+
+def struct_seeds(m, n=STRUCT_SEEDS, master_seed=11):
+    return [sample_valid_testcase(m.argspecs, Stream(master_seed, STRUCT_SEED_KEY + k)) for k in range(n)]
+
+
 def workloads():
     wdir = REPO / "paper_2603_05725_b200" / "workloads"
     out = {}
     for man in sorted(wdir.glob("*.man")):
         m = rc.load_harness(man)
-        out[man.stem] = batched(m, master_seed=11, iterations=300, round_size=100)
+        if man.stem == "structcfg":   # C4: seed corpus + 8 children per seed, two rounds
+            seeds = struct_seeds(m)
+            out[man.stem] = batched(m, master_seed=11, iterations=3200, round_size=1600,
+                                    extra_seeds=seeds, fanout=8)
+            out[man.stem]["seeds"] = [serialize_testcase(t) for t in seeds]
+        else:
+            out[man.stem] = batched(m, master_seed=11, iterations=300, round_size=100)
     return out
 
 

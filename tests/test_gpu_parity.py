@@ -165,16 +165,21 @@ def test_pipelined_equals_sequential_under_overlap(engine_cls):
     assert seq[1:] == pip[1:]
 
 
-@pytest.mark.parametrize("stem", ["matmul", "vadd"])
-@pytest.mark.parametrize("depth", [1, 3])
-def test_workloads_match_reference(engine_cls, stem, depth):
-    """C1 (vadd, off-by-one OOB write) and C2 (matmul, stride/size OOB) on the
-    device vs the reference's batched records (tests/golden/ref_workloads.json)."""
-    from conftest import workload_manifest
+@pytest.mark.parametrize("stem", ["matmul", "vadd", "ctxchain", "structcfg"])
+@pytest.mark.parametrize("depth,soft_cap", [(1, None), (3, None), (3, 0), (2, 300)])
+def test_workloads_match_reference(engine_cls, stem, depth, soft_cap):
+    """C1 (vadd, off-by-one OOB write), C2 (matmul, stride/size OOB), C3 (3-launch
+    chain, OOB + use-after-free) and C4 (struct argument, 200-seed corpus, fixed
+    fan-out 8) on the device vs the reference's batched records
+    (tests/golden/ref_workloads.json).  soft_cap: long inputs deferred to the tail
+    pass (None = default, 0 = off, 300 = most inputs deferred) -- the results must
+    not depend on it."""
+    from conftest import workload_case
     ref = golden("ref_workloads.json")[stem]
-    dc = engine_cls(workload_manifest(stem), master_seed=11)
+    m, kw, R, iters = workload_case(stem)
+    dc = engine_cls(m, master_seed=11, soft_cap=soft_cap, **kw)
     got = []
-    dc.run_rounds(1, 301, 100, depth=depth, on_round=lambda res: got.extend(dc.round_records(res)))
+    dc.run_rounds(1, iters + 1, R, depth=depth, on_round=lambda res: got.extend(dc.round_records(res)))
     assert len(got) == len(ref["records"])
     for g, w in zip(got, ref["records"]):
         assert g["parent"] == w["parent"], g["it"]
@@ -188,4 +193,48 @@ def test_workloads_match_reference(engine_cls, stem, depth):
     assert dc.findings.render_text() == ref["findings"]
     assert report_to_rec(build_report(dc.coverage_map())) == ref["coverage"]
     assert [_digest(e[0]) for e in dc.host_entries] == ref["corpus"]
+    dc.close()
+
+
+def test_context_sensitive_map(engine_cls):
+    """C3: the 16 MiB context-sensitive hashed map (derived view) equals the map
+    recomputed from the reference's per-input edge counts."""
+    from conftest import workload_manifest
+    from paper_2603_05725_b200.lowering import ctx_edge_hashes, ctx_slot
+    ref = golden("ref_workloads.json")["ctxchain"]
+    m = workload_manifest("ctxchain")
+    dc = engine_cls(m, master_seed=11, ctx_map_bits=24)
+    dc.run_rounds(1, 301, 100, depth=2)
+    hashes = ctx_edge_hashes(dc.low, m)
+    index = {(name, tuple(e)): j for j, (name, e) in enumerate(dc.low.edge_names)}
+    want = sorted({ctx_slot(hashes[index[(k, (a, b))]], c, 24)
+                   for r in ref["records"] for k, es in r["edges"].items() for a, b, c in es})
+    assert dc.ctx_map_slots().tolist() == want
+    assert int(dc.ctx_new.item()) == len(want)
+    assert report_to_rec(build_report(dc.coverage_map())) == ref["coverage"]
+    dc.close()
+
+
+def test_struct_corpus_full_size_prefix(engine_cls):
+    """C4 at full size: a 10,000-seed corpus (sample_valid_testcase), 64 children
+    per seed, one round of 640,000 inputs on the device; the first 256 inputs
+    (records are prefix-consistent within a round) equal the CPU oracle's."""
+    from conftest import workload_manifest
+    from oracle.loop import batched_loop
+    from paper_2603_05725_b200.testcase import Stream, sample_valid_testcase
+    m = workload_manifest("structcfg")
+    seeds = tuple(sample_valid_testcase(m.argspecs, Stream(11, (7 << 40) + k)) for k in range(9999))
+    R = 10_000 * 64
+    dc = engine_cls(m, master_seed=11, extra_seeds=seeds, fanout=64)
+    res = dc.run_round(1, R)
+    assert res.executed == R
+    got = dc.round_records(res)[:256]
+    ref = batched_loop(m, master_seed=11, iterations=256, round_size=R, extra_seeds=seeds, fanout=64).records
+    for g, w in zip(got, ref):
+        assert g["parent"] == w["parent"], g["it"]
+        assert g["child"].id == w["child"].id, g["it"]
+        assert g["report"] == w["report"], g["it"]
+        assert g["retired"] == w["retired"], g["it"]
+        assert g["edges"] == w["edges"], g["it"]
+        assert g["admitted"] == w["admitted"], g["it"]
     dc.close()

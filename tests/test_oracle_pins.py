@@ -121,16 +121,17 @@ def test_sequential_loop_matches_reference_fuzz_loop(key):
     assert f"compute_runs={res.executed}" in want["summary"]
 
 
-@pytest.mark.parametrize("stem", ["matmul", "vadd"])
+@pytest.mark.parametrize("stem", ["matmul", "vadd", "ctxchain", "structcfg"])
 def test_workloads_batched_matches_reference(stem):
-    """C1/C2 synthetic targets (workloads/*.man): the oracle's batched driver vs
+    """C1-C4 synthetic targets (workloads/*.man): the oracle's batched driver vs
     the reference's own functions driven the same way (make_golden.py workloads)."""
-    from conftest import workload_manifest
+    from conftest import workload_case
     ref = golden("ref_workloads.json")[stem]
-    m = workload_manifest(stem)
-    res = ol.batched_loop(m, master_seed=11, iterations=300, round_size=100)
+    m, kw, R, iters = workload_case(stem)
+    res = ol.batched_loop(m, master_seed=11, iterations=iters, round_size=R, **kw)
     assert len(res.records) == len(ref["records"])
     for got, want in zip(res.records, ref["records"]):
+        assert got["parent"] == want["parent"], got["it"]
         assert _digest(got["child"]) == want["child"], got["it"]
         assert got["report"] == want["report"], got["it"]
         assert got["retired"] == want["retired"], got["it"]
@@ -138,3 +139,4 @@ def test_workloads_batched_matches_reference(stem):
         assert got["admitted"] == want["admitted"], got["it"]
     assert res.findings.render_text() == ref["findings"]
     assert report_to_rec(build_report(res.coverage)) == ref["coverage"]
+    assert [_digest(e.tc) for e in res.corpus] == ref["corpus"]
