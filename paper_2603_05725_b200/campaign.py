@@ -181,15 +181,19 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
                                      f"bug_class:{getattr(want, 'value', want)}")
 
             on_round.mirrored = len(dc.host_entries)
-            it = rng_.start
-            while it < rng_.stop and state["stop"] is None:
+            clock = {"expired": False}
+
+            def should_continue():
+                # wall-clock limit checked before every round submission (campaign.py:733-735);
+                # rounds already in flight are finalized
                 if deadline is not None and time.perf_counter() > deadline:
-                    stop_reason = "wall_clock"
-                    break
-                # bounded chunks so the wall-clock check runs between batches of rounds
-                chunk_stop = min(rng_.stop, it + config.round_size * config.pipeline_depth)
-                dc.run_rounds(it, chunk_stop, config.round_size, depth=config.pipeline_depth, on_round=on_round)
-                it = chunk_stop
+                    clock["expired"] = True
+                return not clock["expired"]
+
+            dc.run_rounds(rng_.start, rng_.stop, config.round_size, depth=config.pipeline_depth,
+                          on_round=on_round, should_continue=should_continue)
+            if clock["expired"] and state["stop"] is None:
+                stop_reason = "wall_clock"
             if state["stop"] is not None:
                 stop_reason = state["stop"]
             if config.mode == "amortized":

@@ -13,7 +13,10 @@ struct sfg_program {
   sfg_prog P;
   cudaLibrary_t jit_lib = nullptr;    // specialized execute kernel (jit.cu), if built
   cudaKernel_t jit_kernel = nullptr;
+  cudaKernel_t jit_tail = nullptr;    // tail pass over deferred long inputs (one-warp CTAs)
   int jit_grid = 0;                   // resident CTAs (occupancy x SMs)
+  int tail_grid = 0;                  // resident one-warp tail CTAs
+  int tail_k = 1;                     // long inputs per tail warp
   int jit_block = 128;                // CTA size of the persistent kernel
   int jit_mode = 1;                   // 0 per-lane fetch, 1 per-warp batches
   std::string jit_source, jit_log;
@@ -154,7 +157,7 @@ int sfg_program_create(const void* prog, size_t prog_bytes, const void* ins, siz
         events = (ev + (double)events >= 1.8e19) ? ~0ull : events + (uint64_t)ev;
       }
     const int rc = sfg_jit_build(p->P, (const sfg_ins*)ins, events, p->jit_source, p->jit_log, &p->jit_lib,
-                                 &p->jit_kernel);
+                                 &p->jit_kernel, &p->jit_tail);
     if (rc != 0) {
       g_err = "sfg_program_create: JIT build failed (" + std::to_string(rc) + "): " + p->jit_log.substr(0, 6000);
       sfg_program_destroy(p);
@@ -168,6 +171,10 @@ int sfg_program_create(const void* prog, size_t prog_bytes, const void* ins, siz
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)p->jit_kernel, p->jit_block, 0);
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
     p->jit_grid = sms * per_sm;
+    if (const char* tk = getenv("SFG_TAIL_K")) p->tail_k = atoi(tk) >= 1 && atoi(tk) <= 32 ? atoi(tk) : 1;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)p->jit_tail, 32, 0);
+    if (e != cudaSuccess || per_sm < 1) per_sm = 1;
+    p->tail_grid = sms * per_sm;
 
   }
   e = cudaFuncSetAttribute(sfg_execute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem);
@@ -322,11 +329,10 @@ int sfg_execute_deferred(const sfg_program* p, const sfg_corpus_dev* c, int n, c
              (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, overlay, n,
              0ull, deferred, work_counter + 1};
   int* next = work_counter + 2;
-  int mode = 2;
-  void* args[] = {(void*)&p->P, (void*)&E, (void*)&next, (void*)&mode};
+  int k = p->tail_k;
+  void* args[] = {(void*)&p->P, (void*)&E, (void*)&next, (void*)&k};
   // one-warp CTAs: a warp that holds long inputs pins only its own slot
-  const unsigned grid = (unsigned)p->jit_grid * (unsigned)(p->jit_block / 32);
-  cudaError_t e = cudaLaunchKernel((const void*)p->jit_kernel, dim3(grid), dim3(32), args, 0, S(stream));
+  cudaError_t e = cudaLaunchKernel((const void*)p->jit_tail, dim3((unsigned)p->tail_grid), dim3(32), args, 0, S(stream));
   if (e != cudaSuccess) return fail("sfg_execute_deferred (jit)", e);
   return 0;
 }

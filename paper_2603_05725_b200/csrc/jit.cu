@@ -381,6 +381,8 @@ struct Gen {
     o << "done:\n  total += ret;\n  return rc;\n}\n\n";
   }
 
+  int tail_minb = 8;
+
   std::string run(int n_edges, uint64_t max_edge_events) {
     edge_ovf_checks = max_edge_events >= 0xFFFFFFFFull;
     const int NE = n_edges > 0 ? n_edges : 1;
@@ -404,12 +406,6 @@ struct Gen {
     o << "extern \"C\" __global__ void __launch_bounds__(128, 1) sfg_jit_execute(sfg_prog P, ExecView E, int* next, int mode) {\n"
          "  JitRunner R;\n"
          "  R.soft_cap = E.soft_cap;\n"
-         "  if (mode == 2) {  // tail pass over the deferred inputs, real budget\n"
-         "    R.soft_cap = 0;\n"
-         "    const int nd = *E.n_deferred;\n"
-         "    for (int j = atomicAdd(next, 1); j < nd; j = atomicAdd(next, 1)) run_input(P, E, E.deferred[j], R);\n"
-         "    return;\n"
-         "  }\n"
          "  if (mode == 0) {\n"
          "    for (int i = atomicAdd(next, 1); i < E.n; i = atomicAdd(next, 1)) run_input(P, E, i, R);\n"
          "    return;\n"
@@ -423,6 +419,25 @@ struct Gen {
          "    if (b + lane < E.n) run_input(P, E, b + lane, R);\n"
          "    __syncwarp();\n"
          "  }\n"
+         "}\n\n";
+    // tail pass over the deferred (long) inputs with the real budget.  One-warp CTAs;
+    // a warp takes k inputs at a time (lanes >= k idle), so a round's few long inputs
+    // spread over many SMs instead of serializing as divergent lanes of a few warps.
+    // Its own register cap (launch bounds) raises the number of resident tail warps.
+    o << "#define SFG_TAIL_MINB " << tail_minb << "\n"
+         "extern \"C\" __global__ void __launch_bounds__(32, SFG_TAIL_MINB) sfg_jit_tail(sfg_prog P, ExecView E, int* next, int k) {\n"
+         "  JitRunner R;\n"
+         "  R.soft_cap = 0;\n"
+         "  const int lane = threadIdx.x;\n"
+         "  const int nd = *E.n_deferred;\n"
+         "  while (true) {\n"
+         "    int b = 0;\n"
+         "    if (lane == 0) b = atomicAdd(next, k);\n"
+         "    b = __shfl_sync(0xffffffffu, b, 0);\n"
+         "    if (b >= nd) break;\n"
+         "    if (lane < k && b + lane < nd) run_input(P, E, E.deferred[b + lane], R);\n"
+         "    __syncwarp();\n"
+         "  }\n"
          "}\n";
     return o.str();
   }
@@ -434,6 +449,7 @@ struct Gen {
 static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_edge_events, std::string& source,
                            std::string& log, std::vector<char>& cubin) {
   sfgjit::Gen g(P, ins);
+  if (const char* tb = getenv("SFG_TAIL_MINB")) g.tail_minb = atoi(tb) >= 1 ? atoi(tb) : 8;
   source = g.run(P.n_edges, max_edge_events);
   // process-wide cache: identical programs (same generated source) compile once
   static std::mutex mu;
@@ -473,9 +489,9 @@ static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_e
   return 0;
 }
 
-// Generate, compile and load the specialized execute kernel.  Returns 0 on success.
+// Generate, compile and load the specialized execute kernels (bulk + tail).  Returns 0 on success.
 static int sfg_jit_build(const sfg_prog& P, const sfg_ins* ins, uint64_t max_edge_events, std::string& source,
-                         std::string& log, cudaLibrary_t* lib_out, cudaKernel_t* kern_out) {
+                         std::string& log, cudaLibrary_t* lib_out, cudaKernel_t* kern_out, cudaKernel_t* tail_out) {
   std::vector<char> cubin;
   const int rc = sfg_jit_compile(P, ins, max_edge_events, source, log, cubin);
   if (rc) return rc;
@@ -485,6 +501,7 @@ static int sfg_jit_build(const sfg_prog& P, const sfg_ins* ins, uint64_t max_edg
     return 3;
   }
   e = cudaLibraryGetKernel(kern_out, *lib_out, "sfg_jit_execute");
+  if (e == cudaSuccess) e = cudaLibraryGetKernel(tail_out, *lib_out, "sfg_jit_tail");
   if (e != cudaSuccess) {
     log += std::string("\ncudaLibraryGetKernel: ") + cudaGetErrorString(e);
     return 4;

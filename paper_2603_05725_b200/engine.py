@@ -556,10 +556,15 @@ class DeviceCampaign:
         self._submit(S, it0, n, self.rounds)
         return self._finalize(S)
 
-    def run_rounds(self, it0: int, it_stop: int, round_size: int, depth: int = 8, on_round=None):
+    def run_rounds(self, it0: int, it_stop: int, round_size: int, depth: int = 8, on_round=None,
+                   should_continue=None):
         """Rounds covering iterations [it0, it_stop) with up to ``depth`` rounds in
         flight.  ``on_round(result)`` runs after each round is finalized (before its
-        slot is reused).  Returns the list of RoundResults (stops early on a stop)."""
+        slot is reused).  ``should_continue()`` is asked before every new submission
+        (e.g. a wall-clock limit); once it says no, the rounds already in flight are
+        finalized and nothing more is submitted.  The pipeline stays full across the
+        whole range, so a long campaign is one call.  Returns the list of RoundResults
+        (stops early on a stop)."""
         plan = []
         it = it0
         while it < it_stop:
@@ -577,7 +582,10 @@ class DeviceCampaign:
             self._submit(S, it_k, n_k, base_round + k)
             inflight.append((k, S))
 
-        while nxt < len(plan) and len(inflight) < depth:
+        def more():
+            return nxt < len(plan) and (should_continue is None or should_continue())
+
+        while len(inflight) < depth and more():
             submit(nxt)
             nxt += 1
         while inflight:
@@ -596,7 +604,7 @@ class DeviceCampaign:
                 for kk, SS in redo:
                     self._submit(SS, SS.round_it0, SS.round_n, SS.round_index, resubmit=True)
                     inflight.append((kk, SS))
-            if nxt < len(plan):
+            if more():
                 submit(nxt)
                 nxt += 1
         return results

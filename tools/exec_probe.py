@@ -13,7 +13,7 @@ from paper_2603_05725_b200.workloads import load
 name = sys.argv[1] if len(sys.argv) > 1 else "matmul"
 R = int(sys.argv[2]) if len(sys.argv) > 2 else 65536
 m = load(name)
-for cap in [int(x) for x in os.environ.get("CAPS", "0,8192,32768,131072").split(",")]:
+for cap in [int(x) for x in os.environ.get("CAPS", "0,8192,32768,131072").split(",") if x]:
     dc = DeviceCampaign(m, master_seed=11, soft_cap=cap)
     dc.timing = True
     it = 1
@@ -35,7 +35,7 @@ for depth in [int(x) for x in os.environ.get("DEPTHS", "8,16,32").split(",")]:
     it = 1
     dc.run_rounds(it, it + 4 * R, R, depth=depth); it += 4 * R
     torch.cuda.synchronize()
-    steps = 16
+    steps = int(os.environ.get("STEPS", "16"))
     t0 = time.perf_counter()
     res = dc.run_rounds(it, it + steps * R, R, depth=depth)
     torch.cuda.synchronize()
