@@ -83,22 +83,37 @@ int sfg_apply(const sfg_program* p, const sfg_corpus_dev* c, int n, const void* 
 int sfg_regen(const sfg_program* p, const sfg_corpus_dev* c, int n_sel, const int32_t* sel,
               const void* children, const void* vals, const uint64_t* dst_off, uint8_t* dst,
               void* stream);
-/* work_counter: 4 ints of device scratch private to this launch pair (the
- * persistent specialized kernel hands out inputs from it; [1] = number of
- * deferred inputs; concurrent launches need their own).
- * soft_cap != 0 (specialized kernel only): an input whose retired-instruction
- * count would reach soft_cap is abandoned and listed in deferred[n]; it is
- * finished by sfg_execute_deferred, which re-materializes its payload and runs
- * it from scratch with the real budget.  Results are identical to soft_cap 0;
- * long inputs then share warps instead of pinning one warp each. */
+/* work_counter: 8 ints of device scratch private to this launch pair (the
+ * persistent specialized kernels hand out inputs from it; [1] = number of
+ * soft-cap deferrals, [3] = number of inputs to re-run thread-sequentially;
+ * concurrent launches need their own).  deferred: 2n ints (the two lists).
+ * Group-parallel mode (specialized kernel, programs whose launches have more
+ * than one simulated thread): the simulated threads of a launch run on the
+ * lanes of a group at once, with per-word conflict tags over the input's work
+ * region in shared memory; a chunk of threads with a cross-thread conflict is
+ * undone (work-region snapshot in shared memory) and re-run in place thread
+ * after thread; an input whose work region exceeds the shared-memory tag
+ * capacity is listed for a thread-sequential re-run.
+ * max_work_bytes bounds every input's work region of this round.  deferred ==
+ * NULL (inputs whose payloads cannot be re-materialized): thread-sequential.
+ * soft_cap != 0 (specialized kernel only): an input one of whose simulated
+ * threads would retire soft_cap instructions (cumulative over threads when
+ * they run sequentially) is abandoned and listed; sfg_execute_deferred
+ * re-materializes the listed inputs' payloads and runs them from scratch with
+ * the real budget (soft-cap list group-parallel, spread one input per warp;
+ * then the sequential list).  Results are identical to soft_cap 0 and to
+ * sequential execution (executor.py:405-424). */
 int sfg_execute(const sfg_program* p, int n, const void* children, const void* vals,
                 const uint64_t* work_base, uint8_t* work, void* verdicts, uint32_t* edge_counts,
                 uint8_t* readouts, const uint64_t* readout_base, uint64_t* overlay, int* work_counter,
-                uint64_t soft_cap, int32_t* deferred, void* stream);
+                uint64_t soft_cap, int32_t* deferred, int64_t max_work_bytes, void* stream);
 int sfg_execute_deferred(const sfg_program* p, const sfg_corpus_dev* c, int n, const void* children,
                          const void* vals, const uint64_t* work_base, uint8_t* work, void* verdicts,
                          uint32_t* edge_counts, uint8_t* readouts, const uint64_t* readout_base,
-                         uint64_t* overlay, int* work_counter, int32_t* deferred, void* stream);
+                         uint64_t* overlay, int* work_counter, int32_t* deferred, int64_t max_work_bytes,
+                         void* stream);
+/* Lanes per input of the program's group-parallel mode (1 = thread-sequential). */
+int sfg_program_group(const sfg_program* p);
 /* Triage in three stream-ordered phases so that a multi-GPU campaign can merge
  * the per-rank partials between them: a rank owns the global
  * round indices [i_base, i_base + n).  All indices written are GLOBAL round

@@ -16,7 +16,11 @@ struct sfg_program {
   cudaKernel_t jit_tail = nullptr;    // tail pass over deferred long inputs (one-warp CTAs)
   int jit_grid = 0;                   // resident CTAs (occupancy x SMs)
   int tail_grid = 0;                  // resident one-warp tail CTAs
-  int tail_k = 1;                     // long inputs per tail warp
+  int sms = 0;
+  int tail_k = 1;                     // long inputs per tail warp (group-parallel pass)
+  int tail_k_seq = 32;                // inputs per warp of the thread-sequential re-run pass
+  int group = 1;                      // lanes per input of the tail pass (group-parallel launches)
+  int bulk_group = 1;                 // lanes per input of the bulk pass (1 = thread-sequential)
   int jit_block = 128;                // CTA size of the persistent kernel
   int jit_mode = 1;                   // 0 per-lane fetch, 1 per-warp batches
   std::string jit_source, jit_log;
@@ -63,6 +67,14 @@ static int fail(const char* where, cudaError_t e) {
 
 static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// shared memory of the group-parallel execute kernels: per group a GroupSmem header,
+// one conflict tag and one snapshot word per 4 bytes of work region (exec_core.cuh)
+constexpr int kExecSmemMax = 96 * 1024;
+constexpr int kBulkSmem = 64 * 1024;   // per 128-thread CTA
+constexpr int kTailSmem = 8 * 1024;    // per one-warp CTA (one input per warp)
+
+static inline int tag_words(int64_t max_work_bytes) { return (int)((max_work_bytes + 3) / 4); }
 static inline CorpusView CV(const sfg_corpus_dev* c) {
   return CorpusView{(const sfg_entry*)c->meta, (const sfg_val*)c->vals, (const uint8_t*)c->data, c->n, c->n_seeds};
 }
@@ -171,8 +183,45 @@ int sfg_program_create(const void* prog, size_t prog_bytes, const void* ins, siz
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)p->jit_kernel, p->jit_block, 0);
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
     p->jit_grid = sms * per_sm;
+    p->sms = sms;
+    // group size: the most simulated threads of any COMPUTE launch, rounded up to a
+    // power of two, at most a warp (SFG_GROUP overrides; 1 = thread-sequential)
+    int maxt = 1;
+    for (size_t h = 0; h < n_hostops; ++h)
+      if (H[h].kind == SFG_H_LAUNCH && (int64_t)H[h].grid * H[h].block > maxt)
+        maxt = (int64_t)H[h].grid * H[h].block > 32 ? 32 : (int)(H[h].grid * H[h].block);
+    p->group = 1;
+    while (p->group < maxt) p->group <<= 1;
+    if (const char* gs = getenv("SFG_GROUP")) {
+      const int v = atoi(gs);
+      if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32) p->group = v;
+    }
+    // the bulk pass stays thread-sequential by default: 32 short inputs per warp cost
+    // less lane work than one input per group (the per-input setup is per lane);
+    // group-parallel pays off for the few long inputs, whose latency bounds a round
+    p->bulk_group = 1;
+    if (const char* bg = getenv("SFG_BULK_GROUP")) {
+      const int v = atoi(bg);
+      if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32) p->bulk_group = v;
+    }
+    cudaFuncSetAttribute((const void*)p->jit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kExecSmemMax);
+    cudaFuncSetAttribute((const void*)p->jit_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, kExecSmemMax);
+    // Reserve the per-thread local memory (stack frame: the per-input allocation
+    // table) of both kernels once.  Otherwise the driver grows the device's local
+    // memory pool for one kernel and may shrink it for the next, and every such
+    // resize synchronizes the device -- which serializes the pipelined rounds.
+    {
+      size_t need = 0, cur = 0;
+      cudaFuncAttributes fa;
+      for (cudaKernel_t k : {p->jit_kernel, p->jit_tail})
+        if (cudaFuncGetAttributes(&fa, (const void*)k) == cudaSuccess && fa.localSizeBytes > need) need = fa.localSizeBytes;
+      need = (need + 1023) & ~(size_t)1023;
+      if (cudaDeviceGetLimit(&cur, cudaLimitStackSize) == cudaSuccess && need > cur)
+        cudaDeviceSetLimit(cudaLimitStackSize, need);
+    }
+    if (const char* tq = getenv("SFG_TAIL_KSEQ")) p->tail_k_seq = atoi(tq) >= 1 && atoi(tq) <= 32 ? atoi(tq) : 32;
     if (const char* tk = getenv("SFG_TAIL_K")) p->tail_k = atoi(tk) >= 1 && atoi(tk) <= 32 ? atoi(tk) : 1;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)p->jit_tail, 32, 0);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)p->jit_tail, 32, kTailSmem);
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
     p->tail_grid = sms * per_sm;
 
@@ -275,40 +324,58 @@ int sfg_regen(const sfg_program* p, const sfg_corpus_dev* c, int n_sel, const in
   return 0;
 }
 
+int sfg_program_group(const sfg_program* p) { return p->jit_kernel ? p->group : 1; }
+
+
 int sfg_execute(const sfg_program* p, int n, const void* children, const void* vals, const uint64_t* work_base,
                 uint8_t* work, void* verdicts, uint32_t* edge_counts, uint8_t* readouts,
                 const uint64_t* readout_base, uint64_t* overlay, int* work_counter, uint64_t soft_cap,
-                int32_t* deferred, void* stream) {
+                int32_t* deferred, int64_t max_work_bytes, void* stream) {
   if (n <= 0) {
-    if (work_counter) cudaMemsetAsync(work_counter, 0, 4 * sizeof(int), S(stream));
+    if (work_counter) cudaMemsetAsync(work_counter, 0, 8 * sizeof(int), S(stream));
     return 0;
   }
   ExecView E{p->ins, p->hostops, p->binds, p->recs, p->base_blob, p->const_blob,
              (const sfg_child*)children, (const sfg_val*)vals, work_base, work,
              (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, overlay, n,
-             0ull, deferred, work_counter ? work_counter + 1 : nullptr};
+             0ull, deferred, work_counter ? work_counter + 1 : nullptr,
+             deferred ? deferred + n : nullptr, work_counter ? work_counter + 3 : nullptr, 1, 0};
   if (p->jit_kernel) {
-    if (work_counter == nullptr) {
-      g_err = "sfg_execute: the specialized kernel needs a per-launch work counter";
-      return 1;
-    }
-    if (soft_cap && deferred == nullptr) {
-      g_err = "sfg_execute: soft_cap needs a deferred list";
+    if (work_counter == nullptr || (deferred == nullptr && soft_cap != 0)) {
+      g_err = "sfg_execute: the specialized kernel needs a per-launch work counter (and deferred lists for soft_cap)";
       return 1;
     }
     E.soft_cap = soft_cap;
-    cudaError_t e = cudaMemsetAsync(work_counter, 0, 4 * sizeof(int), S(stream));
+    E.group = deferred ? p->bulk_group : 1;  // no lists: nothing can be re-run, so thread-sequential
+    size_t smem = 0;
+    if (E.group > 1) {
+      // tag capacity: the round's largest work region, within the CTA's smem budget
+      const int groups = (p->jit_block / 32) * (32 / E.group);
+      int cap = tag_words(max_work_bytes);
+      const int fit = (int)((kBulkSmem / groups - sizeof(GroupSmem)) / 8) & ~3;
+      E.tag_cap = cap < fit ? cap : fit;
+      smem = (size_t)groups * group_stride(E.tag_cap);
+    }
+    cudaError_t e = cudaMemsetAsync(work_counter, 0, 8 * sizeof(int), S(stream));
     if (e != cudaSuccess) return fail("sfg_execute (jit counter)", e);
     int* next = work_counter;
     int mode = p->jit_mode;
     void* args[] = {(void*)&p->P, (void*)&E, (void*)&next, (void*)&mode};
-    const unsigned want = blocks_for(n, p->jit_block);
-    const unsigned grid = want < (unsigned)p->jit_grid ? want : (unsigned)p->jit_grid;
-    e = cudaLaunchKernel((const void*)p->jit_kernel, dim3(grid), dim3(p->jit_block), args, 0, S(stream));
+    const int per_cta = E.group > 1 ? (p->jit_block / 32) * (32 / E.group) : p->jit_block;
+    const unsigned want = blocks_for(n, per_cta);
+    int resident = p->jit_grid;
+    if (smem) {
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)p->jit_kernel, p->jit_block, smem) ==
+              cudaSuccess && per_sm > 0)
+        resident = p->sms * per_sm;
+    }
+    const unsigned grid = want < (unsigned)resident ? want : (unsigned)resident;
+    e = cudaLaunchKernel((const void*)p->jit_kernel, dim3(grid), dim3(p->jit_block), args, smem, S(stream));
     if (e != cudaSuccess) return fail("sfg_execute (jit)", e);
     return 0;
   }
-  if (work_counter) cudaMemsetAsync(work_counter, 0, 4 * sizeof(int), S(stream));
+  if (work_counter) cudaMemsetAsync(work_counter, 0, 8 * sizeof(int), S(stream));
   sfg_execute_kernel<<<blocks_for(n, 128), 128, p->smem, S(stream)>>>(p->P, E);
   SFG_CHECK_LAUNCH("sfg_execute");
   return 0;
@@ -317,23 +384,38 @@ int sfg_execute(const sfg_program* p, int n, const void* children, const void* v
 int sfg_execute_deferred(const sfg_program* p, const sfg_corpus_dev* c, int n, const void* children,
                          const void* vals, const uint64_t* work_base, uint8_t* work, void* verdicts,
                          uint32_t* edge_counts, uint8_t* readouts, const uint64_t* readout_base, uint64_t* overlay,
-                         int* work_counter, int32_t* deferred, void* stream) {
+                         int* work_counter, int32_t* deferred, int64_t max_work_bytes, void* stream) {
   if (n <= 0 || !p->jit_kernel) return 0;  // the interpreter never defers
-  // pristine payloads again (the first attempt's stores landed in the work regions)
-  sfg_apply_kernel<<<p->jit_grid, 256, 0, S(stream)>>>(p->P, CV(c), n, (const sfg_child*)children,
-                                                      (const sfg_val*)vals, work_base, work, deferred,
-                                                      work_counter + 1);
-  SFG_CHECK_LAUNCH("sfg_execute_deferred/apply");
   ExecView E{p->ins, p->hostops, p->binds, p->recs, p->base_blob, p->const_blob,
              (const sfg_child*)children, (const sfg_val*)vals, work_base, work,
              (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, overlay, n,
-             0ull, deferred, work_counter + 1};
-  int* next = work_counter + 2;
-  int k = p->tail_k;
-  void* args[] = {(void*)&p->P, (void*)&E, (void*)&next, (void*)&k};
-  // one-warp CTAs: a warp that holds long inputs pins only its own slot
-  cudaError_t e = cudaLaunchKernel((const void*)p->jit_tail, dim3((unsigned)p->tail_grid), dim3(32), args, 0, S(stream));
-  if (e != cudaSuccess) return fail("sfg_execute_deferred (jit)", e);
+             0ull, deferred, work_counter + 1, deferred + n, work_counter + 3, p->group, 0};
+  for (int pass = 0; pass < 2; ++pass) {
+    // pristine payloads again (the earlier attempt's stores landed in the work regions)
+    int32_t* list = pass == 0 ? deferred : deferred + n;
+    int* count = pass == 0 ? work_counter + 1 : work_counter + 3;
+    sfg_apply_kernel<<<p->jit_grid, 256, 0, S(stream)>>>(p->P, CV(c), n, (const sfg_child*)children,
+                                                        (const sfg_val*)vals, work_base, work, list, count);
+    SFG_CHECK_LAUNCH("sfg_execute_deferred/apply");
+    // pass 0: soft-cap list, group-parallel, one input per one-warp CTA (long inputs
+    // spread over the SMs); pass 1: thread-sequential re-runs
+    int* next = work_counter + (pass == 0 ? 2 : 4);
+    int k = pass == 0 ? p->tail_k : p->tail_k_seq;
+    int seq = pass;
+    size_t smem = 0;
+    E.tag_cap = 0;
+    if (pass == 0 && p->group > 1) {
+      const int per = k < 32 / p->group ? k : 32 / p->group;
+      const int cap = tag_words(max_work_bytes);
+      const int fit = (int)((kTailSmem / per - sizeof(GroupSmem)) / 8) & ~3;
+      E.tag_cap = cap < fit ? cap : fit;
+      smem = (size_t)per * group_stride(E.tag_cap);
+    }
+    void* args[] = {(void*)&p->P, (void*)&E, (void*)&next, (void*)&k, (void*)&seq};
+    cudaError_t e = cudaLaunchKernel((const void*)p->jit_tail, dim3((unsigned)p->tail_grid), dim3(32), args, smem,
+                                     S(stream));
+    if (e != cudaSuccess) return fail("sfg_execute_deferred (jit)", e);
+  }
   return 0;
 }
 

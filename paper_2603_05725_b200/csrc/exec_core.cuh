@@ -81,11 +81,24 @@ struct ExecView {
   uint64_t soft_cap;
   int32_t* deferred;
   int* n_deferred;
+  // inputs that must run thread-sequentially (a cross-thread memory conflict was
+  // seen in group-parallel mode, or the work region exceeds the tag capacity)
+  int32_t* deferred_seq;
+  int* n_deferred_seq;
+  // group-parallel mode: the simulated threads of one launch run on G lanes at once
+  // (G = 1: one lane runs them one after another); tag_cap = per-group conflict-tag
+  // words in shared memory (4 bytes of work region per word)
+  int group;
+  int tag_cap;
 };
 
 namespace {
 
 typedef __int128 i128;
+
+// sanitizer slow path, allocator walk and report assembly: rare, called from every
+// memory access site of the specialized kernel -> out of line (code size / compile time)
+#define SFG_SLOW __device__ __noinline__
 
 // space bases 0x1000_0000 / 0x2000_0000 / 0x3000_0000 (device_memory.py:41-45)
 SFG_DEV int64_t sbase(int s) { return (int64_t)(s + 1) << 28; }
@@ -123,7 +136,7 @@ SFG_DEV int resolve_slot(const Lane& L, int sp, int64_t a) {
 struct Scan { int kind; int64_t gaddr; int code; };  // kind 0 none, 1 spatial, 2 freed, 3 wild
 
 // _scan_shadow (sanitizer.py:102-142) on shadow codes derived from the registry
-SFG_DEV Scan scan_shadow(const sfg_prog& P, const Lane& L, i128 a, int64_t width) {
+SFG_SLOW Scan scan_shadow(const sfg_prog& P, const Lane& L, i128 a, int64_t width) {
   const int sp = space_of(P, a);
   if (sp < 0) return {3, 0, SH_UNALLOC};
   const int64_t g = P.granule;
@@ -155,7 +168,7 @@ SFG_DEV Scan scan_shadow(const sfg_prog& P, const Lane& L, i128 a, int64_t width
 }
 
 // check_access (sanitizer.py:145-187).  prov: lane record index + 1, 0 none.
-SFG_DEV bool check_access(const sfg_prog& P, const Lane& L, i128 a, int64_t width, int decl, int prov,
+SFG_SLOW bool check_access(const sfg_prog& P, const Lane& L, i128 a, int64_t width, int decl, int prov,
                           Report& rep, int& hit) {
   // fast path: the tagged live record contains the whole access in its declared space
   if (prov > 0) {
@@ -190,6 +203,7 @@ SFG_DEV bool check_access(const sfg_prog& P, const Lane& L, i128 a, int64_t widt
   hit = r;
   return false;
 }
+
 
 // _alloc_common (device_memory.py:407-440), scope 0; returns record index or -status
 SFG_DEV int lane_alloc(const sfg_prog& P, Lane& L, int sp, int64_t size, int label, int64_t phys) {
@@ -268,7 +282,7 @@ SFG_DEV uint8_t base_byte(const Mem& M, const Lane& L, const LRec& r, int64_t a)
   return M.blob[r.phys + (a - r.base)];
 }
 
-SFG_DEV uint64_t mem_read(const Mem& M, const Lane& L, const LRec& r, int64_t a, int w) {
+SFG_SLOW uint64_t mem_read(const Mem& M, const Lane& L, const LRec& r, int64_t a, int w) {
   uint64_t v = 0;
   if (!(r.flags & R_BASE)) {
     const uint8_t* p = M.work + r.phys + (a - r.base);
@@ -285,7 +299,7 @@ SFG_DEV uint64_t mem_read(const Mem& M, const Lane& L, const LRec& r, int64_t a,
   return v;
 }
 
-SFG_DEV bool mem_write(const Mem& M, Lane& L, const LRec& r, int64_t a, int w, uint64_t v) {
+SFG_SLOW bool mem_write(const Mem& M, Lane& L, const LRec& r, int64_t a, int w, uint64_t v) {
   if (!(r.flags & R_BASE)) {
     uint8_t* p = M.work + r.phys + (a - r.base);
     if ((((uintptr_t)p) & (w - 1)) == 0) {
@@ -331,7 +345,7 @@ SFG_DEV void st_work(uint8_t* p, int w, uint64_t v) {
 
 // ---------------------------------------------------------------------------
 
-SFG_DEV void fill_report(sfg_verdict& V, const sfg_prog& P, const Lane& L, const Report& rep, int kernel,
+SFG_SLOW void fill_report(sfg_verdict& V, const sfg_prog& P, const Lane& L, const Report& rep, int kernel,
                          int iid, int ctaid, int tid, i128 a, int width, bool store, int space, int prov) {
   V.status = SFG_ST_FINDING;
   V.bug_class = rep.cls;
@@ -393,12 +407,185 @@ struct Pre {
   int nr, nf, na;
 };
 
-enum { RUN_EXIT = 0, RUN_FINDING = 1, RUN_BUDGET = 2, RUN_FATAL = 3, RUN_DEFER = 4 };
+enum { RUN_EXIT = 0, RUN_FINDING = 1, RUN_BUDGET = 2, RUN_FATAL = 3, RUN_DEFER = 4, RUN_CONFLICT = 5, RUN_ABORT = 6 };
+
+// ---------------------------------------------------------------------------
+// group-parallel launches (JIT runner only)
+//
+// executor.py:405-424 runs the simulated threads of a launch one after another
+// (ctaid-major), each to completion, first stop wins.  A group of G lanes runs
+// G consecutive simulated threads at once instead, and the attempt is kept only
+// if it provably equals the sequential run:
+//   * every work-region word carries a tag (writer lane, reader lane / many) in
+//     shared memory; a word written by one thread and read or written by another
+//     is a conflict -> the input is re-run thread-sequentially (deferred_seq);
+//     stores into INIT (baseline) buffers are conflicts too;
+//   * threads are independent otherwise (own registers, own budget,
+//     executor.py:414), so the stop is the smallest stopping thread index s;
+//     threads after s are discarded (their edge counts rolled back, their
+//     retired counts dropped) and threads <= s are exactly the sequential ones;
+//   * a lane polls the group state every few thousand retired instructions and
+//     quits once its thread can no longer matter.
+// Chunks of G threads run in order, so a launch with more threads than lanes
+// sees every earlier chunk's stores.  A chunk with a conflict is undone (its
+// work-region snapshot restored, edge counts rolled back) and re-run in place
+// by the group's first lane, thread after thread.
+
+struct GroupSmem {
+  int stop_min;    // smallest stopping thread index of the chunk
+  int defer_min;   // smallest thread that reached the soft cap
+  int conflict;
+  int seq_rc;      // sequential re-run of a conflicting chunk: LG_* outcome
+  unsigned long long seq_retired;
+  int seq_nov, pad;
+  sfg_verdict V;   // the stopping thread's verdict, broadcast to the group
+  // uint32_t tags[tag_cap], then uint32_t snapshot[tag_cap] of the work region
+};
+
+struct Grp {
+  int G;           // lanes per input
+  int gl;          // this lane's index in the group
+  unsigned mask;   // the group's lanes
+  GroupSmem* sm;
+  uint32_t* tags;
+  int tag_cap;
+};
+
+__host__ __device__ inline size_t group_stride(int tag_cap) {
+  return (sizeof(GroupSmem) + (size_t)tag_cap * 8 + 15) & ~(size_t)15;
+}
+
+// record an access of [off, off+w) of the work region by lane `me` (1-based);
+// true = conflict (another thread wrote a word we touch, or read a word we write)
+SFG_DEV bool par_track(uint32_t* tags, int ntags, int64_t off, int w, bool st, uint32_t me) {
+  if (off < 0) return true;
+  const int64_t w0 = off >> 2, w1 = (off + w - 1) >> 2;
+  if (w1 >= ntags) return true;
+  for (int64_t x = w0; x <= w1; ++x) {
+    uint32_t old = *reinterpret_cast<volatile uint32_t*>(&tags[x]);
+    while (true) {
+      const uint32_t wr = old & 0xFFu, rd = (old >> 8) & 0xFFu;
+      if (wr && wr != me) return true;
+      uint32_t nw;
+      if (st) {
+        if (rd && rd != me) return true;
+        nw = (old & ~0xFFu) | me;
+      } else {
+        if (rd == me || rd == 0xFFu) break;
+        nw = (old & ~0xFF00u) | ((rd ? 0xFFu : me) << 8);
+      }
+      if (nw == old) break;
+      const uint32_t prev = atomicCAS(&tags[x], old, nw);
+      if (prev == old) break;
+      old = prev;
+    }
+  }
+  return false;
+}
+
+// slow-path access (check_access passed, record r) in group-parallel mode
+template <class Runner>
+SFG_DEV bool par_access(const Runner& R, const LRec& r, int64_t lo, int w, bool st) {
+  if (r.flags & R_BASE) return st;  // INIT buffers: reads are shared, writes go through the overlay
+  return par_track(R.tags, R.ntags, r.phys + (lo - r.base), w, st, R.me);
+}
 
 // One input's COMPUTE phase (campaign.py:483-561).  Runner supplies the simulated
 // thread execution: begin_input(), run_thread(...) -> RUN_*, flush(row).
+enum { LG_OK = 0, LG_STOP = 1, LG_DEFER = 2, LG_SEQ = 3 };
+
+// One launch's simulated threads on the lanes of a group, G at a time (see above).
 template <class Runner>
-SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R) {
+SFG_DEV int run_launch_group(const sfg_prog& P, const sfg_hostop& op, Lane& L, Mem& M, sfg_verdict& V,
+                             const Pre& pre, Runner& R, const Grp& g, uint64_t& total_retired, int ntags) {
+  const int T = op.grid * op.block;
+  uint32_t* wk = reinterpret_cast<uint32_t*>(M.work);  // 16-aligned, work_bytes a multiple of 16
+  uint32_t* snap = g.tags + g.tag_cap;
+  for (int c0 = 0; c0 < T; c0 += g.G) {
+    for (int x = g.gl; x < ntags; x += g.G) {
+      g.tags[x] = 0u;
+      snap[x] = wk[x];
+    }
+    if (g.gl == 0) {
+      g.sm->stop_min = 0x7FFFFFFF;
+      g.sm->defer_min = 0x7FFFFFFF;
+      g.sm->conflict = 0;
+    }
+    __syncwarp(g.mask);
+    R.save_edges();
+    const int t = c0 + g.gl;
+    int rc = RUN_EXIT;
+    uint64_t tr = 0;
+    sfg_verdict Vt = V;
+    if (t < T) {
+      R.par_begin(g, t, ntags);
+      rc = R.template run_thread<true>(P, op.kernel, L, M, Vt, pre, t / op.block, t % op.block, op.grid, op.block, tr);
+      R.par_end();
+      if (rc == RUN_FINDING || rc == RUN_BUDGET || rc == RUN_FATAL) atomicMin(&g.sm->stop_min, t);
+      else if (rc == RUN_DEFER) atomicMin(&g.sm->defer_min, t);
+      else if (rc == RUN_CONFLICT) atomicOr(&g.sm->conflict, 1);
+    }
+    __syncwarp(g.mask);
+    const int s = *reinterpret_cast<volatile int*>(&g.sm->stop_min);
+    const int d = *reinterpret_cast<volatile int*>(&g.sm->defer_min);
+    const int cf = *reinterpret_cast<volatile int*>(&g.sm->conflict);
+    __syncwarp(g.mask);
+    if (cf) {
+      // undo the chunk and re-run it thread-sequentially on the first lane
+      for (int x = g.gl; x < ntags; x += g.G) wk[x] = snap[x];
+      R.restore_edges();
+      __syncwarp(g.mask);
+      if (g.gl == 0) {
+        int lg = LG_OK;
+        uint64_t before = total_retired;
+        for (int tt = c0; tt < T && tt < c0 + g.G; ++tt) {
+          const int r2 = R.template run_thread<false>(P, op.kernel, L, M, V, pre, tt / op.block, tt % op.block,
+                                                      op.grid, op.block, total_retired);
+          if (r2 == RUN_EXIT) continue;
+          if (r2 == RUN_BUDGET) V.status = SFG_ST_BUDGET;
+          lg = r2 == RUN_DEFER ? LG_DEFER : LG_STOP;  // finding / budget / fatal stop the phase
+          break;
+        }
+        g.sm->seq_rc = lg;
+        g.sm->seq_retired = total_retired - before;
+        g.sm->seq_nov = L.nov;
+        g.sm->V = V;
+      }
+      __syncwarp(g.mask);
+      const int lg = g.sm->seq_rc;
+      if (g.gl != 0) {
+        total_retired += g.sm->seq_retired;
+        L.nov = g.sm->seq_nov;  // overlay entries (INIT-buffer stores) are shared
+        V = g.sm->V;
+      }
+      __syncwarp(g.mask);
+      if (lg != LG_OK) return lg;
+      continue;
+    }
+    if (d < s) return LG_DEFER;
+    const bool keep = t < T && t <= s;
+    if (!keep) R.restore_edges();
+    uint64_t sum = keep ? tr : 0ull;
+    for (int o = g.G >> 1; o; o >>= 1) sum += __shfl_xor_sync(g.mask, sum, o);
+    total_retired += sum;
+    if (s != 0x7FFFFFFF) {
+      if (t == s) {
+        if (rc == RUN_BUDGET) Vt.status = SFG_ST_BUDGET;
+        g.sm->V = Vt;
+      }
+      __syncwarp(g.mask);
+      V = g.sm->V;
+      __syncwarp(g.mask);
+      return LG_STOP;
+    }
+  }
+  return LG_OK;
+}
+
+// GRP: group-parallel launches (g.G > 1, specialized kernel only) vs one lane
+// running the simulated threads one after another
+template <bool GRP, class Runner>
+SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R, const Grp& g) {
   const sfg_child& ch = E.children[i];
   const sfg_val* cv = E.vals + (size_t)i * P.n_args;
   uint64_t t_start;
@@ -435,8 +622,11 @@ SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R) {
   uint64_t total_retired = 0;
   uint8_t* ro = (P.diff_readback && E.readouts) ? E.readouts + E.readout_base[i] : nullptr;
   const uint64_t arrays_end = ch.work_bytes - (uint64_t)P.named_work_bytes;
+  const int ntags = (int)((ch.work_bytes + 3) / 4);
+  int defer_kind = 0;  // 1: soft cap reached (deferred), 2: re-run thread-sequentially (deferred_seq)
+  if (GRP && ntags > g.tag_cap) defer_kind = 2;
 
-  bool stop = false;
+  bool stop = defer_kind != 0;
   for (int h = 0; h < P.n_hostops && !stop; ++h) {
     const sfg_hostop& op = E.hostops[h];
     if (op.kind == SFG_H_SYNC) continue;
@@ -534,31 +724,44 @@ SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R) {
     if (stop) break;
     V.entered |= 1u << op.kernel;
     V.launches++;
+    if constexpr (GRP) {
+      __syncwarp(g.mask);  // host-op stores (made identically by every lane) visible to all
+      const int lg = run_launch_group(P, op, L, M, V, pre, R, g, total_retired, ntags);
+      if (lg == LG_STOP) stop = true;
+      else if (lg == LG_DEFER) { defer_kind = 1; stop = true; }
+      else if (lg == LG_SEQ) { defer_kind = 2; stop = true; }
+      continue;
+    }
     for (int ctaid = 0; ctaid < op.grid && !stop; ++ctaid) {
       for (int tid = 0; tid < op.block && !stop; ++tid) {
-        const int rc = R.run_thread(P, op.kernel, L, M, V, pre, ctaid, tid, op.grid, op.block, total_retired);
+        const int rc = R.template run_thread<false>(P, op.kernel, L, M, V, pre, ctaid, tid, op.grid, op.block,
+                                                    total_retired);
         if (rc == RUN_BUDGET) { V.status = SFG_ST_BUDGET; stop = true; }
-        else if (rc == RUN_DEFER) { V.status = SFG_ST_DEFERRED; stop = true; }
+        else if (rc == RUN_DEFER) { defer_kind = 1; stop = true; }
         else if (rc != RUN_EXIT) stop = true;  // finding (V filled) or fatal (V.status set)
       }
     }
   }
-  if (V.status == SFG_ST_DEFERRED) {  // nothing of this attempt is kept
-    E.deferred[atomicAdd(E.n_deferred, 1)] = i;
+  if (defer_kind) {  // nothing of this attempt is kept
+    if (g.gl == 0) {
+      if (defer_kind == 1) E.deferred[atomicAdd(E.n_deferred, 1)] = i;
+      else E.deferred_seq[atomicAdd(E.n_deferred_seq, 1)] = i;
+    }
     return;
   }
   V.retired = total_retired;
   V.allocs = L.nalloc;
   uint32_t* erow = E.edge_counts + (size_t)i * P.n_edges;
   bool overflow = false;
-  R.flush(erow, overflow);
+  if constexpr (GRP) R.flush_group(erow, overflow, g.mask, g.gl == 0);
+  else R.flush(erow, overflow);
   if (overflow && V.status < SFG_ST_OUT_OF_SPACE) V.status = SFG_ST_COUNTER;
   uint64_t t_end;
   uint32_t smid;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
   asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
   V.where = (uint64_t)(smid & 0xff) | ((t_end - t_start) << 8);
-  E.verdicts[i] = V;
+  if (g.gl == 0) E.verdicts[i] = V;
 }
 
 }  // namespace

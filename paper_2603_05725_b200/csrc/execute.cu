@@ -31,6 +31,7 @@ struct InterpRunner {
     ovf = overflow;
   }
 
+  template <bool PAR>
   SFG_DEV int run_thread(const sfg_prog& P, int kidx, Lane& L, Mem& M, sfg_verdict& V, const Pre& pre, int ctaid,
                          int tid, int grid, int block, uint64_t& total_retired) {
     const sfg_kernel& K = P.kernels[kidx];
@@ -231,6 +232,6 @@ extern "C" __global__ void __launch_bounds__(128) sfg_execute_kernel(sfg_prog P,
   const int nw = gridDim.x * nwb;
   for (int base_i = gw * 32; base_i < E.n; base_i += nw * 32) {
     const int i = base_i + lane;
-    if (i < E.n) run_input(P, E, i, R);
+    if (i < E.n) run_input<false>(P, E, i, R, Grp{1, 0, 1u << lane, nullptr, nullptr, 0});
   }
 }

@@ -170,14 +170,18 @@ struct Gen {
       const std::string Q = std::to_string(q);
       const char* T = W == 1 ? "uint8_t" : W == 2 ? "uint16_t" : W == 4 ? "uint32_t" : "uint64_t";
       const std::string ptr = std::string("reinterpret_cast<") + (st ? "" : "const ") + T + "*>(pp" + Q + " + (lo_ - pb" + Q + "))";
-      if (st) return "*" + ptr + " = (" + T + ")sv_;";
-      return "v_ = *" + ptr + ";";
+      const std::string trk = "if (PAR && par_track(J.tags, J.ntags, pw" + Q + " + (lo_ - pb" + Q + "), " + W_s + ", " +
+                              (st ? "true" : "false") + ", J.me)) { " + radj(slow, j) + "rc = RUN_CONFLICT; goto done; } ";
+      if (st) return trk + "*" + ptr + " = (" + T + ")sv_;";
+      return trk + "v_ = *" + ptr + ";";
     };
     std::string slow_path =
         "{ Report rep_; int rh_ = -1;\n"
         "        if (check_access(P, L, A_, " + W_s + ", " + SP + ", " + t(x.s1) + ", rep_, rh_)) { fill_report(V, P, L, rep_, " +
         std::to_string(kidx) + ", " + std::to_string(iid) + ", ctaid, tid, A_, " + W_s + ", " + (st ? "true" : "false") +
         ", " + SP + ", " + t(x.s1) + "); " + radj(slow, j) + "rc = RUN_FINDING; goto done; }\n";
+    slow_path += "        if (PAR && par_access(J, L.rec[rh_], lo_, " + W_s + ", " + (st ? "true" : "false") + ")) { " +
+                 radj(slow, j) + "rc = RUN_CONFLICT; goto done; }\n";
     if (st)
       slow_path += "        if (!mem_write(M, L, L.rec[rh_], lo_, " + W_s + ", sv_)) { V.status = SFG_ST_OVERLAY; " +
                    radj(slow, j) + "rc = RUN_FATAL; goto done; } }";
@@ -305,7 +309,7 @@ struct Gen {
     const auto tags = tag_flow(I, K.n, K, starts, blk_of);
     const int nb = (int)starts.size();
 
-    o << "static __device__ __forceinline__ int sim_" << kidx
+    o << "template <bool PAR>\nstatic __device__ __forceinline__ int sim_" << kidx
       << "(JitRunner& J, const sfg_prog& P, Lane& L, Mem& M, sfg_verdict& V, const Pre& pre, int ctaid, int tid, "
          "int grid, int block, uint64_t& total) {\n";
     for (int q = 0; q < K.regs; ++q) {
@@ -318,18 +322,21 @@ struct Gen {
     for (int q = 0; q < K.na; ++q) {
       const std::string Q = std::to_string(q);
       o << "  const int32_t pt" << Q << " = pre.ap[" << Q << "];\n";
-      o << "  int64_t pb" << Q << " = 0, psz" << Q << " = 0; int psp" << Q << " = -1; bool pok" << Q
+      o << "  int64_t pb" << Q << " = 0, psz" << Q << " = 0, pw" << Q << " = 0; int psp" << Q << " = -1; bool pok" << Q
         << " = false; uint8_t* pp" << Q << " = M.work;\n";
       o << "  if (pt" << Q << " > 0) { const LRec& R_ = L.rec[pt" << Q << " - 1]; pb" << Q << " = R_.base; psz" << Q
         << " = R_.size; psp" << Q << " = R_.space; pok" << Q
-        << " = (R_.flags & (R_RES | R_FREED | R_BASE)) == R_RES; pp" << Q << " = M.work + R_.phys; }\n";
+        << " = (R_.flags & (R_RES | R_FREED | R_BASE)) == R_RES; pp" << Q << " = M.work + R_.phys; pw" << Q << " = R_.phys; }\n";
       o << "  const bool pk" << Q << "_0 = pok" << Q << " && psp" << Q << " == 0, pk" << Q << "_1 = pok" << Q << " && psp"
         << Q << " == 1, pk" << Q << "_2 = pok" << Q << " && psp" << Q << " == 2;\n";
     }
     o << "  uint64_t ret = 0; int rc = RUN_EXIT; const uint64_t BUD = P.budget;\n";
     // fast-path limit: the budget, or the remaining soft cap of the input (deferral)
     o << "  const uint64_t SOFT = J.soft_cap; const bool SFT = SOFT != 0ull && (SOFT <= total || SOFT - total < BUD);\n";
-    o << "  const uint64_t LIM = SFT ? (SOFT > total ? SOFT - total : 0ull) : BUD;\n";
+    o << "  const uint64_t HARD = SFT ? (SOFT > total ? SOFT - total : 0ull) : BUD;\n";
+    // group-parallel mode: stop at poll points every kPoll retired instructions to see
+    // whether this thread can still matter (run_launch_group)
+    o << "  uint64_t LIM = (PAR && HARD > kPoll) ? kPoll : HARD;\n";
     o << "  (void)grid; (void)block; (void)ctaid; (void)tid;\n";
     for (int b = 0; b < nb; ++b) {
       const int s0 = starts[b], e = b + 1 < nb ? starts[b + 1] : K.n;
@@ -340,7 +347,10 @@ struct Gen {
         const bool slow = pass == 1;
         o << (slow ? "S" : "B") << b << ":\n";
         if (!slow && checked > 0)
-          o << "  if (ret + " << checked << "ull >= LIM) { if (SFT) { rc = RUN_DEFER; goto done; } goto S" << b << "; }\n";
+          o << "  if (ret + " << checked << "ull >= LIM) {\n"
+            << "    if constexpr (PAR) { if (LIM < HARD) { if (J.poll()) { rc = RUN_ABORT; goto done; }\n"
+            << "      LIM = (HARD - ret > " << checked << "ull + kPoll) ? ret + " << checked << "ull + kPoll : HARD; goto B" << b << "; } }\n"
+            << "    if (SFT) { rc = RUN_DEFER; goto done; } goto S" << b << "; }\n";
         if (!slow && checked == 0) {
           // a lone exit: nothing to check, the slow copy is identical
         }
@@ -381,61 +391,114 @@ struct Gen {
     o << "done:\n  total += ret;\n  return rc;\n}\n\n";
   }
 
-  int tail_minb = 8;
+  int tail_minb = 16;
 
   std::string run(int n_edges, uint64_t max_edge_events) {
     edge_ovf_checks = max_edge_events >= 0xFFFFFFFFull;
     const int NE = n_edges > 0 ? n_edges : 1;
     o << "#include \"exec_core.cuh\"\n\nnamespace {\n\n";
-    o << "struct JitRunner {\n  uint32_t ec[" << NE << "];\n  bool ovf;\n  uint64_t soft_cap;\n"
+    o << "constexpr uint64_t kPoll = 4096ull;\n\n";
+    o << "struct JitRunner {\n  uint32_t ec[" << NE << "], ecs[" << NE
+      << "];\n  bool ovf, ovfs;\n  uint64_t soft_cap;\n"
+      << "  uint32_t* tags = nullptr;\n  int ntags = 0, t = 0;\n  uint32_t me = 0;\n  GroupSmem* gs = nullptr;\n"
       << "  SFG_DEV void begin_input() {\n#pragma unroll\n    for (int e = 0; e < " << NE << "; ++e) ec[e] = 0u;\n    ovf = false;\n  }\n"
+      << "  SFG_DEV void save_edges() {\n#pragma unroll\n    for (int e = 0; e < " << NE << "; ++e) ecs[e] = ec[e];\n    ovfs = ovf;\n  }\n"
+      << "  SFG_DEV void restore_edges() {\n#pragma unroll\n    for (int e = 0; e < " << NE << "; ++e) ec[e] = ecs[e];\n    ovf = ovfs;\n  }\n"
+      << "  SFG_DEV void par_begin(const Grp& g, int thread, int nt) {\n"
+         "    tags = g.tags; ntags = nt; t = thread; me = (uint32_t)g.gl + 1u; gs = g.sm;\n  }\n"
+      << "  SFG_DEV void par_end() {}\n"
+      << "  SFG_DEV bool poll() const {\n"
+         "    const int s = *reinterpret_cast<volatile const int*>(&gs->stop_min);\n"
+         "    const int d = *reinterpret_cast<volatile const int*>(&gs->defer_min);\n"
+         "    return *reinterpret_cast<volatile const int*>(&gs->conflict) != 0 || t > (s < d ? s : d);\n  }\n"
       << "  SFG_DEV void flush(uint32_t* row, bool& o) {\n#pragma unroll\n    for (int e = 0; e < " << n_edges
       << "; ++e) row[e] = ec[e];\n    o = ovf;\n  }\n"
-      << "  SFG_DEV int run_thread(const sfg_prog& P, int k, Lane& L, Mem& M, sfg_verdict& V, const Pre& pre, int ctaid, "
+      << "  SFG_DEV void flush_group(uint32_t* row, bool& o, unsigned mask, bool leader) {\n"
+         "    bool big = false;\n#pragma unroll\n    for (int e = 0; e < " << n_edges << "; ++e) {\n"
+         "      const uint32_t lo = __reduce_add_sync(mask, ec[e] & 0xFFFFu), hi = __reduce_add_sync(mask, ec[e] >> 16);\n"
+         "      const uint64_t v = ((uint64_t)hi << 16) + lo;\n"
+         "      big |= v > 0xFFFFFFFFull;\n"
+         "      if (leader) row[e] = (uint32_t)v;\n    }\n"
+         "    o = __any_sync(mask, ovf) || big;\n  }\n"
+      << "  template <bool PAR>\n  SFG_DEV int run_thread(const sfg_prog& P, int k, Lane& L, Mem& M, sfg_verdict& V, const Pre& pre, int ctaid, "
          "int tid, int grid, int block, uint64_t& total);\n};\n\n";
     for (int k = 0; k < P.n_kernels; ++k) emit_kernel(k);
-    o << "SFG_DEV int JitRunner::run_thread(const sfg_prog& P, int k, Lane& L, Mem& M, sfg_verdict& V, const Pre& pre, "
+    o << "template <bool PAR>\nSFG_DEV int JitRunner::run_thread(const sfg_prog& P, int k, Lane& L, Mem& M, sfg_verdict& V, const Pre& pre, "
          "int ctaid, int tid, int grid, int block, uint64_t& total) {\n  switch (k) {\n";
     for (int k = 0; k < P.n_kernels; ++k)
-      o << "    case " << k << ": return sim_" << k << "(*this, P, L, M, V, pre, ctaid, tid, grid, block, total);\n";
+      o << "    case " << k << ": return sim_" << k << "<PAR>(*this, P, L, M, V, pre, ctaid, tid, grid, block, total);\n";
     o << "    default: return RUN_FATAL;\n  }\n}\n\n}  // namespace\n\n";
-    // persistent kernel.  mode 0: every lane fetches its next input independently
-    // (a long input never idles its warp-mates); mode 1: a warp fetches 32 consecutive
-    // inputs and re-fetches after all 32 finished (lanes stay in SIMT lockstep while
-    // their inputs follow the same path).
-    o << "extern \"C\" __global__ void __launch_bounds__(128, 1) sfg_jit_execute(sfg_prog P, ExecView E, int* next, int mode) {\n"
+    // persistent bulk kernel.  Group-parallel (E.group = G > 1): a warp takes 32/G
+    // consecutive inputs, one per group of G lanes.  Thread-sequential (G = 1):
+    // mode 0 every lane fetches its next input independently; mode 1 a warp fetches
+    // 32 consecutive inputs and re-fetches after all 32 finished.
+    o << "extern \"C\" __global__ void __launch_bounds__(128, 1) sfg_jit_execute(const __grid_constant__ sfg_prog P, const __grid_constant__ ExecView E, int* next, int mode) {\n"
+         "  extern __shared__ __align__(16) uint8_t smem[];\n"
          "  JitRunner R;\n"
          "  R.soft_cap = E.soft_cap;\n"
-         "  if (mode == 0) {\n"
-         "    for (int i = atomicAdd(next, 1); i < E.n; i = atomicAdd(next, 1)) run_input(P, E, i, R);\n"
+         "  const int lane = threadIdx.x & 31;\n"
+         "  const int G = E.group;\n"
+         "  if (G <= 1) {\n"
+         "    const Grp g{1, 0, 1u << lane, nullptr, nullptr, 0};\n"
+         "    if (mode == 0) {\n"
+         "      for (int i = atomicAdd(next, 1); i < E.n; i = atomicAdd(next, 1)) run_input<false>(P, E, i, R, g);\n"
+         "      return;\n"
+         "    }\n"
+         "    while (true) {\n"
+         "      int b = 0;\n"
+         "      if (lane == 0) b = atomicAdd(next, 32);\n"
+         "      b = __shfl_sync(0xffffffffu, b, 0);\n"
+         "      if (b >= E.n) break;\n"
+         "      if (b + lane < E.n) run_input<false>(P, E, b + lane, R, g);\n"
+         "      __syncwarp();\n"
+         "    }\n"
          "    return;\n"
          "  }\n"
-         "  const int lane = threadIdx.x & 31;\n"
+         "  const int per = 32 / G, gi = lane / G;\n"
+         "  GroupSmem* sm = reinterpret_cast<GroupSmem*>(smem + (size_t)((threadIdx.x >> 5) * per + gi) * group_stride(E.tag_cap));\n"
+         "  const unsigned gmask = G == 32 ? 0xffffffffu : ((1u << G) - 1u) << (gi * G);\n"
+         "  const Grp g{G, lane % G, gmask, sm, reinterpret_cast<uint32_t*>(sm + 1), E.tag_cap};\n"
          "  while (true) {\n"
          "    int b = 0;\n"
-         "    if (lane == 0) b = atomicAdd(next, 32);\n"
+         "    if (lane == 0) b = atomicAdd(next, per);\n"
          "    b = __shfl_sync(0xffffffffu, b, 0);\n"
          "    if (b >= E.n) break;\n"
-         "    if (b + lane < E.n) run_input(P, E, b + lane, R);\n"
+         "    if (b + gi < E.n) run_input<true>(P, E, b + gi, R, g);\n"
          "    __syncwarp();\n"
          "  }\n"
          "}\n\n";
-    // tail pass over the deferred (long) inputs with the real budget.  One-warp CTAs;
-    // a warp takes k inputs at a time (lanes >= k idle), so a round's few long inputs
-    // spread over many SMs instead of serializing as divergent lanes of a few warps.
+    // tail passes over the deferred inputs with the real budget (sfg_execute_deferred).
+    // One-warp CTAs; a warp takes k inputs at a time (at most one per group), so a
+    // round's few long inputs spread over many SMs.  seq = 0: the soft-cap list,
+    // group-parallel; seq = 1: the inputs that must run thread-sequentially.
     // Its own register cap (launch bounds) raises the number of resident tail warps.
     o << "#define SFG_TAIL_MINB " << tail_minb << "\n"
-         "extern \"C\" __global__ void __launch_bounds__(32, SFG_TAIL_MINB) sfg_jit_tail(sfg_prog P, ExecView E, int* next, int k) {\n"
+         "extern \"C\" __global__ void __launch_bounds__(32, SFG_TAIL_MINB) sfg_jit_tail(const __grid_constant__ sfg_prog P, const __grid_constant__ ExecView E, int* next, int k, int seq) {\n"
+         "  extern __shared__ __align__(16) uint8_t smem[];\n"
          "  JitRunner R;\n"
          "  R.soft_cap = 0;\n"
          "  const int lane = threadIdx.x;\n"
-         "  const int nd = *E.n_deferred;\n"
+         "  const int32_t* list = seq ? E.deferred_seq : E.deferred;\n"
+         "  const int nd = seq ? *E.n_deferred_seq : *E.n_deferred;\n"
+         "  const int G = seq ? 1 : E.group;\n"
+         "  int per = 32 / G;\n"
+         "  if (k < per) per = k;\n"
+         "  const int gi = lane / G;\n"
+         "  Grp g{1, 0, 1u << lane, nullptr, nullptr, 0};\n"
+         "  if (G > 1) {\n"
+         "    GroupSmem* sm = reinterpret_cast<GroupSmem*>(smem + (size_t)gi * group_stride(E.tag_cap));\n"
+         "    const unsigned gmask = G == 32 ? 0xffffffffu : ((1u << G) - 1u) << (gi * G);\n"
+         "    g = Grp{G, lane % G, gmask, sm, reinterpret_cast<uint32_t*>(sm + 1), E.tag_cap};\n"
+         "  }\n"
          "  while (true) {\n"
          "    int b = 0;\n"
-         "    if (lane == 0) b = atomicAdd(next, k);\n"
+         "    if (lane == 0) b = atomicAdd(next, per);\n"
          "    b = __shfl_sync(0xffffffffu, b, 0);\n"
          "    if (b >= nd) break;\n"
-         "    if (lane < k && b + lane < nd) run_input(P, E, E.deferred[b + lane], R);\n"
+         "    if (gi < per && b + gi < nd) {\n"
+         "      if (G > 1) run_input<true>(P, E, list[b + gi], R, g);\n"
+         "      else run_input<false>(P, E, list[b + gi], R, g);\n"
+         "    }\n"
          "    __syncwarp();\n"
          "  }\n"
          "}\n";
@@ -449,7 +512,7 @@ struct Gen {
 static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_edge_events, std::string& source,
                            std::string& log, std::vector<char>& cubin) {
   sfgjit::Gen g(P, ins);
-  if (const char* tb = getenv("SFG_TAIL_MINB")) g.tail_minb = atoi(tb) >= 1 ? atoi(tb) : 8;
+  if (const char* tb = getenv("SFG_TAIL_MINB")) g.tail_minb = atoi(tb) >= 1 ? atoi(tb) : 16;
   source = g.run(P.n_edges, max_edge_events);
   // process-wide cache: identical programs (same generated source) compile once
   static std::mutex mu;

@@ -102,8 +102,8 @@ class Slot:
         self.allocs, self.allocs_prefix, self.admit, self.pos = i64(cap), i64(cap), i64(cap), i64(cap)
         self.bytes, self.boff, self.sel, self.dst_off = i64(cap), i64(cap), i32(cap), i64(cap * A)
         self.tmp, self.tot = i64((cap + 2047) // 2048 + 8), i64(16)
-        self.counter = i32(4)            # work counters of this slot's execute launches
-        self.deferred = i32(cap)         # long inputs handed to the tail pass
+        self.counter = i32(8)            # work counters of this slot's execute launches
+        self.deferred = i32(2 * cap)     # tail-pass lists: soft-cap deferrals, sequential re-runs
         # triage partials (merged across ranks between the phases, sfg.h):
         # MIN: [stop, fatal, first_hit[E], key_first[K]]; SUM: [edge_delta[E], key_count[K], entered[16]]
         E0, K0 = dc.E, dc.K
@@ -346,12 +346,16 @@ class DeviceCampaign:
         if self.timing:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             ev[0].record(st)
-        soft = soft_cap if (self.jit and cd is not None) else 0
+        # without a corpus (execute_testcases) payloads cannot be re-materialized:
+        # no deferral lists -> thread-sequential, no soft cap
+        tail = self.jit and cd is not None
+        soft = soft_cap if tail else 0
         _native.check(self.L.sfg_execute(
             self.h, n, S.children.data_ptr(), S.vals.data_ptr(), S.work_base.data_ptr(), S.work.data_ptr(),
             S.verdicts.data_ptr(), S.ecnt.data_ptr(), _ptr(S.readouts), S.ro_base.data_ptr(), _ptr(S.overlay),
-            S.counter.data_ptr(), soft, S.deferred.data_ptr(), st.cuda_stream), "execute")
-        if soft:
+            S.counter.data_ptr(), soft, S.deferred.data_ptr() if tail else None, self.max_entry_work,
+            st.cuda_stream), "execute")
+        if tail:
             if self.timing:
                 evb = torch.cuda.Event(enable_timing=True)
                 evb.record(st)
@@ -361,7 +365,7 @@ class DeviceCampaign:
                 self.h, ctypes.byref(cd), n, S.children.data_ptr(), S.vals.data_ptr(), S.work_base.data_ptr(),
                 S.work.data_ptr(), S.verdicts.data_ptr(), S.ecnt.data_ptr(), _ptr(S.readouts),
                 S.ro_base.data_ptr(), _ptr(S.overlay), S.counter.data_ptr(), S.deferred.data_ptr(),
-                st.cuda_stream), "execute_deferred")
+                self.max_entry_work, st.cuda_stream), "execute_deferred")
         if self.timing:
             ev[1].record(st)
             S.exec_ev = ev

@@ -23,11 +23,12 @@ for cap in [int(x) for x in os.environ.get("CAPS", "0,8192,32768,131072").split(
         res = dc.run_round(it, R); it += R
         torch.cuda.synchronize()
         k3.append(res.slot.exec_ev[0].elapsed_time(res.slot.exec_ev[1]))
-    nd = int(res.slot.counter[1].item())
+    nd = int(res.slot.counter[1].item()); nseq = int(res.slot.counter[3].item())
+    bulk = res.slot.exec_ev[0].elapsed_time(res.slot.bulk_ev) if getattr(res.slot, "bulk_ev", None) else -1
     v = res.slot.verdicts[:R * VERDICT.itemsize].cpu().numpy().view(VERDICT)
     ret = v["retired"].astype(np.int64)
     print(f"soft_cap={cap:>7d} k3_ms={[round(x, 2) for x in k3]} execs/s={R / np.mean(k3) * 1e3:,.0f} "
-          f"deferred={nd} retired_sum={ret.sum():,} max={ret.max():,}", flush=True)
+          f"bulk_ms={bulk:.2f} deferred={nd} seq={nseq} retired_sum={ret.sum():,} max={ret.max():,}", flush=True)
     dc.close(); del dc; torch.cuda.empty_cache()
 
 for depth in [int(x) for x in os.environ.get("DEPTHS", "8,16,32").split(",")]:

@@ -1,0 +1,48 @@
+"""Pipelined-round timeline without extra synchronization (GPU): per round, when
+its execute pass started, when the bulk pass and the tail passes ended (CUDA
+events on the round's stream, read after the run), plus deferral counts.
+Usage: python tools/pipe_probe.py [workload] [R] [depth] [steps]"""
+import sys, time
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import numpy as np
+import torch
+from paper_2603_05725_b200.engine import DeviceCampaign
+from paper_2603_05725_b200.workloads import load
+
+name = sys.argv[1] if len(sys.argv) > 1 else "matmul"
+R = int(sys.argv[2]) if len(sys.argv) > 2 else 65536
+depth = int(sys.argv[3]) if len(sys.argv) > 3 else 32
+steps = int(sys.argv[4]) if len(sys.argv) > 4 else 64
+dc = DeviceCampaign(load(name), master_seed=11)
+dc.run_rounds(1, 1 + 4 * R, R, depth=depth)
+torch.cuda.synchronize()
+dc.timing = True
+t0 = torch.cuda.Event(enable_timing=True)
+t0.record()
+rows = []
+host0 = time.perf_counter()
+
+
+def on_round(res):
+    S = res.slot
+    rows.append((S.exec_ev, getattr(S, "bulk_ev", None), S.counter[:8].clone(), time.perf_counter() - host0))
+
+
+it = 1 + 4 * R
+res = dc.run_rounds(it, it + steps * R, R, depth=depth, on_round=on_round)
+torch.cuda.synchronize()
+wall = time.perf_counter() - host0
+out = []
+for (s, e), b, cnt, h in rows:
+    c = cnt.cpu().numpy()
+    out.append((t0.elapsed_time(s), t0.elapsed_time(b) if b else -1, t0.elapsed_time(e), h * 1e3, c[1], c[3]))
+a = np.array(out)
+print(f"{name} R={R} depth={depth} steps={steps}: wall/step={wall / steps * 1e3:.2f} ms "
+      f"execs/s={sum(r.executed for r in res) / wall:,.0f}")
+print(f"  bulk dur ms: mean {np.mean(a[:, 1] - a[:, 0]):.2f} max {np.max(a[:, 1] - a[:, 0]):.2f}; "
+      f"tail dur ms: mean {np.mean(a[:, 2] - a[:, 1]):.2f} max {np.max(a[:, 2] - a[:, 1]):.2f}; "
+      f"deferred mean {a[:, 4].mean():.0f} seq mean {a[:, 5].mean():.0f}")
+print("round  exec_start  bulk_end  tail_end  host_final  n_def  n_seq")
+for k, r in enumerate(out[:: max(1, len(out) // 24)]):
+    print(f"{k:5d} {r[0]:11.1f} {r[1]:9.1f} {r[2]:9.1f} {r[3]:11.1f} {int(r[4]):6d} {int(r[5]):6d}")
