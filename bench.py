@@ -133,6 +133,7 @@ class ClockSampler:
 
 
 def run_ours(a):
+    import paper_2603_05725_b200  # noqa: F401  (sets CUDA_DEVICE_MAX_CONNECTIONS before the context exists)
     import torch
     import torch.distributed as dist
 
@@ -181,7 +182,9 @@ def run_ours(a):
     it += a.steps * R
     launches = dc.launches - launches0
     executed = sum(r.executed for r in results)
-    k3_ms = [s.elapsed_time(e) for s, e in dc.exec_events]
+    # K3 per round: bulk pass (every input, long ones deferred) and the whole execute
+    bulk_ms = [s.elapsed_time(b) for s, b, e in dc.exec_events if b is not None]
+    k3_ms = [s.elapsed_time(e) for s, b, e in dc.exec_events]
     t_local = t0.elapsed_time(t1) / 1000.0
     t = torch.tensor([t_local], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -190,25 +193,38 @@ def run_ours(a):
     value = executed / t_max
     ms = [t_max * 1000 / a.steps]
 
-    # ---- end to end through the public round API with host buffers
-    e2e = run_e2e(a, dc, torch, R, it, all_streams_done)
+    # ---- end to end through the public API with host buffers
+    e2e = run_e2e(a, m, torch, R, world)
 
-    # ---- dominant kernel roofline (execute: issue-bound interpreter; HBM figure reported honestly)
+    # ---- dominant kernel roofline.  K3's bulk pass (sfg_jit_execute) runs every input
+    # of the round; its algorithmic off-chip bytes are the child payload read once plus
+    # the verdict and edge-count rows written.  It is bound by the
+    # issue latency of each simulated thread's dependent instruction chain, not by HBM:
+    # the HBM fraction is reported as measured, the issue figures beside it.
     peaks = json.loads((REPO / "MEASURED_PEAKS.json").read_text()) if (REPO / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    k3_avg_s = statistics.mean(k3_ms) / 1000.0
+    bulk_s = statistics.mean(bulk_ms) / 1000.0
     bytes_exec = dc.algorithmic_exec_bytes()
-    achieved = bytes_exec * a.round / k3_avg_s / 1e9
+    achieved = bytes_exec * a.round / bulk_s / 1e9
     retired = dc.retired_mean(results[-1].slot)
     collectives = comm.calls
+    prof = {}
+    pf = REPO / "profiles" / "r01_ncu_bulk_execute.json"
+    if pf.exists():
+        prof = json.loads(pf.read_text())
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-            "traffic": None, "kernel": "sfg_execute_kernel", "bytes_per_exec": bytes_exec,
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
-            "note": "execute is SM-issue bound (interpreter); see issue_roofline"}
+            "traffic": prof.get("dram_bytes_per_launch"), "kernel": "sfg_jit_execute (K3 bulk pass)",
+            "bytes_per_exec": bytes_exec, "launch_ms": statistics.mean(bulk_ms),
+            "peak_source": ("MEASURED_PEAKS.json hbm_gbs (of measured)" if peaks else "fallback 6.65 TB/s (of fallback)"),
+            "traffic_source": prof.get("source"),
+            "note": "latency-bound dependent integer/branch chains per simulated thread; see issue_roofline"}
     sm_mhz = clk.summary().get("sm_mhz") or 1965.0
-    issue = {"sim_instr_per_s": retired * a.round / k3_avg_s, "sim_instr_per_exec": retired,
-             "k3_ms_per_launch": statistics.mean(k3_ms),
-             "rounds_in_flight": D, "soft_cap": dc.soft_cap,
+    issue = {"sim_instr_per_s": retired * R / (t_max / a.steps), "sim_instr_per_exec": retired,
+             "bulk_ms_per_launch": statistics.mean(bulk_ms), "k3_ms_per_round": statistics.mean(k3_ms),
+             "k3_ms_per_round_max": max(k3_ms), "rounds_in_flight": D, "soft_cap": dc.soft_cap,
+             "ncu_issue_slots_busy_pct": prof.get("issue_slots_busy_pct"),
+             "ncu_warp_cycles_per_issued": prof.get("warp_cycles_per_issued"),
+             "ncu_active_threads_per_warp": prof.get("active_threads_per_warp"),
              "lane_instr_peak_per_s": 148 * 4 * 32 * sm_mhz * 1e6}
 
     if rank == 0:
@@ -233,40 +249,44 @@ def run_ours(a):
         dist.destroy_process_group()
 
 
-def run_e2e(a, dc, torch, R, it, all_streams_done):
-    """Same metric through the public round API with host buffers: the corpus is
-    uploaded from pinned host memory before the run and every round's verdict
-    records are copied back to pinned host memory as the round is finalized."""
-    host = dc.corpus_host_pinned()
-    r_loc = a.round
-    vers = [torch.empty(r_loc * 112, dtype=torch.uint8, pin_memory=True) for _ in range(a.depth)]
-    h2d = sum(t.numel() for t in host)
-    d2h = r_loc * 112
-
-    def on_round(res):
-        with torch.cuda.stream(res.slot.stream):
-            vers[dc.rounds % a.depth].copy_(res.slot.verdicts[:res.slot.n * 112], non_blocking=True)
-
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record()
-    dc.load_corpus_from_host(host)
-    torch.cuda.current_stream().synchronize()
-    res = dc.run_rounds(it, it + a.steps * R, R, depth=a.depth, on_round=on_round)
-    all_streams_done(t1)
+def run_e2e(a, m, torch, R, world):
+    """The same metric end to end through the public API a user calls:
+    ``campaign.fuzz_loop(manifest, CampaignConfig)`` (drop-in for the reference's
+    ``fuzz_loop``, campaign.py:683), wall-clocked around the call.  Its host<->device
+    traffic is counted from the tensors the campaign copies: program tables, the
+    post-INIT baseline image and the seed corpus up; every round's verdict scalars,
+    dedupe-key counts and new findings / admissions down."""
+    from paper_2603_05725_b200.campaign import CampaignConfig, fuzz_loop
+    import torch.distributed as dist
+    steps = max(a.steps, 1)
+    cfg = CampaignConfig(master_seed=11, iterations=steps * R, round_size=R, pipeline_depth=a.depth,
+                         distributed=world > 1)
     torch.cuda.synchronize()
-    t = t0.elapsed_time(t1) / 1000.0
-    ex = sum(r.executed for r in res)
-    return {"value": ex / t, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    s = fuzz_loop(m, cfg)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    t = torch.tensor([wall], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    wall = float(t.item())
+    tr = s.device_transfer
+    return {"value": s.compute_runs / wall, "unit": UNIT, "h2d_bytes_per_step": tr["h2d_bytes"] / steps,
+            "d2h_bytes_per_step": tr["d2h_bytes"] / steps, "wall_s": wall, "execs": s.compute_runs,
+            "api": "campaign.fuzz_loop(manifest, CampaignConfig) -> CampaignSummary",
+            "includes": "program build (JIT cache hit), INIT baseline, corpus upload, all rounds, result objects",
+            "findings_unique": len(s.findings), "stop": s.stop_reason}
 
 
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=16)
+    p.add_argument("--steps", type=int, default=64)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--round", type=int, default=65536)
-    p.add_argument("--depth", type=int, default=16, help="rounds in flight (speculative pipelining)")
+    p.add_argument("--depth", type=int, default=32, help="rounds in flight (speculative pipelining)")
     p.add_argument("--workload", default="matmul")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--cpu-seconds", type=float, default=15.0)

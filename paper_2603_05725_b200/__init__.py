@@ -9,3 +9,10 @@ Public API mirrors the reference (``simt_forge``): ``load_harness``,
 """
 
 __version__ = "0.1.0"
+
+import os as _os
+
+# Rounds in flight run on separate CUDA streams; with the default 8 hardware work
+# queues, streams alias and a round's short kernels queue behind another round's
+# long tail pass.  Takes effect if set before the process creates its CUDA context.
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")

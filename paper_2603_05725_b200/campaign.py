@@ -71,8 +71,11 @@ class CampaignConfig:
     diff_readback: bool = False
     hooks: object = None
     round_size: int = 65536
-    pipeline_depth: int = 8
+    pipeline_depth: int = 32
     device: str | None = None
+    # shard every round over the ranks of the initialized torch.distributed group
+    # (one process per GPU, per-round merge, shard.py); results do not depend on it
+    distributed: bool = False
 
 
 @dataclass
@@ -141,7 +144,11 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
         (out_dir / "harness.man").write_text(manifest.portable_text("program.sir"))
     t0 = time.perf_counter()
     deadline = t0 + config.max_wall_seconds if config.max_wall_seconds else None
-    dc = DeviceCampaign(manifest, master_seed=config.master_seed, mem=config.mem_config,
+    comm = None
+    if config.distributed:
+        from .shard import RoundComm
+        comm = RoundComm()
+    dc = DeviceCampaign(manifest, master_seed=config.master_seed, mem=config.mem_config, comm=comm,
                         mutation=config.mutation, budget=config.instruction_budget,
                         window=config.admission_window, recent_weight=config.recent_weight,
                         diff_readback=config.diff_readback, stop_on_first_finding=config.stop_on_first_finding,
@@ -185,9 +192,12 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
 
             def should_continue():
                 # wall-clock limit checked before every round submission (campaign.py:733-735);
-                # rounds already in flight are finalized
-                if deadline is not None and time.perf_counter() > deadline:
-                    clock["expired"] = True
+                # rounds already in flight are finalized.  Sharded: the ranks agree (MAX).
+                if deadline is not None and not clock["expired"]:
+                    late = time.perf_counter() > deadline
+                    if dc.comm.world > 1:
+                        late = bool(dc.comm.all_gather_object(late).count(True))
+                    clock["expired"] = late
                 return not clock["expired"]
 
             dc.run_rounds(rng_.start, rng_.stop, config.round_size, depth=config.pipeline_depth,
@@ -216,6 +226,8 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
         (out_dir / "summary.rec").write_text(summary.to_rec())
         (out_dir / "timing.rec").write_text(
             f"timing v1\nwall_seconds={wall:.6f} execs_per_second={summary.execs_per_second:.2f}\n")
+    # host<->device traffic of the campaign (not a reference field; bench e2e accounting)
+    summary.device_transfer = {"h2d_bytes": dc.h2d_bytes, "d2h_bytes": dc.d2h_bytes, "rounds": dc.rounds}
     dc.close()
     return summary
 

@@ -497,7 +497,8 @@ enum { LG_OK = 0, LG_STOP = 1, LG_DEFER = 2, LG_SEQ = 3 };
 // One launch's simulated threads on the lanes of a group, G at a time (see above).
 template <class Runner>
 SFG_DEV int run_launch_group(const sfg_prog& P, const sfg_hostop& op, Lane& L, Mem& M, sfg_verdict& V,
-                             const Pre& pre, Runner& R, const Grp& g, uint64_t& total_retired, int ntags) {
+                             const Pre& pre, Runner& R, const Grp& g, uint64_t& total_retired, int ntags,
+                             int& reruns) {
   const int T = op.grid * op.block;
   uint32_t* wk = reinterpret_cast<uint32_t*>(M.work);  // 16-aligned, work_bytes a multiple of 16
   uint32_t* snap = g.tags + g.tag_cap;
@@ -532,6 +533,7 @@ SFG_DEV int run_launch_group(const sfg_prog& P, const sfg_hostop& op, Lane& L, M
     __syncwarp(g.mask);
     if (cf) {
       // undo the chunk and re-run it thread-sequentially on the first lane
+      ++reruns;
       for (int x = g.gl; x < ntags; x += g.G) wk[x] = snap[x];
       R.restore_edges();
       __syncwarp(g.mask);
@@ -624,6 +626,7 @@ SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R, c
   const uint64_t arrays_end = ch.work_bytes - (uint64_t)P.named_work_bytes;
   const int ntags = (int)((ch.work_bytes + 3) / 4);
   int defer_kind = 0;  // 1: soft cap reached (deferred), 2: re-run thread-sequentially (deferred_seq)
+  int seq_reruns = 0;  // group-parallel chunks undone and re-run sequentially (diagnostics)
   if (GRP && ntags > g.tag_cap) defer_kind = 2;
 
   bool stop = defer_kind != 0;
@@ -726,7 +729,7 @@ SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R, c
     V.launches++;
     if constexpr (GRP) {
       __syncwarp(g.mask);  // host-op stores (made identically by every lane) visible to all
-      const int lg = run_launch_group(P, op, L, M, V, pre, R, g, total_retired, ntags);
+      const int lg = run_launch_group(P, op, L, M, V, pre, R, g, total_retired, ntags, seq_reruns);
       if (lg == LG_STOP) stop = true;
       else if (lg == LG_DEFER) { defer_kind = 1; stop = true; }
       else if (lg == LG_SEQ) { defer_kind = 2; stop = true; }
@@ -760,7 +763,7 @@ SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R, c
   uint32_t smid;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
   asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-  V.where = (uint64_t)(smid & 0xff) | ((t_end - t_start) << 8);
+  V.where = (uint64_t)(smid & 0xff) | ((uint64_t)(seq_reruns > 0) << 8) | ((t_end - t_start) << 9);
   if (g.gl == 0) E.verdicts[i] = V;
 }
 

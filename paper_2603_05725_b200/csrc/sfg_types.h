@@ -169,7 +169,7 @@ typedef struct sfg_verdict { // 112 bytes
   int32_t launches, allocs;
   uint32_t entered;                           // bit k: kernel k launched
   int32_t key;                                // dedupe slot, -1 none
-  uint64_t where;                             // diagnostics: SM id (bits 0-7), ns spent (bits 8-63)
+  uint64_t where;                             // diagnostics: SM id (bits 0-7), sequential re-run (bit 8), ns (bits 9-63)
 } sfg_verdict;
 
 // program-wide scalars passed by value to every kernel

@@ -116,6 +116,7 @@ class Slot:
         self.pin_tot = torch.empty(16, dtype=torch.int64, pin_memory=True)
         self.pin_sc = torch.empty(2, dtype=torch.int32, pin_memory=True)
         self.pin_gath = torch.empty((dc.comm.world, 2), dtype=torch.int64, pin_memory=True)
+        self.pin_kc = torch.empty(max(K0, 1), dtype=torch.int64, pin_memory=True)
         self.work, self.work_cap = None, 0
         self.readouts = None
         self.ev_counts = torch.cuda.Event()
@@ -171,6 +172,9 @@ class DeviceCampaign:
         self.K = self.low.n_keys
         recs = record_table(self.base, self.low.labels)
         self.blob = torch.frombuffer(bytearray(self.base.blob), dtype=torch.uint8).to(self.dev)
+        # host<->device bytes moved by the campaign (bench e2e accounting)
+        self.h2d_bytes = len(self.base.blob)
+        self.d2h_bytes = 0
         h = ctypes.c_void_p()
         P = self.low.prog_bytes()
         _native.check(self.L.sfg_program_create(
@@ -179,6 +183,8 @@ class DeviceCampaign:
             self.low.const_blob, len(self.low.const_blob), self.blob.data_ptr(), ctypes.byref(h)),
             "sfg_program_create")
         self.h = h
+        self.h2d_bytes += (len(P) + self.low.ins.nbytes + self.low.hostops.nbytes + self.low.binds.nbytes +
+                           recs.nbytes + len(self.low.const_blob))
         self.jit = self.L.sfg_program_jit_source(self.h, None, 0) > 0
         # global campaign state on device
         self.edge_total = torch.zeros(max(self.E, 1), dtype=torch.int64, device=self.dev)
@@ -259,6 +265,7 @@ class DeviceCampaign:
         if blob:
             self.c_data[:len(blob)].copy_(torch.frombuffer(blob, dtype=torch.uint8))
         self.n_corpus, self.corpus_bytes = len(seeds), len(blob)
+        self.h2d_bytes += metas.nbytes + v.nbytes + len(blob)
 
     def corpus_dev(self) -> CorpusDev:
         return CorpusDev(self.c_meta.data_ptr(), self.c_vals.data_ptr(), self.c_data.data_ptr(),
@@ -360,7 +367,7 @@ class DeviceCampaign:
                 evb = torch.cuda.Event(enable_timing=True)
                 evb.record(st)
                 S.bulk_ev = evb
-            self.launches += 2
+            self.launches += 4   # two passes: re-materialize + tail kernel each
             _native.check(self.L.sfg_execute_deferred(
                 self.h, ctypes.byref(cd), n, S.children.data_ptr(), S.vals.data_ptr(), S.work_base.data_ptr(),
                 S.work.data_ptr(), S.verdicts.data_ptr(), S.ecnt.data_ptr(), _ptr(S.readouts),
@@ -369,7 +376,8 @@ class DeviceCampaign:
         if self.timing:
             ev[1].record(st)
             S.exec_ev = ev
-            self.exec_events.append(ev)
+            # (execute start, bulk pass end, tail passes end) of this round
+            self.exec_events.append((ev[0], getattr(S, "bulk_ev", None) if tail else None, ev[1]))
 
     # ---- finalize: triage in order ------------------------------------------------------
     def _finalize(self, S: Slot) -> RoundResult:
@@ -408,6 +416,9 @@ class DeviceCampaign:
             S.pin_sc.copy_(S.scalars, non_blocking=True)
             S.pin_tot.copy_(S.tot, non_blocking=True)
             S.pin_gath.copy_(gath, non_blocking=True)
+            if self.K:
+                S.pin_kc[:self.K].copy_(S.kcount, non_blocking=True)
+            self.d2h_bytes += S.pin_sc.nbytes + S.pin_tot.nbytes + S.pin_gath.nbytes + 8 * self.K
             ev = torch.cuda.Event()
             ev.record(st)
         ev.synchronize()
@@ -505,6 +516,7 @@ class DeviceCampaign:
         base = min(offs) if offs else 0
         top = max([int(v["data_off"]) + int(v["nbytes"]) for v in vals if v["kind"] == 2] + [base])
         data = self.c_data[base:top].cpu().numpy().tobytes() if top > base else b""
+        self.d2h_bytes += meta.nbytes + vals.nbytes + chld.nbytes + len(data)
         for j in range(hi - lo):
             row = vals[j * self.n_args:(j + 1) * self.n_args]
             args = unpack_values(row, data, base)
@@ -522,11 +534,12 @@ class DeviceCampaign:
         decoded by the rank owning their first input and shared with all ranks."""
         comm = self.comm
         with torch.cuda.stream(S.stream):
-            kc = S.kcount.cpu().numpy()
+            kc = S.pin_kc.numpy()[:self.K]   # copied with the round's scalars (_finalize)
             hot = np.nonzero(kc)[0]
             if not len(hot):
                 return []
             kf = S.kfirst.cpu().numpy()
+            self.d2h_bytes += kf.nbytes
             fresh = []
             for k in hot:
                 ks = self.key_strings.get(int(k))
@@ -541,6 +554,7 @@ class DeviceCampaign:
                 idx = torch.tensor([g - S.i_base for g, _ in mine], dtype=torch.long, device=self.dev)
                 vt = _np(S.verdicts.view(-1, VERDICT.itemsize)[idx].reshape(-1), VERDICT)
                 ap = S.allocs_prefix[idx].cpu().numpy()
+                self.d2h_bytes += vt.nbytes + ap.nbytes
                 for j, (g, k) in enumerate(mine):
                     reps.append((g, k, decode_verdict(vt[j], self.low, S.round_it0 + g,
                                                       self._id_base(S, int(ap[j])))))

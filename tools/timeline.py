@@ -34,11 +34,11 @@ def on_round(res):
     d = S.deferred[:nd].cpu().numpy()
     w = v["where"][d] if nd else np.zeros(0, np.uint64)
     sms = collections.Counter((w & 0xff).tolist())
-    dur = (w >> 8) / 1e6
+    dur = (w >> 9) / 1e6
     rows.append((t0.elapsed_time(s), t0.elapsed_time(b) if b else -1, t0.elapsed_time(e),
                  (time.perf_counter() - host0) * 1e3, nd, len(sms), max(sms.values()) if sms else 0,
                  float(dur.max()) if nd else 0, float(np.median(dur)) if nd else 0,
-                 float(((v["where"] >> 8) / 1e6).max())))
+                 float(((v["where"] >> 9) / 1e6).max())))
 
 
 it = 1 + 2 * R
