@@ -106,7 +106,8 @@ int sfg_regen(const sfg_program* p, const sfg_corpus_dev* c, int n_sel, const in
 int sfg_execute(const sfg_program* p, int n, const void* children, const void* vals,
                 const uint64_t* work_base, uint8_t* work, void* verdicts, uint32_t* edge_counts,
                 uint8_t* readouts, const uint64_t* readout_base, uint64_t* overlay, int* work_counter,
-                uint64_t soft_cap, int32_t* deferred, int64_t max_work_bytes, void* stream);
+                uint64_t soft_cap, int32_t* deferred, int64_t max_work_bytes, const int32_t* order,
+                void* stream);
 int sfg_execute_deferred(const sfg_program* p, const sfg_corpus_dev* c, int n, const void* children,
                          const void* vals, const uint64_t* work_base, uint8_t* work, void* verdicts,
                          uint32_t* edge_counts, uint8_t* readouts, const uint64_t* readout_base,
@@ -114,6 +115,12 @@ int sfg_execute_deferred(const sfg_program* p, const sfg_corpus_dev* c, int n, c
                          void* stream);
 /* Lanes per input of the program's group-parallel mode (1 = thread-sequential). */
 int sfg_program_group(const sfg_program* p);
+/* Bulk-pass schedule: order[0..n) = a permutation of the round's inputs grouped by
+ * a hash of their scalar arguments and array shapes (inputs likely to take the
+ * same path share warps).  Pass it as sfg_execute's `order` (NULL = identity).
+ * scratch: sfg_order_scratch_ints(n) ints of device memory. */
+size_t sfg_order_scratch_ints(int n);
+int sfg_order(const sfg_program* p, int n, const void* vals, int32_t* order, int32_t* scratch, void* stream);
 /* Triage in three stream-ordered phases so that a multi-GPU campaign can merge
  * the per-rank partials between them: a rank owns the global
  * round indices [i_base, i_base + n).  All indices written are GLOBAL round

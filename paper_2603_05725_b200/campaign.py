@@ -71,7 +71,7 @@ class CampaignConfig:
     diff_readback: bool = False
     hooks: object = None
     round_size: int = 65536
-    pipeline_depth: int = 32
+    pipeline_depth: int = 24
     device: str | None = None
     # shard every round over the ranks of the initialized torch.distributed group
     # (one process per GPU, per-round merge, shard.py); results do not depend on it

@@ -19,6 +19,7 @@ struct sfg_program {
   int sms = 0;
   int tail_k = 1;                     // long inputs per tail warp (group-parallel pass)
   int tail_k_seq = 32;                // inputs per warp of the thread-sequential re-run pass
+  int tail_ctas = 512;                // one-warp CTAs of the long-input pass
   int group = 1;                      // lanes per input of the tail pass (group-parallel launches)
   int bulk_group = 1;                 // lanes per input of the bulk pass (1 = thread-sequential)
   int jit_block = 128;                // CTA size of the persistent kernel
@@ -50,6 +51,7 @@ static_assert(sizeof(sfg_prog) < 4096, "sfg_prog must fit the kernel parameter s
 #include "execute.cu"
 #include "triage.cu"
 #include "ctxmap.cu"
+#include "order.cu"
 #include "jit.cu"
 
 static thread_local std::string g_err;
@@ -219,6 +221,7 @@ int sfg_program_create(const void* prog, size_t prog_bytes, const void* ins, siz
       if (cudaDeviceGetLimit(&cur, cudaLimitStackSize) == cudaSuccess && need > cur)
         cudaDeviceSetLimit(cudaLimitStackSize, need);
     }
+    if (const char* tc = getenv("SFG_TAIL_CTAS")) p->tail_ctas = atoi(tc) >= 1 ? atoi(tc) : 512;
     if (const char* tq = getenv("SFG_TAIL_KSEQ")) p->tail_k_seq = atoi(tq) >= 1 && atoi(tq) <= 32 ? atoi(tq) : 32;
     if (const char* tk = getenv("SFG_TAIL_K")) p->tail_k = atoi(tk) >= 1 && atoi(tk) <= 32 ? atoi(tk) : 1;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)p->jit_tail, 32, kTailSmem);
@@ -326,11 +329,26 @@ int sfg_regen(const sfg_program* p, const sfg_corpus_dev* c, int n_sel, const in
 
 int sfg_program_group(const sfg_program* p) { return p->jit_kernel ? p->group : 1; }
 
+size_t sfg_order_scratch_ints(int n) { return (size_t)kOrderBuckets + (size_t)(n > 0 ? n : 0); }
+
+int sfg_order(const sfg_program* p, int n, const void* vals, int32_t* order, int32_t* scratch, void* stream) {
+  if (n <= 0) return 0;
+  int* hist = scratch;
+  int* sig = scratch + kOrderBuckets;
+  cudaError_t e = cudaMemsetAsync(hist, 0, kOrderBuckets * sizeof(int), S(stream));
+  if (e != cudaSuccess) return fail("sfg_order", e);
+  sfg_order_hist_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(p->P, (const sfg_val*)vals, n, hist, sig);
+  sfg_order_scan_kernel<<<1, 128, 0, S(stream)>>>(hist);
+  sfg_order_scatter_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(n, sig, hist, order);
+  SFG_CHECK_LAUNCH("sfg_order");
+  return 0;
+}
+
 
 int sfg_execute(const sfg_program* p, int n, const void* children, const void* vals, const uint64_t* work_base,
                 uint8_t* work, void* verdicts, uint32_t* edge_counts, uint8_t* readouts,
                 const uint64_t* readout_base, uint64_t* overlay, int* work_counter, uint64_t soft_cap,
-                int32_t* deferred, int64_t max_work_bytes, void* stream) {
+                int32_t* deferred, int64_t max_work_bytes, const int32_t* order, void* stream) {
   if (n <= 0) {
     if (work_counter) cudaMemsetAsync(work_counter, 0, 8 * sizeof(int), S(stream));
     return 0;
@@ -339,7 +357,7 @@ int sfg_execute(const sfg_program* p, int n, const void* children, const void* v
              (const sfg_child*)children, (const sfg_val*)vals, work_base, work,
              (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, overlay, n,
              0ull, deferred, work_counter ? work_counter + 1 : nullptr,
-             deferred ? deferred + n : nullptr, work_counter ? work_counter + 3 : nullptr, 1, 0};
+             deferred ? deferred + n : nullptr, work_counter ? work_counter + 3 : nullptr, 1, 0, order};
   if (p->jit_kernel) {
     if (work_counter == nullptr || (deferred == nullptr && soft_cap != 0)) {
       g_err = "sfg_execute: the specialized kernel needs a per-launch work counter (and deferred lists for soft_cap)";
@@ -389,7 +407,7 @@ int sfg_execute_deferred(const sfg_program* p, const sfg_corpus_dev* c, int n, c
   ExecView E{p->ins, p->hostops, p->binds, p->recs, p->base_blob, p->const_blob,
              (const sfg_child*)children, (const sfg_val*)vals, work_base, work,
              (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, overlay, n,
-             0ull, deferred, work_counter + 1, deferred + n, work_counter + 3, p->group, 0};
+             0ull, deferred, work_counter + 1, deferred + n, work_counter + 3, p->group, 0, nullptr};
   for (int pass = 0; pass < 2; ++pass) {
     // pristine payloads again (the earlier attempt's stores landed in the work regions)
     int32_t* list = pass == 0 ? deferred : deferred + n;
@@ -412,8 +430,12 @@ int sfg_execute_deferred(const sfg_program* p, const sfg_corpus_dev* c, int n, c
       smem = (size_t)per * group_stride(E.tag_cap);
     }
     void* args[] = {(void*)&p->P, (void*)&E, (void*)&next, (void*)&k, (void*)&seq};
-    cudaError_t e = cudaLaunchKernel((const void*)p->jit_tail, dim3((unsigned)p->tail_grid), dim3(32), args, smem,
-                                     S(stream));
+    // persistent one-warp CTAs sized for the usual load (a few hundred long inputs per
+    // round, far fewer re-runs): a kernel completes only once every CTA has had a slot,
+    // and slots are scarce while other rounds run, so idle CTAs would add latency
+    const int want = pass == 0 ? p->tail_ctas : p->tail_ctas / 4 + 1;
+    const unsigned grid = (unsigned)(want < p->tail_grid ? want : p->tail_grid);
+    cudaError_t e = cudaLaunchKernel((const void*)p->jit_tail, dim3(grid), dim3(32), args, smem, S(stream));
     if (e != cudaSuccess) return fail("sfg_execute_deferred (jit)", e);
   }
   return 0;

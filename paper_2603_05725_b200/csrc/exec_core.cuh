@@ -90,6 +90,8 @@ struct ExecView {
   // words in shared memory (4 bytes of work region per word)
   int group;
   int tag_cap;
+  // bulk-pass schedule: the j-th fetched input is order[j] (sfg_order), null = j
+  const int32_t* order;
 };
 
 namespace {

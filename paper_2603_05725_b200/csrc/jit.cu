@@ -425,6 +425,7 @@ struct Gen {
   }
 
   int tail_minb = 12;
+  int bulk_minb = 1;
 
   std::string run(int n_edges, uint64_t max_edge_events) {
     edge_ovf_checks = max_edge_events >= 0xFFFFFFFFull;
@@ -469,7 +470,8 @@ struct Gen {
     // consecutive inputs, one per group of G lanes.  Thread-sequential (G = 1):
     // mode 0 every lane fetches its next input independently; mode 1 a warp fetches
     // 32 consecutive inputs and re-fetches after all 32 finished.
-    o << "extern \"C\" __global__ void __launch_bounds__(128, 1) sfg_jit_execute(const __grid_constant__ sfg_prog P, const __grid_constant__ ExecView E, int* next, int mode) {\n"
+    o << "#define SFG_BULK_MINB " << bulk_minb << "\n";
+    o << "extern \"C\" __global__ void __launch_bounds__(128, SFG_BULK_MINB) sfg_jit_execute(const __grid_constant__ sfg_prog P, const __grid_constant__ ExecView E, int* next, int mode) {\n"
          "  extern __shared__ __align__(16) uint8_t smem[];\n"
          "  JitRunner R;\n"
          "  R.soft_cap = E.soft_cap;\n"
@@ -486,7 +488,7 @@ struct Gen {
          "      if (lane == 0) b = atomicAdd(next, 32);\n"
          "      b = __shfl_sync(0xffffffffu, b, 0);\n"
          "      if (b >= E.n) break;\n"
-         "      if (b + lane < E.n) run_input<false>(P, E, b + lane, R, g);\n"
+         "      if (b + lane < E.n) run_input<false>(P, E, E.order ? E.order[b + lane] : b + lane, R, g);\n"
          "      __syncwarp();\n"
          "    }\n"
          "    return;\n"
@@ -500,7 +502,7 @@ struct Gen {
          "    if (lane == 0) b = atomicAdd(next, per);\n"
          "    b = __shfl_sync(0xffffffffu, b, 0);\n"
          "    if (b >= E.n) break;\n"
-         "    if (b + gi < E.n) run_input<true>(P, E, b + gi, R, g);\n"
+         "    if (b + gi < E.n) run_input<true>(P, E, E.order ? E.order[b + gi] : b + gi, R, g);\n"
          "    __syncwarp();\n"
          "  }\n"
          "}\n\n";
@@ -550,6 +552,7 @@ static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_e
                            std::string& log, std::vector<char>& cubin) {
   sfgjit::Gen g(P, ins);
   if (const char* tb = getenv("SFG_TAIL_MINB")) g.tail_minb = atoi(tb) >= 1 ? atoi(tb) : 12;
+  if (const char* bb = getenv("SFG_BULK_MINB")) g.bulk_minb = atoi(bb) >= 1 ? atoi(bb) : 1;
   source = g.run(P.n_edges, max_edge_events);
   // process-wide cache: identical programs (same generated source) compile once
   static std::mutex mu;

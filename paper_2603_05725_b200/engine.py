@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import time
 from collections import deque
 from dataclasses import dataclass
 
@@ -104,6 +105,8 @@ class Slot:
         self.tmp, self.tot = i64((cap + 2047) // 2048 + 8), i64(16)
         self.counter = i32(8)            # work counters of this slot's execute launches
         self.deferred = i32(2 * cap)     # tail-pass lists: soft-cap deferrals, sequential re-runs
+        self.order = i32(cap)            # bulk-pass schedule (sfg_order)
+        self.order_scratch = i32(int(dc.L.sfg_order_scratch_ints(cap)))
         # triage partials (merged across ranks between the phases, sfg.h):
         # MIN: [stop, fatal, first_hit[E], key_first[K]]; SUM: [edge_delta[E], key_count[K], entered[16]]
         E0, K0 = dc.E, dc.K
@@ -149,6 +152,8 @@ class DeviceCampaign:
         if soft_cap is None:
             soft_cap = int(os.environ.get("SFG_SOFT_CAP", DEFAULT_SOFT_CAP))
         self.soft_cap = soft_cap
+        # bulk pass in signature order (sfg_order): warps of inputs likely to share a path
+        self.order_inputs = os.environ.get("SFG_ORDER", "1") != "0"
         self.manifest = manifest
         self.mem = mem or MemConfig()
         self.mutation = mutation or MutationConfig()
@@ -311,6 +316,10 @@ class DeviceCampaign:
         it0, n = S.it0, S.n
         cd = self.corpus_dev()
         C = self.C
+        if self.timing:
+            S.sub_ev = torch.cuda.Event(enable_timing=True)
+            S.sub_ev.record(st)
+            S.sub_host = time.perf_counter()
         self.launches += 2 + 3 * C
         _native.check(L.sfg_plan(hp, ctypes.byref(cd), it0, n, S.parent.data_ptr(), S.picks.data_ptr(),
                                  S.flags.data_ptr(), s), "plan")
@@ -357,10 +366,16 @@ class DeviceCampaign:
         # no deferral lists -> thread-sequential, no soft cap
         tail = self.jit and cd is not None
         soft = soft_cap if tail else 0
+        order = None
+        if tail and self.order_inputs:
+            self.launches += 3
+            _native.check(self.L.sfg_order(self.h, n, S.vals.data_ptr(), S.order.data_ptr(),
+                                           S.order_scratch.data_ptr(), st.cuda_stream), "order")
+            order = S.order.data_ptr()
         _native.check(self.L.sfg_execute(
             self.h, n, S.children.data_ptr(), S.vals.data_ptr(), S.work_base.data_ptr(), S.work.data_ptr(),
             S.verdicts.data_ptr(), S.ecnt.data_ptr(), _ptr(S.readouts), S.ro_base.data_ptr(), _ptr(S.overlay),
-            S.counter.data_ptr(), soft, S.deferred.data_ptr() if tail else None, self.max_entry_work,
+            S.counter.data_ptr(), soft, S.deferred.data_ptr() if tail else None, self.max_entry_work, order,
             st.cuda_stream), "execute")
         if tail:
             if self.timing:
@@ -568,6 +583,13 @@ class DeviceCampaign:
             return out
 
     # ---- public round API --------------------------------------------------------------
+    def reserve(self, depth: int, round_size: int) -> None:
+        """Allocate the device buffers of ``depth`` rounds of ``round_size`` inputs
+        (and their work arenas for the current corpus) ahead of a pipelined run."""
+        for k in range(depth):
+            S = self._slot(k, round_size)
+            S.ensure_work(round_size * self.max_entry_work + 64, self.dev)
+
     def run_round(self, it0: int, n: int) -> RoundResult:
         """Submit and finalize one round (no pipelining)."""
         S = self._slot(0, n)
@@ -593,6 +615,11 @@ class DeviceCampaign:
         inflight = deque()
         base_round = self.rounds
         nxt = 0
+
+        # every slot this call will use exists before the first submission: allocating
+        # device memory mid-pipeline can stall the device behind in-flight rounds
+        if plan:
+            self.reserve(min(depth, len(plan)), max(n for _, n in plan))
 
         def submit(k):
             it_k, n_k = plan[k]

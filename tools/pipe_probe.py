@@ -26,7 +26,8 @@ host0 = time.perf_counter()
 
 def on_round(res):
     S = res.slot
-    rows.append((S.exec_ev, getattr(S, "bulk_ev", None), S.counter[:8].clone(), time.perf_counter() - host0))
+    rows.append((S.exec_ev, getattr(S, "bulk_ev", None), S.counter[:8].clone(), time.perf_counter() - host0,
+                 S.sub_ev, S.sub_host - host0))
 
 
 it = 1 + 4 * R
@@ -34,15 +35,16 @@ res = dc.run_rounds(it, it + steps * R, R, depth=depth, on_round=on_round)
 torch.cuda.synchronize()
 wall = time.perf_counter() - host0
 out = []
-for (s, e), b, cnt, h in rows:
+for (s, e), b, cnt, h, sub, subh in rows:
     c = cnt.cpu().numpy()
-    out.append((t0.elapsed_time(s), t0.elapsed_time(b) if b else -1, t0.elapsed_time(e), h * 1e3, c[1], c[3]))
+    out.append((t0.elapsed_time(s), t0.elapsed_time(b) if b else -1, t0.elapsed_time(e), h * 1e3, c[1], c[3],
+                t0.elapsed_time(sub), subh * 1e3))
 a = np.array(out)
 print(f"{name} R={R} depth={depth} steps={steps}: wall/step={wall / steps * 1e3:.2f} ms "
       f"execs/s={sum(r.executed for r in res) / wall:,.0f}")
 print(f"  bulk dur ms: mean {np.mean(a[:, 1] - a[:, 0]):.2f} max {np.max(a[:, 1] - a[:, 0]):.2f}; "
       f"tail dur ms: mean {np.mean(a[:, 2] - a[:, 1]):.2f} max {np.max(a[:, 2] - a[:, 1]):.2f}; "
       f"deferred mean {a[:, 4].mean():.0f} seq mean {a[:, 5].mean():.0f}")
-print("round  exec_start  bulk_end  tail_end  host_final  n_def  n_seq")
-for k, r in enumerate(out[:: max(1, len(out) // 24)]):
-    print(f"{k:5d} {r[0]:11.1f} {r[1]:9.1f} {r[2]:9.1f} {r[3]:11.1f} {int(r[4]):6d} {int(r[5]):6d}")
+print("round  host_submit  gpu_submit  exec_start  bulk_end  tail_end  host_final  n_def  n_seq")
+for k, r in enumerate(out):
+    print(f"{k:5d} {r[7]:12.1f} {r[6]:11.1f} {r[0]:11.1f} {r[1]:9.1f} {r[2]:9.1f} {r[3]:11.1f} {int(r[4]):6d} {int(r[5]):6d}")
