@@ -268,7 +268,9 @@ def run_e2e(a, m, torch, R, world):
     dedupe-key counts and new findings / admissions down."""
     from paper_2603_05725_b200.campaign import CampaignConfig, fuzz_loop
     import torch.distributed as dist
-    steps = max(a.steps, 1)
+    # a campaign long enough that pipeline fill/drain (one slowest-round latency,
+    # ~0.15 s on C2) does not dominate: twice the timed steps, at least 48 rounds
+    steps = max(2 * a.steps, 48)
     cfg = CampaignConfig(master_seed=11, iterations=steps * R, round_size=R, pipeline_depth=a.depth,
                          distributed=world > 1)
     torch.cuda.synchronize()
@@ -284,7 +286,7 @@ def run_e2e(a, m, torch, R, world):
     wall = float(t.item())
     tr = s.device_transfer
     return {"value": s.compute_runs / wall, "unit": UNIT, "h2d_bytes_per_step": tr["h2d_bytes"] / steps,
-            "d2h_bytes_per_step": tr["d2h_bytes"] / steps, "wall_s": wall, "execs": s.compute_runs,
+            "d2h_bytes_per_step": tr["d2h_bytes"] / steps, "wall_s": wall, "execs": s.compute_runs, "rounds": steps,
             "api": "campaign.fuzz_loop(manifest, CampaignConfig) -> CampaignSummary",
             "includes": "program build (JIT cache hit), INIT baseline, corpus upload, all rounds, result objects",
             "findings_unique": len(s.findings), "stop": s.stop_reason}

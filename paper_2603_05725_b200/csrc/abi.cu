@@ -20,6 +20,7 @@ struct sfg_program {
   int tail_k = 1;                     // long inputs per tail warp (group-parallel pass)
   int tail_k_seq = 32;                // inputs per warp of the thread-sequential re-run pass
   int tail_ctas = 512;                // one-warp CTAs of the long-input pass
+  int bulk_persist = 1;               // bulk pass: persistent grid (1) or a CTA per batch (0)
   int group = 1;                      // lanes per input of the tail pass (group-parallel launches)
   int bulk_group = 1;                 // lanes per input of the bulk pass (1 = thread-sequential)
   int jit_block = 128;                // CTA size of the persistent kernel
@@ -221,6 +222,7 @@ int sfg_program_create(const void* prog, size_t prog_bytes, const void* ins, siz
       if (cudaDeviceGetLimit(&cur, cudaLimitStackSize) == cudaSuccess && need > cur)
         cudaDeviceSetLimit(cudaLimitStackSize, need);
     }
+    if (const char* bp = getenv("SFG_BULK_PERSIST")) p->bulk_persist = atoi(bp) != 0;
     if (const char* tc = getenv("SFG_TAIL_CTAS")) p->tail_ctas = atoi(tc) >= 1 ? atoi(tc) : 512;
     if (const char* tq = getenv("SFG_TAIL_KSEQ")) p->tail_k_seq = atoi(tq) >= 1 && atoi(tq) <= 32 ? atoi(tq) : 32;
     if (const char* tk = getenv("SFG_TAIL_K")) p->tail_k = atoi(tk) >= 1 && atoi(tk) <= 32 ? atoi(tk) : 1;
@@ -388,7 +390,9 @@ int sfg_execute(const sfg_program* p, int n, const void* children, const void* v
               cudaSuccess && per_sm > 0)
         resident = p->sms * per_sm;
     }
-    const unsigned grid = want < (unsigned)resident ? want : (unsigned)resident;
+    // persistent (one resident wave) or one CTA per batch: the latter frees SM slots
+    // CTA by CTA, so other rounds' long-input warps are not locked out for a whole pass
+    const unsigned grid = (!p->bulk_persist || want < (unsigned)resident) ? want : (unsigned)resident;
     e = cudaLaunchKernel((const void*)p->jit_kernel, dim3(grid), dim3(p->jit_block), args, smem, S(stream));
     if (e != cudaSuccess) return fail("sfg_execute (jit)", e);
     return 0;

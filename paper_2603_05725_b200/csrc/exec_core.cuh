@@ -439,7 +439,8 @@ struct GroupSmem {
   int conflict;
   int seq_rc;      // sequential re-run of a conflicting chunk: LG_* outcome
   unsigned long long seq_retired;
-  int seq_nov, pad;
+  int seq_nov;
+  int waw;         // some word written by several threads of the chunk (and read by none)
   sfg_verdict V;   // the stopping thread's verdict, broadcast to the group
   // uint32_t tags[tag_cap], then uint32_t snapshot[tag_cap] of the work region
 };
@@ -457,9 +458,14 @@ __host__ __device__ inline size_t group_stride(int tag_cap) {
   return (sizeof(GroupSmem) + (size_t)tag_cap * 8 + 15) & ~(size_t)15;
 }
 
-// record an access of [off, off+w) of the work region by lane `me` (1-based);
-// true = conflict (another thread wrote a word we touch, or read a word we write)
-SFG_DEV bool par_track(uint32_t* tags, int ntags, int64_t off, int w, bool st, uint32_t me) {
+// record an access of [off, off+w) of the work region by lane `me` (1-based).
+// Tag: bits 0-7 writer (lane + 1, 0xFF several), bits 8-15 reader (lane + 1, 0xFF
+// several).  true = conflict: a word read by one thread and written by another
+// (either order), or read after several threads wrote it.  A word written by
+// several threads and read by none is not a conflict but sets *waw: only the
+// final memory differs from the sequential run, which matters iff memory is
+// read later (run_launch_group decides).
+SFG_DEV bool par_track(uint32_t* tags, int ntags, int64_t off, int w, bool st, uint32_t me, int* waw) {
   if (off < 0) return true;
   const int64_t w0 = off >> 2, w1 = (off + w - 1) >> 2;
   if (w1 >= ntags) return true;
@@ -467,12 +473,17 @@ SFG_DEV bool par_track(uint32_t* tags, int ntags, int64_t off, int w, bool st, u
     uint32_t old = *reinterpret_cast<volatile uint32_t*>(&tags[x]);
     while (true) {
       const uint32_t wr = old & 0xFFu, rd = (old >> 8) & 0xFFu;
-      if (wr && wr != me) return true;
       uint32_t nw;
       if (st) {
         if (rd && rd != me) return true;
-        nw = (old & ~0xFFu) | me;
+        if (wr && wr != me) {
+          *waw = 1;
+          nw = old | 0xFFu;
+        } else {
+          nw = (old & ~0xFFu) | me;
+        }
       } else {
+        if (wr && wr != me) return true;
         if (rd == me || rd == 0xFFu) break;
         nw = (old & ~0xFF00u) | ((rd ? 0xFFu : me) << 8);
       }
@@ -489,7 +500,7 @@ SFG_DEV bool par_track(uint32_t* tags, int ntags, int64_t off, int w, bool st, u
 template <class Runner>
 SFG_DEV bool par_access(const Runner& R, const LRec& r, int64_t lo, int w, bool st) {
   if (r.flags & R_BASE) return st;  // INIT buffers: reads are shared, writes go through the overlay
-  return par_track(R.tags, R.ntags, r.phys + (lo - r.base), w, st, R.me);
+  return par_track(R.tags, R.ntags, r.phys + (lo - r.base), w, st, R.me, R.waw);
 }
 
 // One input's COMPUTE phase (campaign.py:483-561).  Runner supplies the simulated
@@ -500,7 +511,7 @@ enum { LG_OK = 0, LG_STOP = 1, LG_DEFER = 2, LG_SEQ = 3 };
 template <class Runner>
 SFG_DEV int run_launch_group(const sfg_prog& P, const sfg_hostop& op, Lane& L, Mem& M, sfg_verdict& V,
                              const Pre& pre, Runner& R, const Grp& g, uint64_t& total_retired, int ntags,
-                             int& reruns) {
+                             int& reruns, bool mem_dead) {
   const int T = op.grid * op.block;
   uint32_t* wk = reinterpret_cast<uint32_t*>(M.work);  // 16-aligned, work_bytes a multiple of 16
   uint32_t* snap = g.tags + g.tag_cap;
@@ -513,6 +524,7 @@ SFG_DEV int run_launch_group(const sfg_prog& P, const sfg_hostop& op, Lane& L, M
       g.sm->stop_min = 0x7FFFFFFF;
       g.sm->defer_min = 0x7FFFFFFF;
       g.sm->conflict = 0;
+      g.sm->waw = 0;
     }
     __syncwarp(g.mask);
     R.save_edges();
@@ -531,7 +543,12 @@ SFG_DEV int run_launch_group(const sfg_prog& P, const sfg_hostop& op, Lane& L, M
     __syncwarp(g.mask);
     const int s = *reinterpret_cast<volatile int*>(&g.sm->stop_min);
     const int d = *reinterpret_cast<volatile int*>(&g.sm->defer_min);
-    const int cf = *reinterpret_cast<volatile int*>(&g.sm->conflict);
+    // several writers of a word: harmless if nothing reads memory afterwards -- the
+    // phase stops here (s), or this is the last chunk of the last launch and no
+    // readout is taken (campaign.py:516-517 skips copy_out values without diff_readback)
+    const bool waw = *reinterpret_cast<volatile int*>(&g.sm->waw) != 0;
+    const int cf = *reinterpret_cast<volatile int*>(&g.sm->conflict) ||
+                   (waw && s == 0x7FFFFFFF && !(mem_dead && c0 + g.G >= T));
     __syncwarp(g.mask);
     if (cf) {
       // undo the chunk and re-run it thread-sequentially on the first lane
@@ -731,7 +748,11 @@ SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R, c
     V.launches++;
     if constexpr (GRP) {
       __syncwarp(g.mask);  // host-op stores (made identically by every lane) visible to all
-      const int lg = run_launch_group(P, op, L, M, V, pre, R, g, total_retired, ntags, seq_reruns);
+      // memory is dead after this launch: no later launch and no readout taken
+      bool later_launch = false;
+      for (int h2 = h + 1; h2 < P.n_hostops; ++h2) later_launch |= E.hostops[h2].kind == SFG_H_LAUNCH;
+      const bool mem_dead = !later_launch && ro == nullptr;
+      const int lg = run_launch_group(P, op, L, M, V, pre, R, g, total_retired, ntags, seq_reruns, mem_dead);
       if (lg == LG_STOP) stop = true;
       else if (lg == LG_DEFER) { defer_kind = 1; stop = true; }
       else if (lg == LG_SEQ) { defer_kind = 2; stop = true; }

@@ -172,7 +172,7 @@ struct Gen {
       const char* T = W == 1 ? "uint8_t" : W == 2 ? "uint16_t" : W == 4 ? "uint32_t" : "uint64_t";
       const std::string ptr = std::string("reinterpret_cast<") + (st ? "" : "const ") + T + "*>(pp" + Q + " + (lo_ - pb" + Q + "))";
       const std::string trk = "if (PAR && par_track(J.tags, J.ntags, pw" + Q + " + (lo_ - pb" + Q + "), " + W_s + ", " +
-                              (st ? "true" : "false") + ", J.me)) { " + radj(slow, j) + "rc = RUN_CONFLICT; goto done; } ";
+                              (st ? "true" : "false") + ", J.me, J.waw)) { " + radj(slow, j) + "rc = RUN_CONFLICT; goto done; } ";
       if (st) return trk + "*" + ptr + " = (" + T + ")sv_;";
       return trk + "v_ = *" + ptr + ";";
     };
@@ -434,7 +434,7 @@ struct Gen {
     o << "constexpr uint32_t kPoll = 4096u;\n\n";
     o << "struct JitRunner {\n  uint32_t ec[" << NE << "], ecs[" << NE
       << "];\n  bool ovf, ovfs;\n  uint64_t soft_cap;\n"
-      << "  uint32_t* tags = nullptr;\n  int ntags = 0, t = 0;\n  uint32_t me = 0;\n  GroupSmem* gs = nullptr;\n"
+      << "  uint32_t* tags = nullptr;\n  int ntags = 0, t = 0;\n  uint32_t me = 0;\n  GroupSmem* gs = nullptr;\n  int* waw = nullptr;\n"
       << "  SFG_DEV void begin_input() {\n#pragma unroll\n    for (int e = 0; e < " << NE << "; ++e) ec[e] = 0u;\n    ovf = false;\n"
          "    asm volatile(\"mov.u32 %0, 0;\" : \"=r\"(J_dyn));  // opaque 0: keeps ecs[] out of registers\n  }\n"
       // the chunk-start copy lives in local memory (a dynamically indexed array), so
@@ -443,7 +443,7 @@ struct Gen {
       << "  SFG_DEV void restore_edges() {\n#pragma unroll\n    for (int e = 0; e < " << NE << "; ++e) ec[e] = ecs[e ^ J_dyn];\n    ovf = ovfs;\n  }\n"
       << "  int J_dyn = 0;\n"
       << "  SFG_DEV void par_begin(const Grp& g, int thread, int nt) {\n"
-         "    tags = g.tags; ntags = nt; t = thread; me = (uint32_t)g.gl + 1u; gs = g.sm;\n  }\n"
+         "    tags = g.tags; ntags = nt; t = thread; me = (uint32_t)g.gl + 1u; gs = g.sm; waw = &g.sm->waw;\n  }\n"
       << "  SFG_DEV void par_end() {}\n"
       << "  SFG_DEV bool poll() const {\n"
          "    const int s = *reinterpret_cast<volatile const int*>(&gs->stop_min);\n"

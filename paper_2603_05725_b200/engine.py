@@ -95,6 +95,9 @@ class Slot:
         u8 = lambda m: torch.empty(max(m, 16), dtype=torch.uint8, device=dev)  # noqa: E731
         self.cap = cap
         self.stream = torch.cuda.Stream(device=dev)
+        # the long-input pass runs on a high-priority stream: its CTAs are dispatched
+        # ahead of other rounds' bulk CTAs whenever SM slots free up
+        self.tail_stream = torch.cuda.Stream(device=dev, priority=-1) if dc.tail_priority else self.stream
         self.parent, self.picks, self.flags, self.prefix = i32(cap), u8(cap * 3), i32(cap * C), i64(cap * C)
         self.children, self.vals = u8(cap * CHILD.itemsize), u8(cap * A * VAL.itemsize)
         self.work_base, self.ro_base = i64(cap), i64(cap)
@@ -154,6 +157,7 @@ class DeviceCampaign:
         self.soft_cap = soft_cap
         # bulk pass in signature order (sfg_order): warps of inputs likely to share a path
         self.order_inputs = os.environ.get("SFG_ORDER", "1") != "0"
+        self.tail_priority = os.environ.get("SFG_TAIL_PRIO", "0") != "0"
         self.manifest = manifest
         self.mem = mem or MemConfig()
         self.mutation = mutation or MutationConfig()
@@ -383,11 +387,16 @@ class DeviceCampaign:
                 evb.record(st)
                 S.bulk_ev = evb
             self.launches += 4   # two passes: re-materialize + tail kernel each
+            ts = S.tail_stream
+            if ts is not st:
+                ts.wait_stream(st)
             _native.check(self.L.sfg_execute_deferred(
                 self.h, ctypes.byref(cd), n, S.children.data_ptr(), S.vals.data_ptr(), S.work_base.data_ptr(),
                 S.work.data_ptr(), S.verdicts.data_ptr(), S.ecnt.data_ptr(), _ptr(S.readouts),
                 S.ro_base.data_ptr(), _ptr(S.overlay), S.counter.data_ptr(), S.deferred.data_ptr(),
-                self.max_entry_work, st.cuda_stream), "execute_deferred")
+                self.max_entry_work, ts.cuda_stream), "execute_deferred")
+            if ts is not st:
+                st.wait_stream(ts)
         if self.timing:
             ev[1].record(st)
             S.exec_ev = ev

@@ -1,1 +1,2 @@
-for k in 1 2 3 4; do timeout 300 python bench.py --no-cpu 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('R %d D %d value %.3gM e2e %.3gM k3 %.1f max %.1f bulk %.2f' % (d['config']['round_size'], d['config']['rounds_in_flight'], d['value']/1e6, d['e2e']['value']/1e6, d['issue_roofline']['k3_ms_per_round'], d['issue_roofline']['k3_ms_per_round_max'], d['roofline']['launch_ms']), d['clocks'])"; done
+for k in 1 2 3; do timeout 300 python tools/pipe_probe.py matmul 131072 24 32 2>&1 | head -6; done
+timeout 300 python bench.py --no-cpu | cut -c1-300

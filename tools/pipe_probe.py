@@ -24,8 +24,21 @@ rows = []
 host0 = time.perf_counter()
 
 
+slowest = []
+
+
 def on_round(res):
     S = res.slot
+    from paper_2603_05725_b200.lowering import VERDICT
+    nd = int(S.counter[1].item())
+    if nd:
+        d = S.deferred[:nd].cpu().numpy()
+        v = S.verdicts[:S.n * VERDICT.itemsize].cpu().numpy().view(VERDICT)
+        ns = (v["where"][d] >> 9).astype(np.int64)
+        j = int(np.argmax(ns))
+        i = int(d[j])
+        slowest.append((float(ns[j]) / 1e6, int(v["retired"][i]), int((v["where"][i] >> 8) & 1), int(v["status"][i]),
+                        len(slowest), dc.child_testcases([i], S)[0]))
     rows.append((S.exec_ev, getattr(S, "bulk_ev", None), S.counter[:8].clone(), time.perf_counter() - host0,
                  S.sub_ev, S.sub_host - host0))
 
@@ -45,6 +58,10 @@ print(f"{name} R={R} depth={depth} steps={steps}: wall/step={wall / steps * 1e3:
 print(f"  bulk dur ms: mean {np.mean(a[:, 1] - a[:, 0]):.2f} max {np.max(a[:, 1] - a[:, 0]):.2f}; "
       f"tail dur ms: mean {np.mean(a[:, 2] - a[:, 1]):.2f} max {np.max(a[:, 2] - a[:, 1]):.2f}; "
       f"deferred mean {a[:, 4].mean():.0f} seq mean {a[:, 5].mean():.0f}")
+slowest.sort(key=lambda x: -x[0])
+print("slowest long input per round (ms, retired, rerun, status, round, scalar args):")
+for ms, ret, rr, st, k, tc in slowest[:12]:
+    print(f"  {ms:7.1f} {ret:>10,} {rr} {st} r{k} {[a.value if hasattr(a, 'value') else len(a.data) for a in tc.args]}")
 print("round  host_submit  gpu_submit  exec_start  bulk_end  tail_end  host_final  n_def  n_seq")
 for k, r in enumerate(out):
     print(f"{k:5d} {r[7]:12.1f} {r[6]:11.1f} {r[0]:11.1f} {r[1]:9.1f} {r[2]:9.1f} {r[3]:11.1f} {int(r[4]):6d} {int(r[5]):6d}")
