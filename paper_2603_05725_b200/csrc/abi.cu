@@ -205,7 +205,7 @@ int sfg_program_create(const void* prog, size_t prog_bytes, const void* ins, siz
     p->bulk_group = 1;
     if (const char* bg = getenv("SFG_BULK_GROUP")) {
       const int v = atoi(bg);
-      if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32) p->bulk_group = v;
+      if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32) p->bulk_group = v < p->group ? v : p->group;
     }
     cudaFuncSetAttribute((const void*)p->jit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kExecSmemMax);
     cudaFuncSetAttribute((const void*)p->jit_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, kExecSmemMax);

@@ -239,3 +239,29 @@ def test_struct_corpus_full_size_prefix(engine_cls):
         assert g["edges"] == w["edges"], g["it"]
         assert g["admitted"] == w["admitted"], g["it"]
     dc.close()
+
+
+@pytest.mark.parametrize("name", bench_names())
+def test_group_parallel_bulk_matches_reference(engine_cls, name, monkeypatch):
+    """Every input through the group-parallel mode (simulated threads of a launch on
+    the lanes of a group, conflict tags, in-place sequential re-run of conflicting
+    chunks, WAW acceptance when memory is dead): the bundled harnesses include
+    cross-thread read-modify-writes (amax/amin/asum/nrm2/dot reduce into out[0]),
+    so conflicts, re-runs and WAW all occur.  Records equal the reference's."""
+    monkeypatch.setenv("SFG_BULK_GROUP", "32")  # capped to the program's group size per launch
+    data = golden("ref_batched.json")
+    cfg = data["config"]
+    ref = data["runs"][name]
+    m = bench_manifest(name)
+    dc = engine_cls(m, master_seed=cfg["master_seed"], soft_cap=200)
+    got = []
+    dc.run_rounds(1, cfg["iterations"] + 1, cfg["round_size"], depth=3,
+                  on_round=lambda res: got.extend(dc.round_records(res)))
+    assert len(got) == len(ref["records"])
+    for g, w in zip(got, ref["records"]):
+        assert _digest(g["child"]) == w["child"], g["it"]
+        assert (g["status"], g["report"], g["retired"], g["allocs"], g["edges"], g["admitted"]) == \
+               (w["status"], w["report"], w["retired"], w["allocs"], w["edges"], w["admitted"]), g["it"]
+    assert dc.findings.render_text() == ref["findings"]
+    assert report_to_rec(build_report(dc.coverage_map())) == ref["coverage"]
+    dc.close()
