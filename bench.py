@@ -295,9 +295,9 @@ def run_e2e(a, m, torch, R, world):
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=64)
+    p.add_argument("--steps", type=int, default=48)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--round", type=int, default=131072)
+    p.add_argument("--round", type=int, default=262144)
     p.add_argument("--depth", type=int, default=24, help="rounds in flight (speculative pipelining); at most "
                    "~30 so that every round's stream has its own hardware queue (CUDA_DEVICE_MAX_CONNECTIONS=32)")
     p.add_argument("--workload", default="matmul")
