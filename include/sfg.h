@@ -120,6 +120,12 @@ int sfg_program_group(const sfg_program* p);
  * same path share warps).  Pass it as sfg_execute's `order` (NULL = identity).
  * scratch: sfg_order_scratch_ints(n) ints of device memory. */
 size_t sfg_order_scratch_ints(int n);
+/* Bit a set: harness argument a can steer the simulated kernels' control flow
+ * (taint analysis at program creation); sfg_order hashes only these. */
+uint32_t sfg_program_order_mask(const sfg_program* p);
+/* The same analysis on host tables, no device needed (tests, tooling). */
+uint32_t sfg_control_mask(const void* prog, size_t prog_bytes, const void* ins, const void* hostops,
+                          size_t n_hostops, const void* binds);
 int sfg_order(const sfg_program* p, int n, const void* vals, int32_t* order, int32_t* scratch, void* stream);
 /* Triage in three stream-ordered phases so that a multi-GPU campaign can merge
  * the per-rank partials between them: a rank owns the global

@@ -21,6 +21,7 @@ struct sfg_program {
   int tail_k_seq = 32;                // inputs per warp of the thread-sequential re-run pass
   int tail_ctas = 1024;               // one-warp CTAs of the long-input pass
   int bulk_persist = 1;               // bulk pass: persistent grid (1) or a CTA per batch (0)
+  uint32_t order_mask = ~0u;          // harness args hashed by sfg_order (control_arg_mask)
   int group = 1;                      // lanes per input of the tail pass (group-parallel launches)
   int bulk_group = 1;                 // lanes per input of the bulk pass (1 = thread-sequential)
   int jit_block = 128;                // CTA size of the persistent kernel
@@ -56,6 +57,70 @@ static_assert(sizeof(sfg_prog) < 4096, "sfg_prog must fit the kernel parameter s
 #include "jit.cu"
 
 static thread_local std::string g_err;
+
+// Harness arguments that can steer the simulated kernels' control flow: taint of
+// every kernel parameter propagated (flow-insensitively, to a fixpoint) through
+// moves, arithmetic, conversions and load addresses into setp sources; the
+// launches' bindings map tainted parameters to harness arguments.
+static uint32_t control_arg_mask(const sfg_prog& P, const sfg_ins* ins, const sfg_hostop* H, size_t nh,
+                                 const sfg_binding* B) {
+  uint32_t args = 0;
+  for (size_t h = 0; h < nh; ++h) {
+    if (H[h].kind != SFG_H_LAUNCH) continue;
+    const sfg_kernel& K = P.kernels[H[h].kernel];
+    uint32_t t[4][SFG_MAX_REGS] = {};
+    int nr = 0, nf = 0, na = 0;
+    for (int q = 0; q < K.n_params && q < 32; ++q) {
+      if (K.ptype[q] == 0) t[SFG_CLS_R][nr++] |= 1u << q;
+      else if (K.ptype[q] == 1) t[SFG_CLS_F][nf++] |= 1u << q;
+      else t[SFG_CLS_A][na++] |= 1u << q;
+    }
+    uint32_t ctrl = 0;
+    for (bool changed = true; changed;) {
+      changed = false;
+      auto flow = [&](int cls, int r, uint32_t m) {
+        if (r < SFG_MAX_REGS && (t[cls][r] | m) != t[cls][r]) { t[cls][r] |= m; changed = true; }
+      };
+      for (int i = 0; i < K.n_ins; ++i) {
+        const sfg_ins& x = ins[K.ins_base + i];
+        const bool i1 = x.flags & SFG_F_S1_IMM, i2 = x.flags & SFG_F_S2_IMM;
+        auto src = [&](int cls, int r, bool imm) { return imm || r >= SFG_MAX_REGS ? 0u : t[cls][r]; };
+        switch (x.op) {
+          case SFG_MOV: flow(x.mode, x.dst, src(x.mode, x.s1, i1)); break;
+          case SFG_ADD: case SFG_SUB: case SFG_MUL:
+            if (x.mode == SFG_CLS_A) flow(SFG_CLS_A, x.dst, src(SFG_CLS_A, x.s1, false) | src(SFG_CLS_R, x.s2, i2));
+            else flow(SFG_CLS_R, x.dst, src(SFG_CLS_R, x.s1, i1) | src(SFG_CLS_R, x.s2, i2));
+            break;
+          case SFG_FADD: case SFG_FSUB: case SFG_FMUL:
+            flow(SFG_CLS_F, x.dst, src(SFG_CLS_F, x.s1, i1) | src(SFG_CLS_F, x.s2, i2));
+            break;
+          case SFG_SETP: {
+            const int c = (x.flags & SFG_F_FLOAT) ? SFG_CLS_F : SFG_CLS_R;
+            const uint32_t m = src(c, x.s1, i1) | src(c, x.s2, i2);
+            if ((ctrl | m) != ctrl) { ctrl |= m; changed = true; }
+            flow(SFG_CLS_P, x.dst, m);
+            break;
+          }
+          case SFG_LD: {
+            const int c = x.mode == SFG_MK_F32 ? SFG_CLS_F : x.mode == SFG_MK_B64 ? SFG_CLS_A : SFG_CLS_R;
+            flow(c, x.dst, src(SFG_CLS_A, x.s1, false));
+            break;
+          }
+          case SFG_CVT:
+            if (x.mode == SFG_CVT_F_FROM_I) flow(SFG_CLS_F, x.dst, src(SFG_CLS_R, x.s1, i1));
+            else flow(SFG_CLS_R, x.dst, src(SFG_CLS_F, x.s1, i1));
+            break;
+          default: break;
+        }
+      }
+    }
+    for (int q = 0; q < H[h].n_bind && q < 32; ++q) {
+      const sfg_binding& b = B[H[h].bind_base + q];
+      if (((ctrl >> q) & 1u) && b.form == SFG_B_ARG && b.idx < 32) args |= 1u << b.idx;
+    }
+  }
+  return args;
+}
 
 static int fail(const char* where, cudaError_t e) {
   g_err = std::string(where) + ": " + cudaGetErrorString(e);
@@ -223,6 +288,8 @@ int sfg_program_create(const void* prog, size_t prog_bytes, const void* ins, siz
         cudaDeviceSetLimit(cudaLimitStackSize, need);
     }
     if (const char* bp = getenv("SFG_BULK_PERSIST")) p->bulk_persist = atoi(bp) != 0;
+    p->order_mask = control_arg_mask(p->P, (const sfg_ins*)ins, H, n_hostops, (const sfg_binding*)binds);
+    if (const char* om = getenv("SFG_ORDER_ALL")) if (atoi(om)) p->order_mask = ~0u;
     if (const char* tc = getenv("SFG_TAIL_CTAS")) p->tail_ctas = atoi(tc) >= 1 ? atoi(tc) : 512;
     if (const char* tq = getenv("SFG_TAIL_KSEQ")) p->tail_k_seq = atoi(tq) >= 1 && atoi(tq) <= 32 ? atoi(tq) : 32;
     if (const char* tk = getenv("SFG_TAIL_K")) p->tail_k = atoi(tk) >= 1 && atoi(tk) <= 32 ? atoi(tk) : 1;
@@ -331,6 +398,17 @@ int sfg_regen(const sfg_program* p, const sfg_corpus_dev* c, int n_sel, const in
 
 int sfg_program_group(const sfg_program* p) { return p->jit_kernel ? p->group : 1; }
 
+uint32_t sfg_program_order_mask(const sfg_program* p) { return p->order_mask; }
+
+uint32_t sfg_control_mask(const void* prog, size_t prog_bytes, const void* ins, const void* hostops,
+                          size_t n_hostops, const void* binds) {
+  if (prog_bytes != sizeof(sfg_prog)) return ~0u;
+  sfg_prog P;
+  memcpy(&P, prog, sizeof P);
+  return control_arg_mask(P, (const sfg_ins*)ins, (const sfg_hostop*)hostops, n_hostops,
+                          (const sfg_binding*)binds);
+}
+
 size_t sfg_order_scratch_ints(int n) { return (size_t)kOrderBuckets + (size_t)(n > 0 ? n : 0); }
 
 int sfg_order(const sfg_program* p, int n, const void* vals, int32_t* order, int32_t* scratch, void* stream) {
@@ -339,7 +417,8 @@ int sfg_order(const sfg_program* p, int n, const void* vals, int32_t* order, int
   int* sig = scratch + kOrderBuckets;
   cudaError_t e = cudaMemsetAsync(hist, 0, kOrderBuckets * sizeof(int), S(stream));
   if (e != cudaSuccess) return fail("sfg_order", e);
-  sfg_order_hist_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(p->P, (const sfg_val*)vals, n, hist, sig);
+  sfg_order_hist_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(p->P, (const sfg_val*)vals, n, p->order_mask,
+                                                                  hist, sig);
   sfg_order_scan_kernel<<<1, 128, 0, S(stream)>>>(hist);
   sfg_order_scatter_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(n, sig, hist, order);
   SFG_CHECK_LAUNCH("sfg_order");

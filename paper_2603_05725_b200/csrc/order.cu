@@ -8,6 +8,12 @@
 // inputs by a hash of that signature (counting sort with warp-aggregated
 // atomics) and the bulk pass fetches inputs in bucket order.  Only the
 // schedule changes: every input still writes its own verdict and edge row.
+//
+// The signature covers only the arguments that can steer control flow: a
+// flow-insensitive taint analysis of the simulated kernels (control_arg_mask,
+// abi.cu) marks the parameters reaching a setp, directly or through
+// arithmetic, conversions or load addresses.  Arguments used only as strides
+// or data (matmul's lda/ldb/ldc, array contents) move the stop point at most.
 #include "common.cuh"
 
 namespace {
@@ -19,9 +25,10 @@ SFG_DEV uint64_t sig_mix(uint64_t h, uint64_t v) {
   return h * 0xBF58476D1CE4E5B9ull;
 }
 
-SFG_DEV int sig_bucket(const sfg_prog& P, const sfg_val* v) {
+SFG_DEV int sig_bucket(const sfg_prog& P, const sfg_val* v, uint32_t mask) {
   uint64_t h = 0x243F6A8885A308D3ull;
   for (int a = 0; a < P.n_args; ++a) {
+    if (!((mask >> a) & 1u)) continue;
     h = sig_mix(h, (uint64_t)v[a].kind | ((uint64_t)v[a].space << 8) | ((uint64_t)v[a].elem << 16));
     if (v[a].kind != SFG_V_ARR) {
       h = sig_mix(h, v[a].bits);
@@ -50,10 +57,11 @@ SFG_DEV int warp_agg_add(int* counters, int bucket, bool active) {
 
 }  // namespace
 
-extern "C" __global__ void sfg_order_hist_kernel(sfg_prog P, const sfg_val* vals, int n, int* hist, int* sig) {
+extern "C" __global__ void sfg_order_hist_kernel(sfg_prog P, const sfg_val* vals, int n, uint32_t mask, int* hist,
+                                                 int* sig) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = i < n;
-  const int b = active ? sig_bucket(P, vals + (size_t)i * P.n_args) : 0;
+  const int b = active ? sig_bucket(P, vals + (size_t)i * P.n_args, mask) : 0;
   if (active) sig[i] = b;
   warp_agg_add(hist, b, active);
 }

@@ -165,3 +165,31 @@ def test_sample_valid_testcase_matches_reference_seeds():
     want = golden("ref_workloads.json")["structcfg"]["seeds"]
     for k, text in enumerate(want):
         assert serialize_testcase(sample_valid_testcase(m.argspecs, Stream(11, (7 << 40) + k))) == text
+
+
+def _control_args(m):
+    import ctypes
+    from paper_2603_05725_b200.baseline import MemConfig, build_baseline
+    from paper_2603_05725_b200.engine import MutationConfig
+    from paper_2603_05725_b200.lowering import Lowered
+    base = build_baseline(m, m.seed(11), MemConfig())
+    low = Lowered(m, base, mem=MemConfig(), mutation=MutationConfig(), master_seed=11, budget=10**6, window=256,
+                  recent_weight=4.0)
+    P = low.prog_bytes()
+    L = _native.lib()
+    mask = L.sfg_control_mask(P, len(P), low.ins.ctypes.data, low.hostops.ctypes.data, len(low.hostops),
+                              low.binds.ctypes.data)
+    return {s.name for a, s in enumerate(m.argspecs) if mask >> a & 1}
+
+
+def test_control_taint_mask():
+    """sfg_order's signature covers the arguments that reach a setp (loop bounds,
+    compared values), not strides or stored data (csrc/abi.cu control_arg_mask)."""
+    from paper_2603_05725_b200.workloads import load
+    assert _control_args(load("matmul")) == {"m", "n", "k"}
+    assert _control_args(load("vadd")) == {"n"}
+    # amax compares loaded elements: the array steers control through its contents
+    amax = _control_args(bench_manifest("amax"))
+    assert "n" in amax and "x" in amax
+    # copy only bounds its loop by n
+    assert _control_args(bench_manifest("copy")) == {"n"}
