@@ -113,6 +113,15 @@ int sfg_execute_deferred(const sfg_program* p, const sfg_corpus_dev* c, int n, c
                          uint32_t* edge_counts, uint8_t* readouts, const uint64_t* readout_base,
                          uint64_t* overlay, int* work_counter, int32_t* deferred, int64_t max_work_bytes,
                          void* stream);
+/* Trace mode (replaces the reference's ExecHooks / TraceHooks per event,
+ * executor.py:108-135, cli.py:42-45): run the inputs through the generic
+ * interpreter and record every on_mem_access / on_control_flow event of input i
+ * into trace[i * trace_cap * 4 ...] (4 uint64 words per event; layout in
+ * csrc/execute.cu); trace_count[i] = events produced (> trace_cap: truncated). */
+int sfg_execute_trace(const sfg_program* p, int n, const void* children, const void* vals,
+                      const uint64_t* work_base, uint8_t* work, void* verdicts, uint32_t* edge_counts,
+                      uint8_t* readouts, const uint64_t* readout_base, uint64_t* overlay, uint64_t* trace,
+                      uint32_t trace_cap, uint32_t* trace_count, void* stream);
 /* Lanes per input of the program's group-parallel mode (1 = thread-sequential). */
 int sfg_program_group(const sfg_program* p);
 /* Bulk-pass schedule: order[0..n) = a permutation of the round's inputs grouped by

@@ -24,6 +24,7 @@ from .baseline import MemConfig
 from .coverage import build_report, render_text, report_to_rec
 from .engine import DeviceCampaign, MutationConfig
 from .findings import BugClass, FindingsLog
+from .hooks import ExecHooks, TraceHooks, dispatch  # noqa: F401  (re-export)
 from .lowering import LoweringError
 from .manifest import HarnessManifest, load_harness  # noqa: F401  (re-export)
 from .testcase import argspec_digest, serialize_testcase
@@ -130,8 +131,7 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
         raise CampaignFatalError(f"unknown mode {config.mode!r}")
     if config.workers < 1 or config.iterations < 1:
         raise CampaignFatalError("workers and iterations must be >= 1")
-    if config.hooks is not None:
-        raise LoweringError("per-event Python hooks are not supported on the device path")
+    hooks = config.hooks
     for op in manifest.phases["term"]:
         if op.kind not in ("free", "sync"):
             raise LoweringError("TERM phases other than frees are not lowered")
@@ -145,6 +145,8 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
     t0 = time.perf_counter()
     deadline = t0 + config.max_wall_seconds if config.max_wall_seconds else None
     comm = None
+    if config.distributed and hooks is not None:
+        raise LoweringError("hooks are per-process; trace a campaign on one device")
     if config.distributed:
         from .shard import RoundComm
         comm = RoundComm()
@@ -182,6 +184,13 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
                         tcs = dc.child_testcases([i for i, _ in res.new_keys], res.slot)
                         for (i, rep), tc in zip(res.new_keys, tcs):
                             _write_crash(out_dir, rep, tc, specs, manifest)
+                if hooks is not None and res.executed:
+                    # the round's inputs once more through the device trace mode, events
+                    # replayed to the hooks in iteration order (hooks.py)
+                    k = min(res.executed, res.slot.n)
+                    tcs = dc.child_testcases(list(range(k)), res.slot)
+                    for out in dc.execute_testcases(tcs, iteration0=res.slot.it0, trace=True):
+                        dispatch(hooks, out["events"])
                 if res.stop is not None:
                     want = config.stop_bug_class
                     state["stop"] = ("first_finding" if config.stop_on_first_finding else
@@ -200,7 +209,8 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
                     clock["expired"] = late
                 return not clock["expired"]
 
-            dc.run_rounds(rng_.start, rng_.stop, config.round_size, depth=config.pipeline_depth,
+            dc.run_rounds(rng_.start, rng_.stop, config.round_size,
+                          depth=1 if hooks is not None else config.pipeline_depth,
                           on_round=on_round, should_continue=should_continue)
             if clock["expired"] and state["stop"] is None:
                 stop_reason = "wall_clock"

@@ -438,7 +438,8 @@ int sfg_execute(const sfg_program* p, int n, const void* children, const void* v
              (const sfg_child*)children, (const sfg_val*)vals, work_base, work,
              (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, overlay, n,
              0ull, deferred, work_counter ? work_counter + 1 : nullptr,
-             deferred ? deferred + n : nullptr, work_counter ? work_counter + 3 : nullptr, 1, 0, order};
+             deferred ? deferred + n : nullptr, work_counter ? work_counter + 3 : nullptr, 1, 0, order,
+             nullptr, 0, nullptr};
   if (p->jit_kernel) {
     if (work_counter == nullptr || (deferred == nullptr && soft_cap != 0)) {
       g_err = "sfg_execute: the specialized kernel needs a per-launch work counter (and deferred lists for soft_cap)";
@@ -482,6 +483,20 @@ int sfg_execute(const sfg_program* p, int n, const void* children, const void* v
   return 0;
 }
 
+int sfg_execute_trace(const sfg_program* p, int n, const void* children, const void* vals, const uint64_t* work_base,
+                      uint8_t* work, void* verdicts, uint32_t* edge_counts, uint8_t* readouts,
+                      const uint64_t* readout_base, uint64_t* overlay, uint64_t* trace, uint32_t trace_cap,
+                      uint32_t* trace_count, void* stream) {
+  if (n <= 0) return 0;
+  ExecView E{p->ins, p->hostops, p->binds, p->recs, p->base_blob, p->const_blob,
+             (const sfg_child*)children, (const sfg_val*)vals, work_base, work,
+             (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, overlay, n,
+             0ull, nullptr, nullptr, nullptr, nullptr, 1, 0, nullptr, trace, trace_cap, trace_count};
+  sfg_execute_kernel<<<blocks_for(n, 128), 128, p->smem, S(stream)>>>(p->P, E);
+  SFG_CHECK_LAUNCH("sfg_execute_trace");
+  return 0;
+}
+
 int sfg_execute_deferred(const sfg_program* p, const sfg_corpus_dev* c, int n, const void* children,
                          const void* vals, const uint64_t* work_base, uint8_t* work, void* verdicts,
                          uint32_t* edge_counts, uint8_t* readouts, const uint64_t* readout_base, uint64_t* overlay,
@@ -490,7 +505,8 @@ int sfg_execute_deferred(const sfg_program* p, const sfg_corpus_dev* c, int n, c
   ExecView E{p->ins, p->hostops, p->binds, p->recs, p->base_blob, p->const_blob,
              (const sfg_child*)children, (const sfg_val*)vals, work_base, work,
              (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, overlay, n,
-             0ull, deferred, work_counter + 1, deferred + n, work_counter + 3, p->group, 0, nullptr};
+             0ull, deferred, work_counter + 1, deferred + n, work_counter + 3, p->group, 0, nullptr,
+             nullptr, 0, nullptr};
   for (int pass = 0; pass < 2; ++pass) {
     // pristine payloads again (the earlier attempt's stores landed in the work regions)
     int32_t* list = pass == 0 ? deferred : deferred + n;

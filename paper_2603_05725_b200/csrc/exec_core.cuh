@@ -92,6 +92,12 @@ struct ExecView {
   int tag_cap;
   // bulk-pass schedule: the j-th fetched input is order[j] (sfg_order), null = j
   const int32_t* order;
+  // trace mode (generic interpreter only, sfg_execute_trace): ExecHooks events
+  // (executor.py:122-135) of input i into trace[i * trace_cap ...], 4 words each;
+  // trace_count[i] = events produced (may exceed trace_cap: truncated)
+  uint64_t* trace;
+  uint32_t trace_cap;
+  uint32_t* trace_count;
 };
 
 namespace {
@@ -640,6 +646,7 @@ SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R, c
   for (int k = 0; k < P.n_args; ++k) L.mat_rec[k] = -1;
   L.ro_cursor = 0;
   R.begin_input();
+  R.set_input(E, i);
   uint64_t total_retired = 0;
   uint8_t* ro = (P.diff_readback && E.readouts) ? E.readouts + E.readout_base[i] : nullptr;
   const uint64_t arrays_end = ch.work_bytes - (uint64_t)P.named_work_bytes;
@@ -775,6 +782,7 @@ SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R, c
     }
     return;
   }
+  R.end_input(E, i);
   V.retired = total_retired;
   V.allocs = L.nalloc;
   uint32_t* erow = E.edge_counts + (size_t)i * P.n_edges;

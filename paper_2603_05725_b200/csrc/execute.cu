@@ -21,9 +21,36 @@ struct InterpRunner {
     for (int e = 0; e < n_edges; ++e) s_ecnt[e * 32 + lane] = 0;
   }
 
+  // trace mode: event words of the current input (executor.py:122-135)
+  //   w0: kind (0 mem, 1 cf) | store << 2 | width << 3 | space << 8 | kernel << 16 | iid or edge << 32
+  //   w1: ctaid | tid << 32;  w2, w3: address low / high (mem)
+  uint64_t* tr = nullptr;
+  uint32_t tr_cap = 0, tr_n = 0;
+  int cur_kernel = 0, cur_ctaid = 0, cur_tid = 0;
+
+  SFG_DEV void set_input(const ExecView& E, int i) {
+    tr = E.trace ? E.trace + (size_t)i * E.trace_cap * 4 : nullptr;
+    tr_cap = E.trace_cap;
+    tr_n = 0;
+  }
+  SFG_DEV void end_input(const ExecView& E, int i) {
+    if (tr) E.trace_count[i] = tr_n;
+  }
+  SFG_DEV void ev(uint64_t w0, uint64_t w2, uint64_t w3) {
+    if (tr_n < tr_cap) {
+      uint64_t* p = tr + (size_t)tr_n * 4;
+      p[0] = w0;
+      p[1] = (uint64_t)(uint32_t)cur_ctaid | ((uint64_t)(uint32_t)cur_tid << 32);
+      p[2] = w2;
+      p[3] = w3;
+    }
+    ++tr_n;
+  }
+
   SFG_DEV void hit(int e) {
     uint32_t* p = s_ecnt + e * 32 + lane;
     if (*p == 0xFFFFFFFFu) overflow = true; else ++*p;
+    if (tr) ev(1ull | ((uint64_t)(uint32_t)cur_kernel << 16) | ((uint64_t)(uint32_t)e << 32), 0, 0);
   }
 
   SFG_DEV void flush(uint32_t* erow, bool& ovf) {
@@ -47,6 +74,9 @@ struct InterpRunner {
     uint32_t preds = 0;
     int pc = 0;
     uint64_t retired = 0;
+    cur_kernel = kidx;
+    cur_ctaid = ctaid;
+    cur_tid = tid;
     int rc = RUN_EXIT;
     while (true) {
       const sfg_ins I = kins[pc];
@@ -67,6 +97,10 @@ struct InterpRunner {
           const i128 a = areg + (i128)I.imm2;
           const int prov = s_ap[I.s1 * 32 + lane];
           const bool st = I.op == SFG_ST;
+          if (tr)  // on_mem_access precedes the sanitizer check (executor.py:244-247)
+            ev((uint64_t)(st ? 4 : 0) | ((uint64_t)I.width << 3) | ((uint64_t)I.space << 8) |
+                   ((uint64_t)(uint32_t)kidx << 16) | ((uint64_t)(uint32_t)pc << 32),
+               (uint64_t)a, (uint64_t)(a >> 64));
           Report rep;
           int rh = -1;
           if (check_access(P, L, a, I.width, I.space, prov, rep, rh)) {
@@ -233,5 +267,6 @@ extern "C" __global__ void __launch_bounds__(128) sfg_execute_kernel(sfg_prog P,
   for (int base_i = gw * 32; base_i < E.n; base_i += nw * 32) {
     const int i = base_i + lane;
     if (i < E.n) run_input<false>(P, E, i, R, Grp{1, 0, 1u << lane, nullptr, nullptr, 0});
+    __syncwarp();
   }
 }

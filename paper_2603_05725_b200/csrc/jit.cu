@@ -445,6 +445,7 @@ struct Gen {
       << "  SFG_DEV void par_begin(const Grp& g, int thread, int nt) {\n"
          "    tags = g.tags; ntags = nt; t = thread; me = (uint32_t)g.gl + 1u; gs = g.sm; waw = &g.sm->waw;\n  }\n"
       << "  SFG_DEV void par_end() {}\n"
+      << "  SFG_DEV void set_input(const ExecView&, int) {}\n  SFG_DEV void end_input(const ExecView&, int) {}\n"
       << "  SFG_DEV bool poll() const {\n"
          "    const int s = *reinterpret_cast<volatile const int*>(&gs->stop_min);\n"
          "    const int d = *reinterpret_cast<volatile const int*>(&gs->defer_min);\n"

@@ -33,6 +33,7 @@ from . import _native
 from .baseline import MemConfig, OutOfSpaceError, build_baseline, record_table
 from .coverage import CoverageMap
 from .findings import FindingsLog
+from .sir import SPACE_ORDER
 from .lowering import (CHILD, ENTRY, ST_COUNTER, MAX_KERNELS, ctx_edge_hashes, ST_FINDING, ST_LANE_RECS, ST_OUT_OF_SPACE, ST_OVERLAY,
                        ST_ZERO_ALLOC, VAL, VERDICT, Lowered, LoweringError, decode_op, decode_verdict,
                        pack_values, unpack_values)
@@ -789,10 +790,14 @@ class DeviceCampaign:
         return out
 
     # ---- one-shot execution of given test cases (execute_once analogue) -------------------
-    def execute_testcases(self, tcs, iteration0: int = 0):
-        """Run COMPUTE for explicit inputs (no mutation); returns per-input dicts."""
+    def execute_testcases(self, tcs, iteration0: int = 0, trace: bool = False, trace_cap: int = 1 << 16):
+        """Run COMPUTE for explicit inputs (no mutation); returns per-input dicts.
+        trace: also return each input's ExecHooks event stream ("events": tuples
+        ("mem", kernel, iid, ctaid, tid, space, addr, width, is_store) /
+        ("cf", kernel, ctaid, tid, src_block, dst_block), executor.py:108-135),
+        recorded on the device by the generic interpreter (sfg_execute_trace)."""
         n = len(tcs)
-        S = self._slot(0, n)
+        S = self._aux_slot(n)
         self.drain()
         vals_all = np.zeros(n * self.n_args, VAL)
         chld = np.zeros(n, CHILD)
@@ -833,7 +838,23 @@ class DeviceCampaign:
         S.readouts = self._u8(ro_total + 16) if self.diff else None
         S.n = n
         torch.cuda.synchronize(self.dev)
-        self._execute(S, n)
+        events = None
+        if trace:
+            tbuf = torch.empty(max(n * trace_cap * 4, 1), dtype=torch.int64, device=self.dev)
+            tcnt = torch.zeros(max(n, 1), dtype=torch.int32, device=self.dev)
+            self.launches += 1
+            _native.check(self.L.sfg_execute_trace(
+                self.h, n, S.children.data_ptr(), S.vals.data_ptr(), S.work_base.data_ptr(), S.work.data_ptr(),
+                S.verdicts.data_ptr(), S.ecnt.data_ptr(), _ptr(S.readouts), S.ro_base.data_ptr(), _ptr(S.overlay),
+                tbuf.data_ptr(), trace_cap, tcnt.data_ptr(), S.stream.cuda_stream), "execute_trace")
+            self.drain()
+            cnt = tcnt.cpu().numpy()
+            if int(cnt.max(initial=0)) > trace_cap:
+                raise DeviceFatal(f"trace buffer overflow ({int(cnt.max())} events > trace_cap {trace_cap})")
+            words = tbuf.cpu().numpy().view(np.uint64).reshape(max(n, 1), trace_cap, 4) if n else None
+            events = [self._decode_events(words[i, :int(cnt[i])]) for i in range(n)]
+        else:
+            self._execute(S, n)
         self.drain()
         verd = _np(S.verdicts[:n * VERDICT.itemsize], VERDICT)
         E1 = max(self.E, 1)
@@ -863,6 +884,32 @@ class DeviceCampaign:
             out.append({"status": STATUS.get(st, f"fatal{st}"), "report": rep, "retired": int(v["retired"]),
                         "allocs": int(v["allocs"]), "edges": self._edges_row(ecnt[i]), "readouts": readouts,
                         "entered": int(v["entered"])})
+            if events is not None:
+                out[-1]["events"] = events[i]
+        return out
+
+    def _aux_slot(self, n: int) -> Slot:
+        """A slot outside the pipelined rounds' ring (explicit executions, tracing)."""
+        if getattr(self, "_aux", None) is None or self._aux.cap < n:
+            self._aux = Slot(self, max(n, 1024))
+        return self._aux
+
+    def _decode_events(self, w: np.ndarray):
+        """Device trace words -> ExecHooks argument tuples (csrc/execute.cu layout)."""
+        out = []
+        spaces = [s.value for s in SPACE_ORDER]
+        for w0, w1, w2, w3 in w.tolist():
+            kind, kernel, x = w0 & 3, self.low.kernel_names[(w0 >> 16) & 0xFFFF], w0 >> 32
+            ctaid, tid = w1 & 0xFFFFFFFF, w1 >> 32
+            if kind == 1:
+                name, (src, dst) = self.low.edge_names[x]
+                out.append(("cf", kernel, ctaid, tid, src, dst))
+            else:
+                addr = (w3 << 64) | w2
+                if addr >= 1 << 127:
+                    addr -= 1 << 128
+                out.append(("mem", kernel, x, ctaid, tid, spaces[(w0 >> 8) & 0xFF], addr, (w0 >> 3) & 0x1F,
+                            bool(w0 & 4)))
         return out
 
     def close(self):

@@ -17,6 +17,9 @@ Writes (all small, committed):
                       summary, corpus) for a few configs
   ref_workloads.json  the same batched records for this repo's synthetic
                       workloads (paper_2603_05725_b200/workloads)
+  ref_traces.json     ExecHooks event streams (TraceHooks "EV mem" / "EV cf"
+                      lines): per sampled input of every benchmark, and for a
+                      traced batched campaign (dot, amax)
 """
 
 from __future__ import annotations
@@ -126,7 +129,7 @@ def sampled():
 
 
 def batched(m, *, master_seed, iterations, round_size, stop_bug_class=None,
-            stop_on_first_finding=False, extra_seeds=(), fanout=0):
+            stop_on_first_finding=False, extra_seeds=(), fanout=0, hooks=None):
     """Batched-round contract on the reference's own functions.  fanout > 0: input
     it mutates round-corpus entry ((it - 1) // fanout) % len (no scheduling draw)."""
     specs = m.argspecs
@@ -139,7 +142,7 @@ def batched(m, *, master_seed, iterations, round_size, stop_bug_class=None,
     gcov = CoverageMap.for_program(m.program)
     sched = MutationSchedule()
     image = DeviceMemoryImage(rng=Stream(master_seed, 2000))
-    runner = rc.PhaseRunner(m, image)
+    runner = rc.PhaseRunner(m, image, hooks=hooks)
     assert runner.run_phase(rc.INIT, seed_tc, iteration=0).status == "ok"
     runner.mark_baseline()
     snap = image.snapshot()
@@ -242,13 +245,51 @@ def workloads():
     return out
 
 
+TRACE_INPUTS = (0, 1, 2, 12)
+TRACE_CAMPAIGN = dict(master_seed=11, iterations=48, round_size=16)
+
+
+def _trace_summary(text: str, head: int = 24) -> dict:
+    lines = text.splitlines()
+    return {"n_lines": len(lines), "sha256": hashlib.sha256(text.encode()).hexdigest(), "head": lines[:head]}
+
+
+def traces():
+    """Event streams of the reference's TraceHooks (executor.py:122-135)."""
+    import io
+    from simt_forge.executor import TraceHooks
+    from simt_forge.mutation import parse_testcase
+    samp = json.loads((HERE / "ref_sampled.json").read_text())
+    out = {"inputs": {}, "campaigns": {}, "campaign_config": TRACE_CAMPAIGN}
+    for b in rb.list_benchmarks():
+        m = b.load()
+        recs = []
+        for i in TRACE_INPUTS:
+            tc, _ = parse_testcase(samp[b.name][i]["testcase"], m.argspecs)
+            buf = io.StringIO()
+            image = DeviceMemoryImage()
+            runner = rc.PhaseRunner(m, image, hooks=TraceHooks(buf))
+            runner.run_phase(rc.INIT, m.seed(1), iteration=0)
+            buf.seek(0)
+            buf.truncate()
+            runner.run_phase(rc.COMPUTE, tc, iteration=i + 1)
+            recs.append({"testcase": samp[b.name][i]["testcase"], **_trace_summary(buf.getvalue())})
+        out["inputs"][b.name] = recs
+    for name in ("dot", "amax"):
+        m = next(b for b in rb.list_benchmarks() if b.name == name).load()
+        buf = io.StringIO()
+        batched(m, hooks=TraceHooks(buf), **TRACE_CAMPAIGN)
+        out["campaigns"][name] = _trace_summary(buf.getvalue())
+    return out
+
+
 def _dump(obj) -> str:
     return json.dumps(obj, sort_keys=True, separators=(",", ":"))
 
 
 def main():
     import tempfile
-    which = sys.argv[1:] or ["assets", "variants", "sampled", "batched", "fuzzloop", "workloads"]
+    which = sys.argv[1:] or ["assets", "variants", "sampled", "batched", "fuzzloop", "workloads", "traces"]
     if "assets" in which:
         (HERE / "bench_assets.json").write_text(_dump(assets()))
     if "variants" in which:
@@ -263,6 +304,8 @@ def main():
             (HERE / "ref_fuzzloop.json").write_text(_dump(fuzzloops(tmp)))
     if "workloads" in which:
         (HERE / "ref_workloads.json").write_text(_dump(workloads()))
+    if "traces" in which:
+        (HERE / "ref_traces.json").write_text(_dump(traces()))
 
 
 if __name__ == "__main__":

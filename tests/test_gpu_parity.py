@@ -277,3 +277,45 @@ def test_order_mask_is_control_taint(engine_cls):
     mask = dc.L.sfg_program_order_mask(dc.h)
     assert {names[a] for a in range(len(names)) if mask >> a & 1} == {"m", "n", "k"}
     dc.close()
+
+
+def _trace_text(events):
+    import io
+    from paper_2603_05725_b200.hooks import TraceHooks, dispatch
+    buf = io.StringIO()
+    dispatch(TraceHooks(buf), events)
+    return buf.getvalue()
+
+
+@pytest.mark.parametrize("name", bench_names())
+def test_trace_events_match_reference(engine_cls, name):
+    """Device trace mode (sfg_execute_trace) reproduces the reference's TraceHooks
+    stream (executor.py:122-135) line for line on sampled inputs."""
+    ref = golden("ref_traces.json")["inputs"][name]
+    m = bench_manifest(name)
+    dc = engine_cls(m, master_seed=1)
+    tcs = [parse_testcase(r["testcase"])[0] for r in ref]
+    outs = dc.execute_testcases(tcs, iteration0=1, trace=True)
+    for out, r in zip(outs, ref):
+        text = _trace_text(out["events"])
+        assert text.splitlines()[:len(r["head"])] == r["head"]
+        assert len(text.splitlines()) == r["n_lines"]
+        assert hashlib.sha256(text.encode()).hexdigest() == r["sha256"]
+    dc.close()
+
+
+@pytest.mark.parametrize("name", ["dot", "amax"])
+def test_traced_campaign_matches_reference(engine_cls, name):
+    """fuzz_loop(hooks=TraceHooks) over the batched-round contract: the whole event
+    stream of the campaign equals the reference functions' (make_golden traces)."""
+    import io
+    from paper_2603_05725_b200.campaign import CampaignConfig, TraceHooks, fuzz_loop
+    data = golden("ref_traces.json")
+    cfg, ref = data["campaign_config"], data["campaigns"][name]
+    buf = io.StringIO()
+    fuzz_loop(bench_manifest(name), CampaignConfig(master_seed=cfg["master_seed"], iterations=cfg["iterations"],
+                                                   round_size=cfg["round_size"], hooks=TraceHooks(buf)))
+    text = buf.getvalue()
+    assert len(text.splitlines()) == ref["n_lines"]
+    assert text.splitlines()[:len(ref["head"])] == ref["head"]
+    assert hashlib.sha256(text.encode()).hexdigest() == ref["sha256"]
