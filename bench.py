@@ -235,6 +235,10 @@ def run_ours(a):
     # campaign's buffers go back to the allocator first)
     dc.close()
     dc.slots.clear()
+    dc._aux = None
+    del results                 # round results hold their slots: free them all
+    import gc
+    gc.collect()
     e2e = run_e2e(a, m, torch, R, world)
 
     if rank == 0:

@@ -122,6 +122,11 @@ int sfg_execute_trace(const sfg_program* p, int n, const void* children, const v
                       const uint64_t* work_base, uint8_t* work, void* verdicts, uint32_t* edge_counts,
                       uint8_t* readouts, const uint64_t* readout_base, uint64_t* overlay, uint64_t* trace,
                       uint32_t trace_cap, uint32_t* trace_count, void* stream);
+/* A non-blocking CUDA stream (cudaStreamCreateWithPriority).  The Python host keeps
+ * one process-wide ring of them, created back to back, so that each round in
+ * flight owns a hardware work queue (CUDA_DEVICE_MAX_CONNECTIONS) for the life of
+ * the process instead of drawing from torch's shared stream pool. */
+int sfg_stream_create(int priority, void** out);
 /* Lanes per input of the program's group-parallel mode (1 = thread-sequential). */
 int sfg_program_group(const sfg_program* p);
 /* Bulk-pass schedule: order[0..n) = a permutation of the round's inputs grouped by

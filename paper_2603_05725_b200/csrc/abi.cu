@@ -396,6 +396,14 @@ int sfg_regen(const sfg_program* p, const sfg_corpus_dev* c, int n_sel, const in
   return 0;
 }
 
+int sfg_stream_create(int priority, void** out) {
+  cudaStream_t s = nullptr;
+  const cudaError_t e = cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, priority);
+  if (e != cudaSuccess) return fail("sfg_stream_create", e);
+  *out = (void*)s;
+  return 0;
+}
+
 int sfg_program_group(const sfg_program* p) { return p->jit_kernel ? p->group : 1; }
 
 uint32_t sfg_program_order_mask(const sfg_program* p) { return p->order_mask; }

@@ -85,17 +85,35 @@ class RoundResult:
         self.slot = slot
 
 
+_STREAMS: dict = {}
+
+
+def _round_stream(L, dev, index: int):
+    """Process-wide stream of round slot ``index`` (created on first use, reused by
+    every campaign of the process): rounds in flight keep distinct hardware queues.
+    index < 0: a private torch stream (auxiliary slots)."""
+    if index < 0:
+        return torch.cuda.Stream(device=dev)
+    key = (dev.index if dev.index is not None else torch.cuda.current_device(), index)
+    if key not in _STREAMS:
+        with torch.cuda.device(key[0]):
+            h = ctypes.c_void_p()
+            _native.check(L.sfg_stream_create(0, ctypes.byref(h)), "stream")
+            _STREAMS[key] = torch.cuda.ExternalStream(h.value, device=torch.device("cuda", key[0]))
+    return _STREAMS[key]
+
+
 class Slot:
     """Device buffers + stream of one in-flight round."""
 
-    def __init__(self, dc: "DeviceCampaign", cap: int):
+    def __init__(self, dc: "DeviceCampaign", cap: int, index: int = -1):
         dev = dc.dev
         C, E, A = max(dc.C, 1), max(dc.E, 1), dc.n_args
         i64 = lambda m: torch.empty(max(m, 1), dtype=torch.int64, device=dev)  # noqa: E731
         i32 = lambda m: torch.empty(max(m, 1), dtype=torch.int32, device=dev)  # noqa: E731
         u8 = lambda m: torch.empty(max(m, 16), dtype=torch.uint8, device=dev)  # noqa: E731
         self.cap = cap
-        self.stream = torch.cuda.Stream(device=dev)
+        self.stream = _round_stream(dc.L, dev, index)
         # the long-input pass runs on a high-priority stream: its CTAs are dispatched
         # ahead of other rounds' bulk CTAs whenever SM slots free up
         self.tail_stream = torch.cuda.Stream(device=dev, priority=-1) if dc.tail_priority else self.stream
@@ -287,7 +305,7 @@ class DeviceCampaign:
             self.slots.append(None)
         s = self.slots[k]
         if s is None or s.cap < n:
-            s = Slot(self, max(n, 1024))
+            s = Slot(self, max(n, 1024), k)
             self.slots[k] = s
         return s
 
