@@ -178,11 +178,14 @@ def run_ours(a):
         dist.barrier()
     launches0 = dc.launches
     dc.exec_events.clear()
+    fin = []                    # host clock at each round's finalization (diagnostics)
     with ClockSampler(local) as clk:
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
+        h0 = time.perf_counter()
         t0.record()
-        results = dc.run_rounds(it, it + a.steps * R, R, depth=D)
+        results = dc.run_rounds(it, it + a.steps * R, R, depth=D,
+                                on_round=lambda res: fin.append((time.perf_counter() - h0, res.n_admitted)))
         all_streams_done(t1)
         torch.cuda.synchronize()
     it += a.steps * R
@@ -233,6 +236,11 @@ def run_ours(a):
 
     # ---- end to end through the public API with host buffers (the device-timed
     # campaign's buffers go back to the allocator first)
+    if os.environ.get("SFG_BENCH_TIMELINE"):
+        with open(os.environ["SFG_BENCH_TIMELINE"], "w") as f:
+            for k, ((s_, b_, e_), (h, adm)) in enumerate(zip(dc.exec_events, fin)):
+                f.write(f"{k} exec_start {t0.elapsed_time(s_):.1f} bulk_end {t0.elapsed_time(b_):.1f} "
+                        f"tail_end {t0.elapsed_time(e_):.1f} host_final {h * 1e3:.1f} admitted {adm}\n")
     dc.close()
     dc.slots.clear()
     dc._aux = None
@@ -299,7 +307,7 @@ def run_e2e(a, m, torch, R, world):
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=48)
+    p.add_argument("--steps", type=int, default=96)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--round", type=int, default=262144)
     p.add_argument("--depth", type=int, default=24, help="rounds in flight (speculative pipelining); at most "
