@@ -171,8 +171,12 @@ struct Gen {
       const std::string Q = std::to_string(q);
       const char* T = W == 1 ? "uint8_t" : W == 2 ? "uint16_t" : W == 4 ? "uint32_t" : "uint64_t";
       const std::string ptr = std::string("reinterpret_cast<") + (st ? "" : "const ") + T + "*>(pp" + Q + " + (lo_ - pb" + Q + "))";
-      const std::string trk = "if (PAR && par_track(J.tags, J.ntags, pw" + Q + " + (lo_ - pb" + Q + "), " + W_s + ", " +
-                              (st ? "true" : "false") + ", J.me, J.waw)) { " + radj(slow, j) + "rc = RUN_CONFLICT; goto done; } ";
+      // loads from a record no store of this kernel can reach need no tag (no thread
+      // of the launch writes it: nothing to conflict with)
+      const bool ro = !st && !any_untagged_store && !written[q];
+      const std::string trk = ro ? std::string() :
+          "if (PAR && par_track(J.tags, J.ntags, pw" + Q + " + (lo_ - pb" + Q + "), " + W_s + ", " +
+          (st ? "true" : "false") + ", J.me, J.waw)) { " + radj(slow, j) + "rc = RUN_CONFLICT; goto done; } ";
       if (st) return trk + "*" + ptr + " = (" + T + ")sv_;";
       return trk + "v_ = *" + ptr + ";";
     };
@@ -209,6 +213,11 @@ struct Gen {
   }
 
   int cur_na = 0;
+  // stores of the kernel being emitted: written[q] = some store's base carries the
+  // tag of pointer parameter q; any_untagged_store = some store's base has no
+  // static tag (could reach any record)
+  std::vector<char> written;
+  bool any_untagged_store = false;
 
   std::string src_r(const sfg_ins& x, int slot) {
     const bool imm = slot == 1 ? (x.flags & SFG_F_S1_IMM) : (x.flags & SFG_F_S2_IMM);
@@ -309,6 +318,14 @@ struct Gen {
     std::vector<int> blk_of;
     const auto tags = tag_flow(I, K.n, K, starts, blk_of);
     const int nb = (int)starts.size();
+    written.assign(K.na > 0 ? K.na : 1, 0);
+    any_untagged_store = false;
+    for (int i = 0; i < K.n; ++i) {
+      if (I[i].op != SFG_ST) continue;
+      const int tg = tags[i][I[i].s1];
+      if (tg > 0) written[tg - 1] = 1;
+      else if (tg != TAG_BOT) any_untagged_store = true;  // BOT: unreachable store
+    }
 
     o << "template <bool PAR>\nstatic __device__ __forceinline__ int sim_" << kidx
       << "(JitRunner& J, const sfg_prog& P, Lane& L, Mem& M, sfg_verdict& V, const Pre& pre, int ctaid, int tid, "
