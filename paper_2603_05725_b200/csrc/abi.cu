@@ -236,7 +236,21 @@ int sfg_program_create(const void* prog, size_t prog_bytes, const void* ins, siz
         const double ev = (double)H[h].grid * (double)H[h].block * (double)p->P.budget;
         events = (ev + (double)events >= 1.8e19) ? ~0ull : events + (uint64_t)ev;
       }
-    const int rc = sfg_jit_build(p->P, (const sfg_ins*)ins, events, p->jit_source, p->jit_log, &p->jit_lib,
+    // kernels after whose every launch memory is dead: no later launch in COMPUTE and
+    // no readouts (the readout copy_outs only run with diff_readback)
+    uint32_t dead = 0, alive = 0;
+    {
+      int last = -1;
+      for (size_t h = 0; h < n_hostops; ++h)
+        if (H[h].kind == SFG_H_LAUNCH) last = (int)h;
+      for (size_t h = 0; h < n_hostops; ++h) {
+        if (H[h].kind != SFG_H_LAUNCH) continue;
+        if ((int)h == last && !p->P.diff_readback) dead |= 1u << H[h].kernel;
+        else alive |= 1u << H[h].kernel;
+      }
+      dead &= ~alive;
+    }
+    const int rc = sfg_jit_build(p->P, (const sfg_ins*)ins, events, dead, p->jit_source, p->jit_log, &p->jit_lib,
                                  &p->jit_kernel, &p->jit_tail);
     if (rc != 0) {
       g_err = "sfg_program_create: JIT build failed (" + std::to_string(rc) + "): " + p->jit_log.substr(0, 6000);
@@ -339,7 +353,7 @@ int sfg_jit_check(const void* prog, size_t prog_bytes, const void* ins, uint64_t
   memcpy(&P, prog, sizeof P);
   std::string src, log;
   std::vector<char> cubin;
-  const int rc = sfg_jit_compile(P, (const sfg_ins*)ins, max_edge_events, src, log, cubin);
+  const int rc = sfg_jit_compile(P, (const sfg_ins*)ins, max_edge_events, 0u, src, log, cubin);
   const std::string text = rc ? log + "\n----\n" + src : src;
   if (out && cap) {
     const size_t n = text.size() < cap - 1 ? text.size() : cap - 1;

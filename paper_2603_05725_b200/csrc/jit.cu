@@ -174,7 +174,10 @@ struct Gen {
       // loads from a record no store of this kernel can reach need no tag (no thread
       // of the launch writes it: nothing to conflict with)
       const bool ro = !st && !any_untagged_store && !written[q];
-      const std::string trk = ro ? std::string() :
+      // stores into a record this kernel never loads, with memory dead after the
+      // launch: their order across threads cannot be observed
+      const bool wo = st && dead_now && !any_untagged_load && !loaded[q];
+      const std::string trk = (ro || wo) ? std::string() :
           "if (PAR && par_track(J.tags, J.ntags, pw" + Q + " + (lo_ - pb" + Q + "), " + W_s + ", " +
           (st ? "true" : "false") + ", J.me, J.waw)) { " + radj(slow, j) + "rc = RUN_CONFLICT; goto done; } ";
       if (st) return trk + "*" + ptr + " = (" + T + ")sv_;";
@@ -216,8 +219,12 @@ struct Gen {
   // stores of the kernel being emitted: written[q] = some store's base carries the
   // tag of pointer parameter q; any_untagged_store = some store's base has no
   // static tag (could reach any record)
-  std::vector<char> written;
-  bool any_untagged_store = false;
+  std::vector<char> written, loaded;
+  bool any_untagged_store = false, any_untagged_load = false;
+  // bit k: memory is dead after every launch of kernel k (no later launch in the
+  // COMPUTE script, no readouts) -- its stores can only be observed by its own loads
+  uint32_t dead_kernels = 0;
+  bool dead_now = false;
 
   std::string src_r(const sfg_ins& x, int slot) {
     const bool imm = slot == 1 ? (x.flags & SFG_F_S1_IMM) : (x.flags & SFG_F_S2_IMM);
@@ -319,13 +326,16 @@ struct Gen {
     const auto tags = tag_flow(I, K.n, K, starts, blk_of);
     const int nb = (int)starts.size();
     written.assign(K.na > 0 ? K.na : 1, 0);
-    any_untagged_store = false;
+    loaded.assign(K.na > 0 ? K.na : 1, 0);
+    any_untagged_store = any_untagged_load = false;
     for (int i = 0; i < K.n; ++i) {
-      if (I[i].op != SFG_ST) continue;
+      if (I[i].op != SFG_ST && I[i].op != SFG_LD) continue;
       const int tg = tags[i][I[i].s1];
-      if (tg > 0) written[tg - 1] = 1;
-      else if (tg != TAG_BOT) any_untagged_store = true;  // BOT: unreachable store
+      const bool st = I[i].op == SFG_ST;
+      if (tg > 0) (st ? written : loaded)[tg - 1] = 1;
+      else if (tg != TAG_BOT) (st ? any_untagged_store : any_untagged_load) = true;  // BOT: unreachable
     }
+    dead_now = (dead_kernels >> kidx) & 1u;
 
     o << "template <bool PAR>\nstatic __device__ __forceinline__ int sim_" << kidx
       << "(JitRunner& J, const sfg_prog& P, Lane& L, Mem& M, sfg_verdict& V, const Pre& pre, int ctaid, int tid, "
@@ -566,9 +576,11 @@ struct Gen {
 }  // namespace sfgjit
 
 // Generate and compile; on success `cubin` holds the sm_100a image.  Returns 0 on success.
-static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_edge_events, std::string& source,
+static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_edge_events, uint32_t dead_kernels,
+                           std::string& source,
                            std::string& log, std::vector<char>& cubin) {
   sfgjit::Gen g(P, ins);
+  g.dead_kernels = dead_kernels;
   if (const char* tb = getenv("SFG_TAIL_MINB")) g.tail_minb = atoi(tb) >= 1 ? atoi(tb) : 12;
   if (const char* bb = getenv("SFG_BULK_MINB")) g.bulk_minb = atoi(bb) >= 1 ? atoi(bb) : 1;
   source = g.run(P.n_edges, max_edge_events);
@@ -611,10 +623,11 @@ static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_e
 }
 
 // Generate, compile and load the specialized execute kernels (bulk + tail).  Returns 0 on success.
-static int sfg_jit_build(const sfg_prog& P, const sfg_ins* ins, uint64_t max_edge_events, std::string& source,
+static int sfg_jit_build(const sfg_prog& P, const sfg_ins* ins, uint64_t max_edge_events, uint32_t dead_kernels,
+                         std::string& source,
                          std::string& log, cudaLibrary_t* lib_out, cudaKernel_t* kern_out, cudaKernel_t* tail_out) {
   std::vector<char> cubin;
-  const int rc = sfg_jit_compile(P, ins, max_edge_events, source, log, cubin);
+  const int rc = sfg_jit_compile(P, ins, max_edge_events, dead_kernels, source, log, cubin);
   if (rc) return rc;
   cudaError_t e = cudaLibraryLoadData(lib_out, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
   if (e != cudaSuccess) {
