@@ -140,7 +140,7 @@ static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t -
 // one conflict tag and one snapshot word per 4 bytes of work region (exec_core.cuh)
 constexpr int kExecSmemMax = 96 * 1024;
 constexpr int kBulkSmem = 64 * 1024;   // per 128-thread CTA
-constexpr int kTailSmem = 8 * 1024;    // per one-warp CTA (one input per warp)
+constexpr int kTailSmem = 16 * 1024;   // per one-warp CTA (up to 4 inputs per warp)
 
 static inline int tag_words(int64_t max_work_bytes) { return (int)((max_work_bytes + 3) / 4); }
 static inline CorpusView CV(const sfg_corpus_dev* c) {
