@@ -301,7 +301,7 @@ def run_e2e(a, m, torch, R, world):
             "d2h_bytes_per_step": tr["d2h_bytes"] / steps, "wall_s": wall, "execs": s.compute_runs, "rounds": steps,
             "api": "campaign.fuzz_loop(manifest, CampaignConfig) -> CampaignSummary",
             "includes": "program build (JIT cache hit), INIT baseline, corpus upload, all rounds, result objects",
-            "findings_unique": len(s.findings), "stop": s.stop_reason}
+            "findings_unique": len(s.findings), "stop": s.stop_reason, "setup_s": tr.get("setup_s")}
 
 
 def main():

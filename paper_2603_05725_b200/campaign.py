@@ -150,6 +150,7 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
     if config.distributed:
         from .shard import RoundComm
         comm = RoundComm()
+    t_setup = time.perf_counter()
     dc = DeviceCampaign(manifest, master_seed=config.master_seed, mem=config.mem_config, comm=comm,
                         mutation=config.mutation, budget=config.instruction_budget,
                         window=config.admission_window, recent_weight=config.recent_weight,
@@ -158,6 +159,7 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
                         ids_reset_per_input=config.mode == "reinit")
     if out_dir is not None:
         _write_corpus_entry(out_dir, dc.host_entries[0][0], specs)
+    t_setup = time.perf_counter() - t_setup
     stop_reason = "iterations"
     executed = 0
     init_runs = term_runs = 0
@@ -237,7 +239,8 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
         (out_dir / "timing.rec").write_text(
             f"timing v1\nwall_seconds={wall:.6f} execs_per_second={summary.execs_per_second:.2f}\n")
     # host<->device traffic of the campaign (not a reference field; bench e2e accounting)
-    summary.device_transfer = {"h2d_bytes": dc.h2d_bytes, "d2h_bytes": dc.d2h_bytes, "rounds": dc.rounds}
+    summary.device_transfer = {"h2d_bytes": dc.h2d_bytes, "d2h_bytes": dc.d2h_bytes, "rounds": dc.rounds,
+                               "setup_s": t_setup}
     dc.close()
     return summary
 

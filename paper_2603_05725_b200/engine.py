@@ -240,6 +240,7 @@ class DeviceCampaign:
         self._last_done = None           # event: previous round finalized
         self._last_counts = None         # event: counts_run valid for the next submission
         self.rounds = 0
+        self.spec_depth = 2              # adaptive speculation depth (run_rounds)
         self.launches = 0                # kernels launched through the C ABI (bench evidence)
         self.timing = False              # record CUDA events around each execute kernel
         self.exec_events: list = []
@@ -658,9 +659,16 @@ class DeviceCampaign:
         def more():
             return nxt < len(plan) and (should_continue is None or should_continue())
 
-        while len(inflight) < depth and more():
-            submit(nxt)
-            nxt += 1
+        # Speculation depth adapts: an admission invalidates every round in flight, and
+        # admissions cluster at the start of a campaign (new coverage), so the depth
+        # drops to 2 after an admitting round and doubles after each clean one.
+        def fill():
+            nonlocal nxt
+            while len(inflight) < min(depth, self.spec_depth) and more():
+                submit(nxt)
+                nxt += 1
+
+        fill()
         while inflight:
             k, S = inflight.popleft()
             res = self._finalize(S)
@@ -672,14 +680,15 @@ class DeviceCampaign:
                 break
             if res.n_admitted:
                 # later in-flight rounds were mutated from the pre-admission corpus: redo them
+                self.spec_depth = 2
                 redo = list(inflight)
                 inflight.clear()
                 for kk, SS in redo:
                     self._submit(SS, SS.round_it0, SS.round_n, SS.round_index, resubmit=True)
                     inflight.append((kk, SS))
-            if more():
-                submit(nxt)
-                nxt += 1
+            else:
+                self.spec_depth = min(2 * self.spec_depth, 1 << 20)
+            fill()
         return results
 
     # ---- bench / e2e helpers ------------------------------------------------------------
