@@ -398,7 +398,10 @@ struct Gen {
     o << "  const " << RT << " HARD = SFT ? (" << RT << ")(SOFT > total ? SOFT - total : 0ull) : BUD;\n";
     // group-parallel mode: stop at poll points every kPoll retired instructions to see
     // whether this thread can still matter (run_launch_group)
-    o << "  " << RT << " LIM = (PAR && HARD > (" << RT << ")kPoll) ? (" << RT << ")kPoll : HARD;\n";
+    // bulk pass (soft cap on): poll every kStrag retired instructions whether the rest of
+    // the warp's batch has finished; a straggler past kStragMin is deferred then
+    o << "  " << RT << " LIM = PAR ? ((HARD > (" << RT << ")kPoll) ? (" << RT << ")kPoll : HARD)\n"
+         "            : ((J.done != nullptr && HARD > (" << RT << ")kStrag) ? (" << RT << ")kStrag : HARD);\n";
     o << "  (void)grid; (void)block; (void)ctaid; (void)tid;\n";
     for (int b = 0; b < nb; ++b) {
       const int s0 = starts[b], e = b + 1 < nb ? starts[b + 1] : K.n;
@@ -411,6 +414,8 @@ struct Gen {
           o << "  if (ret + " << sp << " >= LIM) {\n"
             << "    if constexpr (PAR) { if (LIM < HARD) { if (J.poll()) { rc = RUN_ABORT; goto done; }\n"
             << "      LIM = (HARD - ret > " << sp << " + kPoll) ? ret + " << sp << " + kPoll : HARD; goto B" << b << "; } }\n"
+            << "    else { if (LIM < HARD) { if (J.straggler(total + ret)) { rc = RUN_DEFER; goto done; }\n"
+            << "      LIM = (HARD - ret > " << sp << " + kStrag) ? ret + " << sp << " + kStrag : HARD; goto B" << b << "; } }\n"
             << "    if (SFT) { rc = RUN_DEFER; goto done; } goto S" << b << "; }\n";
         for (int i = s0; i < e; ++i) {
           const sfg_ins& x = I[i];
@@ -458,10 +463,14 @@ struct Gen {
     edge_ovf_checks = max_edge_events >= 0xFFFFFFFFull;
     const int NE = n_edges > 0 ? n_edges : 1;
     o << "#include \"exec_core.cuh\"\n\nnamespace {\n\n";
-    o << "constexpr uint32_t kPoll = 4096u;\n\n";
+    o << "constexpr uint32_t kPoll = 4096u;\n";
+    o << "constexpr uint32_t kStrag = 2048u;\nconstexpr uint64_t kStragMin = 8192ull;\n\n";
     o << "struct JitRunner {\n  uint32_t ec[" << NE << "], ecs[" << NE
       << "];\n  bool ovf, ovfs;\n  uint64_t soft_cap;\n"
       << "  uint32_t* tags = nullptr;\n  int ntags = 0, t = 0;\n  uint32_t me = 0;\n  GroupSmem* gs = nullptr;\n  int* waw = nullptr;\n"
+         "  int* done = nullptr;  // bulk: inputs of this warp's batch finished so far\n  int batch_n = 0;\n"
+         "  SFG_DEV bool straggler(uint64_t retired) const {\n"
+         "    return retired >= kStragMin && *reinterpret_cast<volatile const int*>(done) >= batch_n - 1;\n  }\n"
       << "  SFG_DEV void begin_input() {\n#pragma unroll\n    for (int e = 0; e < " << NE << "; ++e) ec[e] = 0u;\n    ovf = false;\n"
          "    asm volatile(\"mov.u32 %0, 0;\" : \"=r\"(J_dyn));  // opaque 0: keeps ecs[] out of registers\n  }\n"
       // the chunk-start copy lives in local memory (a dynamically indexed array), so
@@ -511,12 +520,20 @@ struct Gen {
          "      for (int i = atomicAdd(next, 1); i < E.n; i = atomicAdd(next, 1)) run_input<false>(P, E, i, R, g);\n"
          "      return;\n"
          "    }\n"
+         "    __shared__ int s_done[32];\n"
+         "    const int w = threadIdx.x >> 5;\n"
          "    while (true) {\n"
          "      int b = 0;\n"
          "      if (lane == 0) b = atomicAdd(next, 32);\n"
          "      b = __shfl_sync(0xffffffffu, b, 0);\n"
          "      if (b >= E.n) break;\n"
-         "      if (b + lane < E.n) run_input<false>(P, E, E.order ? E.order[b + lane] : b + lane, R, g);\n"
+         "      if (lane == 0) s_done[w] = 0;\n"
+         "      __syncwarp();\n"
+         "      if (E.soft_cap) { R.done = &s_done[w]; R.batch_n = E.n - b < 32 ? E.n - b : 32; }\n"
+         "      if (b + lane < E.n) {\n"
+         "        run_input<false>(P, E, E.order ? E.order[b + lane] : b + lane, R, g);\n"
+         "        atomicAdd(&s_done[w], 1);\n"
+         "      }\n"
          "      __syncwarp();\n"
          "    }\n"
          "    return;\n"
