@@ -14,6 +14,9 @@
 // abi.cu) marks the parameters reaching a setp, directly or through
 // arithmetic, conversions or load addresses.  Arguments used only as strides
 // or data (matmul's lda/ldb/ldc, array contents) move the stop point at most.
+// i32 arguments enter by magnitude class (sign, bit length) rather than value:
+// loop bounds of similar size run similar trip counts, and the inputs that will
+// run long (huge bounds) end up in the same warps instead of one per warp.
 #include "common.cuh"
 
 namespace {
@@ -30,7 +33,13 @@ SFG_DEV int sig_bucket(const sfg_prog& P, const sfg_val* v, uint32_t mask) {
   for (int a = 0; a < P.n_args; ++a) {
     if (!((mask >> a) & 1u)) continue;
     h = sig_mix(h, (uint64_t)v[a].kind | ((uint64_t)v[a].space << 8) | ((uint64_t)v[a].elem << 16));
-    if (v[a].kind != SFG_V_ARR) {
+    if (v[a].kind == SFG_V_I32) {
+      // magnitude class (sign, bit length): loop bounds of similar size share a
+      // bucket, so the long-running inputs gather in the same warps
+      const int32_t x = (int32_t)v[a].bits;
+      const uint32_t mag = x < 0 ? (uint32_t)(-(int64_t)x) : (uint32_t)x;
+      h = sig_mix(h, ((uint64_t)(x < 0) << 8) | (uint64_t)(32 - __clz(mag)));
+    } else if (v[a].kind != SFG_V_ARR) {
       h = sig_mix(h, v[a].bits);
     } else {
       h = sig_mix(h, v[a].nbytes);
