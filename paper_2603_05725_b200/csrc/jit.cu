@@ -457,7 +457,7 @@ struct Gen {
   }
 
   int tail_minb = 12;
-  int bulk_minb = 1;
+  int bulk_minb = 3;
 
   std::string run(int n_edges, uint64_t max_edge_events) {
     edge_ovf_checks = max_edge_events >= 0xFFFFFFFFull;
@@ -599,7 +599,7 @@ static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_e
   sfgjit::Gen g(P, ins);
   g.dead_kernels = dead_kernels;
   if (const char* tb = getenv("SFG_TAIL_MINB")) g.tail_minb = atoi(tb) >= 1 ? atoi(tb) : 12;
-  if (const char* bb = getenv("SFG_BULK_MINB")) g.bulk_minb = atoi(bb) >= 1 ? atoi(bb) : 1;
+  if (const char* bb = getenv("SFG_BULK_MINB")) g.bulk_minb = atoi(bb) >= 1 ? atoi(bb) : 3;
   source = g.run(P.n_edges, max_edge_events);
   // process-wide cache: identical programs (same generated source) compile once
   static std::mutex mu;
