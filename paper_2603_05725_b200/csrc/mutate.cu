@@ -68,13 +68,15 @@ __device__ int pick_parent(SfgStream& s, const sfg_prog& P, const CorpusView& C,
 __device__ int draw_picks(SfgStream& s, const sfg_prog& P, int8_t* picks) {
   int cap = P.max_ops < P.n_mutable ? P.max_ops : P.n_mutable;
   const int n_ops = 1 + s.geometric_small(0.5, cap - 1);
-  int8_t pool[SFG_MAX_ARGS];
+  // pool.pop(integers(len)): the idx-th remaining entry of mutable_args, kept as a
+  // bitmask of remaining positions (registers, no local array)
   int len = P.n_mutable;
-  for (int i = 0; i < len; ++i) pool[i] = P.mutable_args[i];
+  uint32_t rem = len >= 32 ? 0xffffffffu : (1u << len) - 1u;
   for (int k = 0; k < n_ops; ++k) {
     const int idx = (int)s.integers(0, len);
-    picks[k] = pool[idx];
-    for (int i = idx; i + 1 < len; ++i) pool[i] = pool[i + 1];
+    const int pos = (int)__fns(rem, 0, idx + 1);
+    picks[k] = P.mutable_args[pos];
+    rem &= ~(1u << pos);
     --len;
   }
   return n_ops;
@@ -318,7 +320,7 @@ extern "C" __global__ void sfg_plan_kernel(sfg_prog P, CorpusView C, int64_t it0
 }
 
 // counts_prefix[i][c]: rotation count of int column c seen by input i
-extern "C" __global__ void sfg_mutate_kernel(sfg_prog P, CorpusView C, int64_t it0, int n,
+extern "C" __global__ void __launch_bounds__(128, 8) sfg_mutate_kernel(sfg_prog P, CorpusView C, int64_t it0, int n,
                                              const uint64_t* counts_prefix, const uint64_t* counts_base,
                                              sfg_child* child_out, sfg_val* vals_out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -328,10 +330,16 @@ extern "C" __global__ void sfg_mutate_kernel(sfg_prog P, CorpusView C, int64_t i
   memset(&ch, 0, sizeof(ch));
   ch.it = it;
   sfg_val* vout = vals_out + (size_t)i * P.n_args;
+  const sfg_val* pv = C.vals;             // parent values (the seed for it == 1)
+  // picked args: the mutated value goes straight to vout; its kind / materialized
+  // size / nbytes stay in registers for the layout pass
+  int ma[SFG_MAX_OPS] = {-1, -1, -1};
+  uint64_t msz[SFG_MAX_OPS] = {0, 0, 0};
+  uint32_t mnb[SFG_MAX_OPS] = {0, 0, 0};
+  uint8_t mkind[SFG_MAX_OPS] = {0, 0, 0};
   if (it == 1) {  // fuzz_loop evaluates the recorded seed first (campaign.py:739-740)
     ch.parent = -1;
     ch.rng_seed = C.meta[0].rng_seed;
-    for (int a = 0; a < P.n_args; ++a) vout[a] = C.vals[a];
   } else {
     SfgStream s;
     s.init(P.master_seed, P.keybase + (uint64_t)it);
@@ -340,8 +348,7 @@ extern "C" __global__ void sfg_mutate_kernel(sfg_prog P, CorpusView C, int64_t i
     const int n_ops = draw_picks(s, P, picks);
     ch.parent = parent;
     ch.n_ops = n_ops;
-    const sfg_val* pv = C.vals + (size_t)parent * P.n_args;
-    for (int a = 0; a < P.n_args; ++a) vout[a] = pv[a];
+    pv = C.vals + (size_t)parent * P.n_args;
     for (int k = 0; k < n_ops; ++k) {
       const int a = picks[k];
       sfg_op op;
@@ -366,24 +373,45 @@ extern "C" __global__ void sfg_mutate_kernel(sfg_prog P, CorpusView C, int64_t i
         gen_array_op(s, P, v, op);
       }
       apply_desc(P, v, op);
-      vout[a] = v;
+      vout[a] = v;   // data_off filled by the layout pass
+      ma[k] = a;
+      msz[k] = sfg_mat_size(v);
+      mnb[k] = v.nbytes;
+      mkind[k] = v.kind;
       ch.ops[k] = op;
     }
     ch.rng_seed = s.next64();
   }
-  // work layout: array regions (materialized size, 16-aligned) then COMPUTE named allocs
-  uint64_t off = 0;
+  // one pass over the child's values: parent value or its mutation, work layout
+  // (array regions at materialized size, 16-aligned, then COMPUTE named allocs),
+  // readout sizes; each value written once
+  uint64_t off = 0, rb = P.diff_readback ? (uint64_t)P.readout_bytes_fixed : 0ull;
   for (int a = 0; a < P.n_args; ++a) {
-    if (vout[a].kind != SFG_V_ARR) continue;
-    vout[a].data_off = off;
-    off += sfg_align16(sfg_mat_size(vout[a]));
+    int m = -1;
+#pragma unroll
+    for (int k = 0; k < SFG_MAX_OPS; ++k)
+      if (ma[k] == a) m = k;
+    uint32_t nb;
+    if (m >= 0) {       // mutated: value already written
+      nb = mnb[m];
+      if (mkind[m] == SFG_V_ARR) {
+        vout[a].data_off = off;
+        off += sfg_align16(msz[m]);
+      }
+    } else {
+      sfg_val v = pv[a];
+      nb = v.nbytes;
+      if (v.kind == SFG_V_ARR) {
+        v.data_off = off;
+        off += sfg_align16(sfg_mat_size(v));
+      }
+      vout[a] = v;
+    }
+    if (P.diff_readback)
+      for (int k = 0; k < P.n_copyout_arg; ++k)
+        if (P.copyout_arg[k] == a) rb += sfg_align16(nb);
   }
   ch.work_bytes = off + (uint64_t)P.named_work_bytes;
-  uint64_t rb = 0;
-  if (P.diff_readback) {
-    rb = (uint64_t)P.readout_bytes_fixed;
-    for (int k = 0; k < P.n_copyout_arg; ++k) rb += sfg_align16(vout[P.copyout_arg[k]].nbytes);
-  }
   ch.readout_bytes = rb;
   child_out[i] = ch;
 }
