@@ -395,7 +395,7 @@ int sfg_mutate(const sfg_program* p, const sfg_corpus_dev* c, int64_t it0, int n
 int sfg_apply(const sfg_program* p, const sfg_corpus_dev* c, int n, const void* children, const void* vals,
               const uint64_t* work_base, uint8_t* work, void* stream) {
   if (n <= 0) return 0;
-  sfg_apply_kernel<<<blocks_for((int64_t)n * 32, 256), 256, 0, S(stream)>>>(
+  sfg_apply_kernel<<<blocks_for((int64_t)n * kApplyLanes, 256), 256, 0, S(stream)>>>(
       p->P, CV(c), n, (const sfg_child*)children, (const sfg_val*)vals, work_base, work, nullptr, nullptr);
   SFG_CHECK_LAUNCH("sfg_apply");
   return 0;

@@ -419,14 +419,19 @@ extern "C" __global__ void __launch_bounds__(128, 8) sfg_mutate_kernel(sfg_prog 
 // warp per input: parent payloads -> child work region (materialized contents)
 // (sel != nullptr: only the inputs sel[0 .. *sel_n) -- the deferred long inputs
 // re-materialized for the tail pass)
+// An input's arrays are a few hundred bytes (16-byte chunks), so a group of
+// kApplyLanes lanes handles one input and a warp keeps 32 / kApplyLanes inputs'
+// dependent descriptor loads in flight at once.
+constexpr int kApplyLanes = 8;
+
 extern "C" __global__ void sfg_apply_kernel(sfg_prog P, CorpusView C, int n, const sfg_child* children,
                                             const sfg_val* vals, const uint64_t* work_base, uint8_t* work,
                                             const int32_t* sel, const int* sel_n) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int gid = (blockIdx.x * blockDim.x + threadIdx.x) / kApplyLanes;
+  const int lane = threadIdx.x % kApplyLanes;
+  const int ngroups = (gridDim.x * blockDim.x) / kApplyLanes;
   if (sel) n = *sel_n;
-  for (int j = warp; j < n; j += nwarps) {
+  for (int j = gid; j < n; j += ngroups) {
     const int i = sel ? sel[j] : j;
     const sfg_child& ch = children[i];
     const int parent = ch.parent < 0 ? 0 : ch.parent;
@@ -439,7 +444,7 @@ extern "C" __global__ void sfg_apply_kernel(sfg_prog P, CorpusView C, int n, con
       for (int k = 0; k < ch.n_ops; ++k)
         if (ch.ops[k].arg == a) op = &ch.ops[k];
       emit_child(base + cv[a].data_off, sfg_mat_size(cv[a]), C.data + pv[a].data_off, pv[a].nbytes, cv[a],
-                 op, lane, 32);
+                 op, lane, kApplyLanes);
     }
   }
 }
