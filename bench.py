@@ -145,9 +145,12 @@ def run_ours(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    # one rank per GPU; SFG_DIST_BACKEND=gloo lets several ranks share a GPU (tests of
+    # the multi-rank path on a one-GPU box: collectives staged through host memory)
+    backend = os.environ.get("SFG_DIST_BACKEND", "nccl")
+    torch.cuda.set_device(local % torch.cuda.device_count())
     if world > 1:
-        dist.init_process_group("nccl")
+        dist.init_process_group(backend)
     from paper_2603_05725_b200.engine import DeviceCampaign
     from paper_2603_05725_b200.workloads import load
 
@@ -179,7 +182,7 @@ def run_ours(a):
     launches0 = dc.launches
     dc.exec_events.clear()
     fin = []                    # host clock at each round's finalization (diagnostics)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local % torch.cuda.device_count()) as clk:
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         h0 = time.perf_counter()
@@ -195,7 +198,7 @@ def run_ours(a):
     bulk_ms = [s.elapsed_time(b) for s, b, e in dc.exec_events if b is not None]
     k3_ms = [s.elapsed_time(e) for s, b, e in dc.exec_events]
     t_local = t0.elapsed_time(t1) / 1000.0
-    t = torch.tensor([t_local], dtype=torch.float64, device="cuda")
+    t = torch.tensor([t_local], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max = float(t.item())
@@ -292,7 +295,8 @@ def run_e2e(a, m, torch, R, world):
     s = fuzz_loop(m, cfg)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
-    t = torch.tensor([wall], dtype=torch.float64, device="cuda")
+    t = torch.tensor([wall], dtype=torch.float64,
+                     device="cuda" if os.environ.get("SFG_DIST_BACKEND", "nccl") == "nccl" else "cpu")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     wall = float(t.item())
