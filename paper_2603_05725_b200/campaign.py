@@ -20,7 +20,7 @@ import time
 from dataclasses import dataclass, field
 from pathlib import Path
 
-from .baseline import MemConfig
+from .baseline import InitFailure, MemConfig
 from .coverage import build_report, render_text, report_to_rec
 from .engine import DeviceCampaign, MutationConfig
 from .findings import BugClass, FindingsLog
@@ -126,6 +126,15 @@ def _worker_ranges(total: int, workers: int):
     return out
 
 
+def _device_campaign(manifest, config: CampaignConfig, comm) -> DeviceCampaign:
+    return DeviceCampaign(manifest, master_seed=config.master_seed, mem=config.mem_config, comm=comm,
+                          mutation=config.mutation, budget=config.instruction_budget,
+                          window=config.admission_window, recent_weight=config.recent_weight,
+                          diff_readback=config.diff_readback, stop_on_first_finding=config.stop_on_first_finding,
+                          stop_bug_class=config.stop_bug_class, device=config.device,
+                          ids_reset_per_input=config.mode == "reinit")
+
+
 def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
     if config.mode not in ("amortized", "reinit"):
         raise CampaignFatalError(f"unknown mode {config.mode!r}")
@@ -151,12 +160,10 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
         from .shard import RoundComm
         comm = RoundComm()
     t_setup = time.perf_counter()
-    dc = DeviceCampaign(manifest, master_seed=config.master_seed, mem=config.mem_config, comm=comm,
-                        mutation=config.mutation, budget=config.instruction_budget,
-                        window=config.admission_window, recent_weight=config.recent_weight,
-                        diff_readback=config.diff_readback, stop_on_first_finding=config.stop_on_first_finding,
-                        stop_bug_class=config.stop_bug_class, device=config.device,
-                        ids_reset_per_input=config.mode == "reinit")
+    try:
+        dc = _device_campaign(manifest, config, comm)
+    except InitFailure as e:   # campaign.py:723-725: the init phase failed on the seed input
+        raise CampaignFatalError(str(e)) from e
     if out_dir is not None:
         _write_corpus_entry(out_dir, dc.host_entries[0][0], specs)
     t_setup = time.perf_counter() - t_setup

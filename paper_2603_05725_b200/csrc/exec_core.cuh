@@ -244,6 +244,16 @@ SFG_DEV int lane_alloc(const sfg_prog& P, Lane& L, int sp, int64_t size, int lab
   return L.nrec++;
 }
 
+// out of space: the figures of OutOfSpaceError's message (device_memory.py:426-430)
+// -- space, slot bytes needed, bytes remaining in scope 0 -- into the verdict
+SFG_DEV void oos_detail(const sfg_prog& P, const Lane& L, sfg_verdict& V, int sp, int64_t size) {
+  if (V.status != SFG_ST_OUT_OF_SPACE) return;
+  const int64_t g = P.granule;
+  V.space = (uint8_t)sp;
+  V.alloc_size = P.redzone + ((size + g - 1) / g) * g + P.redzone;
+  V.alloc_base = P.scope_size[sp] - L.cursor[sp];
+}
+
 // free (device_memory.py:442-487); returns 0 ok, 1 invalid free, -status fatal
 SFG_DEV int lane_free(const sfg_prog& P, Lane& L, int64_t addr) {
   const int sp = space_of(P, addr);
@@ -663,7 +673,7 @@ SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R, c
       if (op.size <= 0) { V.status = SFG_ST_ZERO_ALLOC; break; }
       const int64_t phys = (int64_t)arrays_end + op.work_off;
       const int k = lane_alloc(P, L, op.space, op.size, op.label, phys);
-      if (k < 0) { V.status = -k; break; }
+      if (k < 0) { V.status = -k; oos_detail(P, L, V, op.space, op.size); break; }
       for (int64_t b = 0; b < op.size; ++b) M.work[phys + b] = 0;
       L.named_addr[op.buf] = L.rec[k].base;
       L.named_rec[op.buf] = (int16_t)k;
@@ -743,7 +753,7 @@ SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R, c
       if (L.mat_rec[B.idx] < 0) {
         const int64_t size = (int64_t)sfg_mat_size(v);
         const int k = lane_alloc(P, L, v.space, size, P.label_arg_base + B.idx, (int64_t)v.data_off);
-        if (k < 0) { V.status = -k; stop = true; break; }
+        if (k < 0) { V.status = -k; oos_detail(P, L, V, v.space, size); stop = true; break; }
         L.mat_rec[B.idx] = (int16_t)k;
       }
       const LRec& r = L.rec[L.mat_rec[B.idx]];

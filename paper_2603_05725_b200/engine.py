@@ -493,10 +493,11 @@ class DeviceCampaign:
         st = None
         if S.i_base <= g < S.i_base + S.n:
             i = g - S.i_base
-            st = int(_np(S.verdicts[i * VERDICT.itemsize:(i + 1) * VERDICT.itemsize], VERDICT)[0]["status"])
-        st = next(x for x in self.comm.all_gather_object(st) if x is not None)
-        if st == ST_OUT_OF_SPACE:
-            raise OutOfSpaceError(f"input {g}: allocation does not fit its space")
+            v = _np(S.verdicts[i * VERDICT.itemsize:(i + 1) * VERDICT.itemsize], VERDICT)[0]
+            st = (int(v["status"]), int(v["space"]), int(v["alloc_size"]), int(v["alloc_base"]))
+        st, space, need, remain = next(x for x in self.comm.all_gather_object(st) if x is not None)
+        if st == ST_OUT_OF_SPACE:   # the reference's message (device_memory.py:428-430)
+            raise OutOfSpaceError(f"{SPACE_ORDER[space].value} scope 0: need {need} bytes, {remain} remain")
         if st == ST_ZERO_ALLOC:
             raise ValueError("allocation size must be positive")
         raise DeviceFatal({ST_LANE_RECS: "per-input allocation table overflow",

@@ -17,6 +17,8 @@ Writes (all small, committed):
                       summary, corpus) for a few configs
   ref_workloads.json  the same batched records for this repo's synthetic
                       workloads (paper_2603_05725_b200/workloads)
+  ref_errors.json     the exception class the reference fuzz_loop raises for
+                      failing harnesses (INIT failure, out of space)
   ref_traces.json     ExecHooks event streams (TraceHooks "EV mem" / "EV cf"
                       lines): per sampled input of every benchmark, and for a
                       traced batched campaign (dot, amax)
@@ -283,13 +285,56 @@ def traces():
     return out
 
 
+# Error behaviour (campaign.py:79-80, 685-688, 723-725; device_memory.py:62-63,
+# 426-430): which exception the reference's fuzz_loop raises, for harnesses
+# written here in the reference's own formats.
+ERROR_KERNEL = """\
+kernel poke(buf:ptr.global, n:i32) regs=8
+  st.global.b32 [%a0], %r0
+  exit
+"""
+ERROR_CASES = {
+    # INIT copies 128 bytes into a 64-byte buffer: the init phase fails on the seed
+    "init_overflow": ("argspec b ptr global i32 count=4 seed=zeros lo=0 hi=9\n"
+                      "argspec n i32 seed=3 lo=0 hi=9\n\n"
+                      "init:\n  alloc scratch global 64\n  copy_in scratch hex:" + "00" * 128 + "\n"
+                      "compute:\n  launch poke grid=1 block=1 args=arg:0,arg:1\n"
+                      "term:\n  free scratch\n", {}),
+    # a COMPUTE allocation larger than the global space
+    "compute_out_of_space": ("argspec b ptr global i32 count=4 seed=zeros lo=0 hi=9\n"
+                             "argspec n i32 seed=3 lo=0 hi=9\n\n"
+                             "compute:\n  alloc big global 100000\n"
+                             "  launch poke grid=1 block=1 args=arg:0,arg:1\n  free big\n",
+                             {"global_size": 65536}),
+}
+
+
+def errors(tmp):
+    from simt_forge.device_memory import MemConfig
+    out = {}
+    for name, (body, mem) in ERROR_CASES.items():
+        d = Path(tmp) / name
+        d.mkdir()
+        (d / "kernel.sir").write_text(ERROR_KERNEL)
+        (d / "harness.man").write_text("program kernel.sir\n\n" + body)
+        m = rc.load_harness(d / "harness.man")
+        try:
+            rc.fuzz_loop(m, rc.CampaignConfig(master_seed=11, iterations=8, mem_config=MemConfig(**mem)))
+            out[name] = {"raises": None}
+        except Exception as e:  # noqa: BLE001 - the class is the golden value
+            out[name] = {"raises": type(e).__name__, "message": str(e)}
+    return {"kernel": ERROR_KERNEL, "cases": {k: {"harness": "program kernel.sir\n\n" + v[0], "mem": v[1],
+                                                 **out[k]} for k, v in ERROR_CASES.items()}}
+
+
 def _dump(obj) -> str:
     return json.dumps(obj, sort_keys=True, separators=(",", ":"))
 
 
 def main():
     import tempfile
-    which = sys.argv[1:] or ["assets", "variants", "sampled", "batched", "fuzzloop", "workloads", "traces"]
+    which = sys.argv[1:] or ["assets", "variants", "sampled", "batched", "fuzzloop", "workloads", "traces",
+                             "errors"]
     if "assets" in which:
         (HERE / "bench_assets.json").write_text(_dump(assets()))
     if "variants" in which:
@@ -306,6 +351,9 @@ def main():
         (HERE / "ref_workloads.json").write_text(_dump(workloads()))
     if "traces" in which:
         (HERE / "ref_traces.json").write_text(_dump(traces()))
+    if "errors" in which:
+        with tempfile.TemporaryDirectory() as tmp:
+            (HERE / "ref_errors.json").write_text(_dump(errors(tmp)))
 
 
 if __name__ == "__main__":

@@ -319,3 +319,20 @@ def test_traced_campaign_matches_reference(engine_cls, name):
     assert len(text.splitlines()) == ref["n_lines"]
     assert text.splitlines()[:len(ref["head"])] == ref["head"]
     assert hashlib.sha256(text.encode()).hexdigest() == ref["sha256"]
+
+
+@pytest.mark.parametrize("case", ["init_overflow", "compute_out_of_space"])
+def test_fatal_conditions_raise_reference_exceptions(engine_cls, case):
+    """fuzz_loop raises the reference's exception class (and message) for a failing
+    INIT phase (CampaignFatalError) and for a COMPUTE allocation that does not fit
+    (OutOfSpaceError), tests/golden/ref_errors.json (made by the reference)."""
+    from paper_2603_05725_b200.baseline import MemConfig
+    from paper_2603_05725_b200.campaign import CampaignConfig, fuzz_loop
+    from paper_2603_05725_b200.manifest import harness_from_text
+    data = golden("ref_errors.json")
+    c = data["cases"][case]
+    m = harness_from_text(c["harness"], data["kernel"], f"{case}/harness.man")
+    with pytest.raises(Exception) as ei:
+        fuzz_loop(m, CampaignConfig(master_seed=11, iterations=8, mem_config=MemConfig(**c["mem"])))
+    assert type(ei.value).__name__ == c["raises"]
+    assert str(ei.value) == c["message"]
