@@ -75,6 +75,20 @@ int sfg_jit_check(const void* prog, size_t prog_bytes, const void* ins, uint64_t
 
 int sfg_plan(const sfg_program* p, const sfg_corpus_dev* c, int64_t it0, int n, int32_t* parent,
              int8_t* picks, uint32_t* int_flags, void* stream);
+/* Sequential stream discipline (the reference fuzz_loop itself, campaign.py:714-749:
+ * one worker stream Stream(master_seed, 1000 + w), one MutationSchedule): one
+ * thread generates children it0 .. it0+n-1 in order from the worker state *state
+ * (device, sfg_stream_state_bytes() bytes), rotation counts from counts_base,
+ * writing children / vals as sfg_mutate does, the int-arg picks per input
+ * (int_flags[n][n_int_args]) and the stream state before every input and after
+ * the last (states[n + 1]), so that a round can be cut after an admission and
+ * resumed from there.  sfg_stream_state_init fills a host buffer with
+ * Stream(seed, stream_id)'s initial state. */
+size_t sfg_stream_state_bytes(void);
+int sfg_stream_state_init(uint64_t seed, uint64_t stream_id, void* out_host);
+int sfg_plan_seq(const sfg_program* p, const sfg_corpus_dev* c, int64_t it0, int n, const void* state,
+                 const uint64_t* counts_base, void* children, void* vals, uint32_t* int_flags, void* states,
+                 void* stream);
 int sfg_mutate(const sfg_program* p, const sfg_corpus_dev* c, int64_t it0, int n,
                const uint64_t* counts_prefix, const uint64_t* counts_base, void* children,
                void* vals, void* stream);

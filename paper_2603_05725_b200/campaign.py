@@ -77,6 +77,12 @@ class CampaignConfig:
     # shard every round over the ranks of the initialized torch.distributed group
     # (one process per GPU, per-round merge, shard.py); results do not depend on it
     distributed: bool = False
+    # "batched": the batched-round contract (per-input streams, parents
+    # from the round-start corpus) -- the throughput path; "sequential": the
+    # reference fuzz_loop's own discipline (one worker stream, live corpus), rounds
+    # generated in order on the device and cut after each admission -- results
+    # identical to the reference fuzz_loop, output directories byte for byte
+    discipline: str = "batched"
 
 
 @dataclass
@@ -132,7 +138,8 @@ def _device_campaign(manifest, config: CampaignConfig, comm) -> DeviceCampaign:
                           window=config.admission_window, recent_weight=config.recent_weight,
                           diff_readback=config.diff_readback, stop_on_first_finding=config.stop_on_first_finding,
                           stop_bug_class=config.stop_bug_class, device=config.device,
-                          ids_reset_per_input=config.mode == "reinit")
+                          ids_reset_per_input=config.mode == "reinit",
+                          sequential=config.discipline == "sequential")
 
 
 def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
@@ -140,6 +147,8 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
         raise CampaignFatalError(f"unknown mode {config.mode!r}")
     if config.workers < 1 or config.iterations < 1:
         raise CampaignFatalError("workers and iterations must be >= 1")
+    if config.discipline not in ("batched", "sequential"):
+        raise CampaignFatalError(f"unknown discipline {config.discipline!r}")
     hooks = config.hooks
     for op in manifest.phases["term"]:
         if op.kind not in ("free", "sync"):
@@ -174,7 +183,7 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
         for w, rng_ in enumerate(_worker_ranges(config.iterations, config.workers)):
             if stop_reason != "iterations":
                 break
-            dc.new_worker()   # fresh rotation counts + alloc ids (one image per worker)
+            dc.new_worker(w)  # fresh rotation counts + alloc ids (one image per worker)
             if config.mode == "amortized":
                 init_runs += 1
             state = {"stop": None}

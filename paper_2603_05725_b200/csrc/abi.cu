@@ -383,6 +383,29 @@ int sfg_plan(const sfg_program* p, const sfg_corpus_dev* c, int64_t it0, int n, 
   return 0;
 }
 
+size_t sfg_stream_state_bytes(void) { return sizeof(SfgStream); }
+
+int sfg_stream_state_init(uint64_t seed, uint64_t stream_id, void* out_host) {
+  SfgStream st;
+  memset(&st, 0, sizeof st);
+  st.ctr[0] = st.ctr[1] = st.ctr[2] = st.ctr[3] = 0;
+  st.key0 = seed;
+  st.key1 = stream_id;
+  st.pos = 4;
+  memcpy(out_host, &st, sizeof st);
+  return 0;
+}
+
+int sfg_plan_seq(const sfg_program* p, const sfg_corpus_dev* c, int64_t it0, int n, const void* state,
+                 const uint64_t* counts_base, void* children, void* vals, uint32_t* int_flags, void* states,
+                 void* stream) {
+  if (n <= 0) return 0;
+  sfg_plan_seq_kernel<<<1, 32, 0, S(stream)>>>(p->P, CV(c), it0, n, (const SfgStream*)state, counts_base,
+                                                (sfg_child*)children, (sfg_val*)vals, int_flags, (SfgStream*)states);
+  SFG_CHECK_LAUNCH("sfg_plan_seq");
+  return 0;
+}
+
 int sfg_mutate(const sfg_program* p, const sfg_corpus_dev* c, int64_t it0, int n, const uint64_t* counts_prefix,
                const uint64_t* counts_base, void* children, void* vals, void* stream) {
   if (n <= 0) return 0;

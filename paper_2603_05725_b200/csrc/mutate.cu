@@ -320,16 +320,16 @@ extern "C" __global__ void sfg_plan_kernel(sfg_prog P, CorpusView C, int64_t it0
 }
 
 // counts_prefix[i][c]: rotation count of int column c seen by input i
-extern "C" __global__ void __launch_bounds__(128, 8) sfg_mutate_kernel(sfg_prog P, CorpusView C, int64_t it0, int n,
-                                             const uint64_t* counts_prefix, const uint64_t* counts_base,
-                                             sfg_child* child_out, sfg_val* vals_out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int64_t it = it0 + i;
-  sfg_child ch;
+// One child of the mutation stage (mutation.py:499-518 mutate_testcase + the
+// work layout): parent pick, picks, op generation, descriptor-level apply, child
+// values written once.  s: the input's Philox stream (its own in the batched
+// contract, the worker's in the sequential one); cnt_of[c]: MutationSchedule
+// rotation count of int column c as this input sees it; picks out.
+__device__ __forceinline__ void mutate_child(const sfg_prog& P, const CorpusView& C, int64_t it, SfgStream& s,
+                                             const uint64_t* cnt_of, int8_t* picks, sfg_child& ch,
+                                             sfg_val* vout) {
   memset(&ch, 0, sizeof(ch));
   ch.it = it;
-  sfg_val* vout = vals_out + (size_t)i * P.n_args;
   const sfg_val* pv = C.vals;             // parent values (the seed for it == 1)
   // picked args: the mutated value goes straight to vout; its kind / materialized
   // size / nbytes stay in registers for the layout pass
@@ -341,10 +341,7 @@ extern "C" __global__ void __launch_bounds__(128, 8) sfg_mutate_kernel(sfg_prog 
     ch.parent = -1;
     ch.rng_seed = C.meta[0].rng_seed;
   } else {
-    SfgStream s;
-    s.init(P.master_seed, P.keybase + (uint64_t)it);
     const int parent = pick_parent(s, P, C, it);
-    int8_t picks[SFG_MAX_OPS] = {-1, -1, -1};
     const int n_ops = draw_picks(s, P, picks);
     ch.parent = parent;
     ch.n_ops = n_ops;
@@ -356,8 +353,7 @@ extern "C" __global__ void __launch_bounds__(128, 8) sfg_mutate_kernel(sfg_prog 
       op.arg = (uint8_t)a;
       sfg_val v = pv[a];
       if (v.kind == SFG_V_I32) {  // MutationSchedule.next_int_op (mutation.py:378-386)
-        const int c = P.int_slot[a];
-        const uint64_t cnt = counts_base[c] + counts_prefix[(size_t)i * P.n_int_args + c];
+        const uint64_t cnt = cnt_of[P.int_slot[a]];
         if (cnt < 3) {
           op.kind = SFG_M_INT_BOUNDARY;
           op.sub = (uint8_t)cnt;
@@ -413,7 +409,53 @@ extern "C" __global__ void __launch_bounds__(128, 8) sfg_mutate_kernel(sfg_prog 
   }
   ch.work_bytes = off + (uint64_t)P.named_work_bytes;
   ch.readout_bytes = rb;
+  ch.readout_bytes = rb;
+}
+
+extern "C" __global__ void __launch_bounds__(128, 8) sfg_mutate_kernel(sfg_prog P, CorpusView C, int64_t it0, int n,
+                                             const uint64_t* counts_prefix, const uint64_t* counts_base,
+                                             sfg_child* child_out, sfg_val* vals_out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t it = it0 + i;
+  uint64_t cnt[8];
+  for (int c = 0; c < P.n_int_args && c < 8; ++c) cnt[c] = counts_base[c] + counts_prefix[(size_t)i * P.n_int_args + c];
+  SfgStream s;
+  s.init(P.master_seed, P.keybase + (uint64_t)it);
+  int8_t picks[SFG_MAX_OPS] = {-1, -1, -1};
+  sfg_child ch;
+  mutate_child(P, C, it, s, cnt, picks, ch, vals_out + (size_t)i * P.n_args);
   child_out[i] = ch;
+}
+
+// The reference fuzz_loop's own stream discipline (campaign.py:714-749): one worker
+// stream Stream(master_seed, 1000 + w) and one MutationSchedule consumed input after
+// input.  A single thread generates the round's children in order from the worker
+// state (*state), saving the state before every input (states[0..n]) and the
+// int-arg picks (flags, as sfg_plan) so the host can cut the round after an
+// admission and resume exactly there.  Rotation counts start from counts_base.
+extern "C" __global__ void sfg_plan_seq_kernel(sfg_prog P, CorpusView C, int64_t it0, int n, const SfgStream* state,
+                                               const uint64_t* counts_base, sfg_child* child_out, sfg_val* vals_out,
+                                               uint32_t* flags_out, SfgStream* states) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  SfgStream s = *state;
+  uint64_t cnt[8];
+  for (int c = 0; c < P.n_int_args && c < 8; ++c) cnt[c] = counts_base[c];
+  for (int i = 0; i < n; ++i) {
+    states[i] = s;
+    const int64_t it = it0 + i;
+    int8_t picks[SFG_MAX_OPS] = {-1, -1, -1};
+    sfg_child ch;
+    mutate_child(P, C, it, s, cnt, picks, ch, vals_out + (size_t)i * P.n_args);
+    child_out[i] = ch;
+    for (int c = 0; c < P.n_int_args; ++c) flags_out[(size_t)i * P.n_int_args + c] = 0;
+    for (int k = 0; k < SFG_MAX_OPS; ++k)
+      if (picks[k] >= 0 && P.int_slot[picks[k]] >= 0) {
+        flags_out[(size_t)i * P.n_int_args + P.int_slot[picks[k]]] = 1;
+        ++cnt[P.int_slot[picks[k]]];
+      }
+  }
+  states[n] = s;
 }
 
 // warp per input: parent payloads -> child work region (materialized contents)

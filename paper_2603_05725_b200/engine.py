@@ -128,6 +128,8 @@ class Slot:
         self.counter = i32(8)            # work counters of this slot's execute launches
         self.deferred = i32(2 * cap)     # tail-pass lists: soft-cap deferrals, sequential re-runs
         self.order = i32(cap)            # bulk-pass schedule (sfg_order)
+        # sequential discipline: worker stream state before every input and after the last
+        self.states = u8((cap + 1) * dc.state_bytes) if dc.sequential else None
         self.order_scratch = i32(int(dc.L.sfg_order_scratch_ints(cap)))
         # triage partials (merged across ranks between the phases, sfg.h):
         # MIN: [stop, fatal, first_hit[E], key_first[K]]; SUM: [edge_delta[E], key_count[K], entered[16]]
@@ -165,12 +167,18 @@ class DeviceCampaign:
                  mutation: MutationConfig | None = None, budget=1_000_000, window=256, recent_weight=4.0,
                  diff_readback=False, stop_on_first_finding=False, stop_bug_class=None, device=None,
                  extra_seeds=(), ids_reset_per_input=False, comm: RoundComm | None = None,
-                 soft_cap: int | None = None, ctx_map_bits: int = 0, fanout: int = 0):
+                 soft_cap: int | None = None, ctx_map_bits: int = 0, fanout: int = 0, sequential: bool = False):
         if not torch.cuda.is_available():
             raise _native.NativeError("no CUDA device: the fuzzing inner loop runs only on the GPU")
         self.L = _native.lib()
         self.dev = torch.device(device or "cuda")
         self.comm = comm or RoundComm()
+        # sequential: the reference fuzz_loop's own stream discipline (one worker stream,
+        # rounds cut after each admission) instead of the batched-round contract
+        self.sequential = bool(sequential)
+        self.state_bytes = int(self.L.sfg_stream_state_bytes())
+        if self.sequential and (self.comm.world > 1 or fanout):
+            raise LoweringError("the sequential discipline runs on one device without fan-out")
         if soft_cap is None:
             soft_cap = int(os.environ.get("SFG_SOFT_CAP", DEFAULT_SOFT_CAP))
         self.soft_cap = soft_cap
@@ -219,6 +227,8 @@ class DeviceCampaign:
         self.ghit = torch.zeros(max(self.E, 1), dtype=torch.uint8, device=self.dev)
         self.entered = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.counts_run = torch.zeros(max(self.C, 1), dtype=torch.int64, device=self.dev)
+        self.seq_state = torch.zeros(self.state_bytes, dtype=torch.uint8, device=self.dev)
+        self._set_worker_stream(0)
         # context-sensitive hashed coverage map (derived view, csrc/ctxmap.cu)
         self.ctx_bits = int(ctx_map_bits)
         if self.ctx_bits:
@@ -315,13 +325,22 @@ class DeviceCampaign:
         _native.check(self.L.sfg_scan_u64(src.data_ptr(), n, stride, col, out.data_ptr(), 1, 0, S.tmp.data_ptr(),
                                           S.tot.data_ptr() + 8 * total_slot, S.stream.cuda_stream), "scan")
 
-    def new_worker(self):
+    def _set_worker_stream(self, w: int):
+        """Worker w's stream Stream(master_seed, 1000 + w) (campaign.py:714)."""
+        buf = (ctypes.c_uint8 * self.state_bytes)()
+        self.L.sfg_stream_state_init(self.master_seed & ((1 << 64) - 1), 1000 + w, buf)
+        self.seq_state.copy_(torch.frombuffer(bytearray(buf), dtype=torch.uint8))
+
+    def new_worker(self, w: int = 0):
         """Reference workers (campaign.py:712-730) get a fresh MutationSchedule and a fresh
-        image: rotation counts and alloc ids restart; corpus/findings/coverage are shared."""
+        image: rotation counts and alloc ids restart; corpus/findings/coverage are shared.
+        Sequential discipline: the worker's own stream too."""
         self.drain()
         self.counts_run.zero_()
         self._last_counts = None
         self.next_alloc_id = self.base.next_id
+        if self.sequential:
+            self._set_worker_stream(w)
 
     def drain(self):
         torch.cuda.synchronize(self.dev)
@@ -340,6 +359,9 @@ class DeviceCampaign:
         it0, n = S.it0, S.n
         cd = self.corpus_dev()
         C = self.C
+        if self.sequential:
+            self._submit_sequential(S, cd)
+            return
         if self.timing:
             S.sub_ev = torch.cuda.Event(enable_timing=True)
             S.sub_ev.record(st)
@@ -374,6 +396,35 @@ class DeviceCampaign:
             S.readouts = self._u8(int(S.tot[1].item()) + 16)
         else:
             S.readouts = None
+        _native.check(L.sfg_apply(hp, ctypes.byref(cd), n, S.children.data_ptr(), S.vals.data_ptr(),
+                                  S.work_base.data_ptr(), S.work.data_ptr(), s), "apply")
+        self._execute(S, n, self.soft_cap, cd)
+
+    def _submit_sequential(self, S: Slot, cd):
+        """Children of the round from the worker stream, one after another (sfg_plan_seq),
+        then the same layout scan, payloads and execute as the batched path."""
+        L, hp, st = self.L, self.h, S.stream
+        s = st.cuda_stream
+        it0, n = S.it0, S.n
+        if it0 + n - 1 >= 2 and self.low.prog["n_mutable"] == 0:
+            raise MutationError("no mutable arguments")
+        with torch.cuda.stream(st):
+            if self._last_done is not None:     # the previous round's cut fixes our start
+                st.wait_event(self._last_done)
+            S.counts_base.copy_(self.counts_run)
+        self.launches += 1
+        _native.check(L.sfg_plan_seq(hp, ctypes.byref(cd), it0, n, self.seq_state.data_ptr(),
+                                     S.counts_base.data_ptr(), S.children.data_ptr(), S.vals.data_ptr(),
+                                     S.flags.data_ptr(), S.states.data_ptr(), s), "plan_seq")
+        cw = CHILD.itemsize // 8
+        self._scan64(S, S.children.view(torch.int64), n, cw, CHILD.fields["work_bytes"][1] // 8, S.work_base, 0)
+        S.ensure_work(n * self.max_entry_work + 64, self.dev)
+        S.readouts = None
+        if self.diff:
+            self._scan64(S, S.children.view(torch.int64), n, cw, CHILD.fields["readout_bytes"][1] // 8, S.ro_base, 1)
+            with torch.cuda.stream(st):
+                S.tot[:2].cpu()
+            S.readouts = self._u8(int(S.tot[1].item()) + 16)
         _native.check(L.sfg_apply(hp, ctypes.byref(cd), n, S.children.data_ptr(), S.vals.data_ptr(),
                                   S.work_base.data_ptr(), S.work.data_ptr(), s), "apply")
         self._execute(S, n, self.soft_cap, cd)
@@ -424,31 +475,28 @@ class DeviceCampaign:
             self.exec_events.append((ev[0], getattr(S, "bulk_ev", None) if tail else None, ev[1]))
 
     # ---- finalize: triage in order ------------------------------------------------------
-    def _finalize(self, S: Slot) -> RoundResult:
-        """Triage one round: stop -> [MIN] -> absorb -> [MIN, SUM] -> admit ->
-        scans -> [gather] -> corpus append, map commit, findings (sfg.h)."""
+    def _triage_pass(self, S: Slot, cut=None):
+        """stop -> [MIN] -> absorb -> [MIN, SUM] -> admit -> scans -> [gather], read
+        back to the host.  cut: round index after which inputs are discarded (the
+        sequential discipline's cut after an admission), applied as a stop."""
         L, hp, st, comm = self.L, self.h, S.stream, self.comm
         s = st.cuda_stream
         n, ib = S.n, S.i_base
         self.launches += 7
         with torch.cuda.stream(st):
-            if self._last_done is not None:
-                st.wait_event(self._last_done)
             S.mins.fill_(NONE)
             S.sums.zero_()
         vp, ep = S.verdicts.data_ptr(), S.ecnt.data_ptr()
         _native.check(L.sfg_triage_stop(hp, n, ib, vp, S.scalars.data_ptr(), s), "triage_stop")
         comm.all_reduce(S.scalars, "min", st)
+        if cut is not None:
+            with torch.cuda.stream(st):
+                S.scalars[:1].clamp_(max=cut)
         _native.check(L.sfg_triage_absorb(hp, n, ib, vp, ep, S.scalars.data_ptr(), S.first.data_ptr(),
                                           S.edelta.data_ptr(), S.kfirst.data_ptr(), S.kcount.data_ptr(),
                                           S.ent.data_ptr(), S.allocs.data_ptr(), s), "triage_absorb")
         comm.all_reduce(S.mins[2:], "min", st)
         comm.all_reduce(S.sums, "sum", st)
-        if self.ctx_bits:
-            self.launches += 1
-            _native.check(L.sfg_ctxmap(n, self.E, ib, ep, S.scalars.data_ptr(), self.edge_ctx.data_ptr(),
-                                       self.ctx_map.data_ptr(), self.ctx_bits, self.ctx_new.data_ptr(), s), "ctxmap")
-            comm.all_reduce(self.ctx_map, "max", st)
         _native.check(L.sfg_triage_admit(hp, n, ib, vp, ep, S.children.data_ptr(), S.scalars.data_ptr(),
                                          S.first.data_ptr(), self.ghit.data_ptr(), S.admit.data_ptr(), s),
                       "triage_admit")
@@ -467,12 +515,41 @@ class DeviceCampaign:
             ev.record(st)
         ev.synchronize()
         stop, fatal = (int(x) for x in S.pin_sc.numpy())
-        gathered = S.pin_gath.numpy().copy()
+        return stop, fatal, S.pin_gath.numpy().copy()
+
+    def _finalize(self, S: Slot) -> RoundResult:
+        """Triage one round (sfg.h): the triage pass, then corpus append, map commit,
+        findings.  Sequential discipline: a round whose first admission is not its
+        last executed input is triaged again, cut right after that admission (the
+        later inputs were generated from the pre-admission corpus)."""
+        L, hp, st, comm = self.L, self.h, S.stream, self.comm
+        s = st.cuda_stream
+        ib = S.i_base
+        with torch.cuda.stream(st):
+            if self._last_done is not None:
+                st.wait_event(self._last_done)
+        stop, fatal, gathered = self._triage_pass(S)
+        N = S.round_n
+        cut = None
+        if self.sequential and int(gathered[:, 0].sum()):
+            executed0 = N if stop == NONE else stop + 1
+            adm = _np(S.admit[:S.n], np.int64)
+            first = int(np.argmax(adm != 0))
+            if first < executed0 - 1:
+                cut = first
+                stop, fatal, gathered = self._triage_pass(S, cut=cut)
         if fatal != NONE and fatal <= stop:
             self._raise_fatal(S, fatal)
-        N = S.round_n
         executed = N if stop == NONE else stop + 1
+        if cut is not None and stop == cut:
+            stop = NONE        # a cut is not a campaign stop
         S.executed = max(0, min(S.n, executed - ib))
+        if self.ctx_bits:
+            self.launches += 1
+            _native.check(L.sfg_ctxmap(S.n, self.E, ib, S.ecnt.data_ptr(), S.scalars.data_ptr(),
+                                       self.edge_ctx.data_ptr(), self.ctx_map.data_ptr(), self.ctx_bits,
+                                       self.ctx_new.data_ptr(), s), "ctxmap")
+            comm.all_reduce(self.ctx_map, "max", st)
         n_adm = int(gathered[:, 0].sum())
         self._round_id0 = self.next_alloc_id
         S.alloc_base = self.next_alloc_id + int(gathered[:comm.rank, 1].sum())
@@ -482,6 +559,13 @@ class DeviceCampaign:
                                    self.ghit.data_ptr(), self.entered.data_ptr(), s), "commit")
         new_keys = self._absorb_findings(S)
         self.next_alloc_id += int(gathered[:, 1].sum())
+        if self.sequential:
+            # the worker stream and the rotation counts resume after the last kept input
+            k = S.executed
+            with torch.cuda.stream(st):
+                self.seq_state.copy_(S.states[k * self.state_bytes:(k + 1) * self.state_bytes])
+                if self.C and k:
+                    self.counts_run[:self.C] += S.flags[:k * self.C].view(k, self.C).sum(0).to(torch.int64)
         S.ev_done.record(st)
         self._last_done = S.ev_done
         self.rounds += 1
@@ -613,6 +697,25 @@ class DeviceCampaign:
             return out
 
     # ---- public round API --------------------------------------------------------------
+    def _run_rounds_sequential(self, it0, it_stop, round_size, on_round, should_continue):
+        """Sequential discipline: one round at a time, each starting right after the
+        previous round's last kept input (a cut after an admission, or its end)."""
+        results = []
+        it = it0
+        self.reserve(1, min(round_size, max(it_stop - it0, 1)))
+        while it < it_stop and (should_continue is None or should_continue()):
+            n = min(round_size, it_stop - it)
+            S = self._slot(0, n)
+            self._submit(S, it, n, self.rounds)
+            res = self._finalize(S)
+            results.append(res)
+            if on_round is not None:
+                on_round(res)
+            if res.stop is not None:
+                break
+            it += res.executed
+        return results
+
     def reserve(self, depth: int, round_size: int) -> None:
         """Allocate the device buffers of ``depth`` rounds of ``round_size`` inputs
         (and their work arenas for the current corpus) ahead of a pipelined run."""
@@ -635,6 +738,8 @@ class DeviceCampaign:
         finalized and nothing more is submitted.  The pipeline stays full across the
         whole range, so a long campaign is one call.  Returns the list of RoundResults
         (stops early on a stop)."""
+        if self.sequential:
+            return self._run_rounds_sequential(it0, it_stop, round_size, on_round, should_continue)
         plan = []
         it = it0
         while it < it_stop:

@@ -336,3 +336,27 @@ def test_fatal_conditions_raise_reference_exceptions(engine_cls, case):
         fuzz_loop(m, CampaignConfig(master_seed=11, iterations=8, mem_config=MemConfig(**c["mem"])))
     assert type(ei.value).__name__ == c["raises"]
     assert str(ei.value) == c["message"]
+
+
+@pytest.mark.parametrize("key", sorted(golden("ref_fuzzloop.json")))
+@pytest.mark.parametrize("round_size", [64, 4096])
+def test_sequential_fuzz_loop_matches_reference_output_dir(engine_cls, key, round_size, tmp_path):
+    """discipline="sequential": the reference fuzz_loop's own semantics (one worker
+    stream, live corpus; rounds generated in order on the device and cut after each
+    admission).  The output directory equals the reference fuzz_loop's
+    (tests/golden/ref_fuzzloop.json, made by the reference): findings.txt,
+    coverage.rec / coverage.txt, corpus and crash file names (sha256 test-case ids),
+    summary.rec -- whatever the round size."""
+    from paper_2603_05725_b200.campaign import CampaignConfig, fuzz_loop
+    name, seed, iters = key.split("/")
+    want = golden("ref_fuzzloop.json")[key]
+    d = tmp_path / "out"
+    s = fuzz_loop(bench_manifest(name), CampaignConfig(master_seed=int(seed), iterations=int(iters), out_dir=d,
+                                                       discipline="sequential", round_size=round_size,
+                                                       **want["kw"]))
+    assert (d / "findings.txt").read_text() == want["findings"]
+    assert (d / "coverage.rec").read_text() == want["coverage_rec"]
+    assert (d / "coverage.txt").read_text() == want["coverage_txt"]
+    assert sorted(p.name for p in (d / "corpus").iterdir()) == want["corpus"]
+    assert sorted(p.name for p in (d / "crashes").iterdir()) == want["crashes"]
+    assert s.to_rec() == want["summary"]
