@@ -162,10 +162,14 @@ struct Gen {
     const std::string W_s = std::to_string(W), SP = std::to_string(x.space);
     // fast path: tagged live own record of the declared space, access inside its payload
     // and naturally aligned in the work region (phys offsets are 16-aligned)
+    // (pk<q>_<space>_<W> and pl<q>_<W> are loop-invariant: the payload holds a
+    // W-byte access and its last valid offset, computed once per simulated thread)
     auto fast = [&](int q) {
       const std::string Q = std::to_string(q);
-      return "(pk" + Q + "_" + SP + " && (i128)lo_ == A_ && (uint64_t)(lo_ - pb" + Q + ") <= (uint64_t)(psz" + Q + " - " +
-             W_s + ") && psz" + Q + " >= " + W_s + " && ((lo_ - pb" + Q + ") & " + std::to_string(W - 1) + ") == 0)";
+      std::string c = "(pk" + Q + "_" + SP + "_" + W_s + " && (i128)lo_ == A_ && (uint64_t)(lo_ - pb" + Q + ") <= pl" +
+                      Q + "_" + W_s;
+      if (W > 1) c += " && ((lo_ - pb" + Q + ") & " + std::to_string(W - 1) + ") == 0";
+      return c + ")";
     };
     auto fast_body = [&](int q) {
       const std::string Q = std::to_string(q);
@@ -357,6 +361,15 @@ struct Gen {
         << " = (R_.flags & (R_RES | R_FREED | R_BASE)) == R_RES; pp" << Q << " = M.work + R_.phys; pw" << Q << " = R_.phys; }\n";
       o << "  const bool pk" << Q << "_0 = pok" << Q << " && psp" << Q << " == 0, pk" << Q << "_1 = pok" << Q << " && psp"
         << Q << " == 1, pk" << Q << "_2 = pok" << Q << " && psp" << Q << " == 2;\n";
+      // per access width: last valid payload offset, and "the payload holds W bytes"
+      // folded into the space flags (unused combinations are dead code)
+      for (int W : {1, 2, 4, 8}) {
+        const std::string Ws = std::to_string(W);
+        o << "  const uint64_t pl" << Q << "_" << Ws << " = (uint64_t)(psz" << Q << " - " << Ws << ");\n";
+        for (int sp = 0; sp < 3; ++sp)
+          o << "  const bool pk" << Q << "_" << sp << "_" << Ws << " = pk" << Q << "_" << sp << " && psz" << Q
+            << " >= " << Ws << ";\n";
+      }
     }
     // Retired-budget checks.  The fast copy of a block retires its instructions
     // without per-instruction checks; the budget (or soft cap / poll limit) is tested
