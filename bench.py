@@ -188,7 +188,8 @@ def run_ours(a):
         h0 = time.perf_counter()
         t0.record()
         results = dc.run_rounds(it, it + a.steps * R, R, depth=D,
-                                on_round=lambda res: fin.append((time.perf_counter() - h0, res.n_admitted)))
+                                on_round=lambda res: fin.append((time.perf_counter() - h0, res.n_admitted,
+                                                                 getattr(res.slot, "sub_host", h0) - h0)))
         all_streams_done(t1)
         torch.cuda.synchronize()
     it += a.steps * R
@@ -241,9 +242,10 @@ def run_ours(a):
     # campaign's buffers go back to the allocator first)
     if os.environ.get("SFG_BENCH_TIMELINE"):
         with open(os.environ["SFG_BENCH_TIMELINE"], "w") as f:
-            for k, ((s_, b_, e_), (h, adm)) in enumerate(zip(dc.exec_events, fin)):
+            for k, ((s_, b_, e_), (h, adm, sub)) in enumerate(zip(dc.exec_events, fin)):
                 f.write(f"{k} exec_start {t0.elapsed_time(s_):.1f} bulk_end {t0.elapsed_time(b_):.1f} "
-                        f"tail_end {t0.elapsed_time(e_):.1f} host_final {h * 1e3:.1f} admitted {adm}\n")
+                        f"tail_end {t0.elapsed_time(e_):.1f} host_final {h * 1e3:.1f} admitted {adm} "
+                        f"host_submit {sub * 1e3:.1f}\n")
     dc.close()
     dc.slots.clear()
     dc._aux = None
