@@ -53,12 +53,14 @@ def _cpu_worker(args):
     return done, time.perf_counter() - t0
 
 
-def cpu_rate(workload: str, seconds: float, procs: int | None = None):
+def cpu_rate(workload: str, seconds: float, procs: int | None = None, pool=None):
     import multiprocessing as mp
     procs = procs or os.cpu_count() or 1
-    ctx = mp.get_context("fork")
     t0 = time.perf_counter()
-    with ctx.Pool(procs) as pool:
+    if pool is None:
+        with mp.get_context("fork").Pool(procs) as pl:
+            out = pl.map(_cpu_worker, [(workload, 11 + i, seconds) for i in range(procs)])
+    else:
         out = pool.map(_cpu_worker, [(workload, 11 + i, seconds) for i in range(procs)])
     wall = time.perf_counter() - t0
     execs = sum(d for d, _ in out)
@@ -69,21 +71,27 @@ def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    import multiprocessing as mp
     per_step = []
     total_execs = 0
     procs = os.cpu_count() or 1
-    for s in range(a.warmup + a.steps):
-        rate, execs, wall, procs = cpu_rate(a.workload, a.ref_seconds, procs)
-        if s >= a.warmup:
-            per_step.append(wall)
-            total_execs += execs
+    # each step is a bounded sample: the whole --steps K --warmup W run stays within
+    # ~120 s of CPU time per process (1-10 s per step; a step ends at the first
+    # 64-input chunk past its time), one process pool throughout
+    sec = a.ref_seconds if a.ref_seconds else min(10.0, max(1.0, 120.0 / (a.steps + a.warmup)))
+    with mp.get_context("fork").Pool(procs) as pool:
+        for s in range(a.warmup + a.steps):
+            rate, execs, wall, procs = cpu_rate(a.workload, sec, procs, pool)
+            if s >= a.warmup:
+                per_step.append(wall)
+                total_execs += execs
     value = total_execs / sum(per_step)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1000 * statistics.mean(per_step),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "i32/f32",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "sample": f"{a.ref_seconds}s per process per step"},
+            "data": "synthetic", "config": {"workload": WORKLOAD, "sample": f"{sec:.2f}s per process per step"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
-                             "sample": f"oracle batched loop, {procs} processes x {a.ref_seconds}s per step"},
+                             "sample": f"oracle batched loop, {procs} processes x {sec:.2f}s per step"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
@@ -321,7 +329,8 @@ def main():
     p.add_argument("--workload", default="matmul")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--cpu-seconds", type=float, default=15.0)
-    p.add_argument("--ref-seconds", type=float, default=10.0)
+    p.add_argument("--ref-seconds", type=float, default=0.0,
+                   help="seconds per process per reference step (default: 120 s / (steps + warmup), 1-10 s)")
     p.add_argument("--no-cpu", action="store_true")
     a = p.parse_args()
     if a.impl == "reference":
