@@ -204,8 +204,9 @@ def _edges_of(delta: CoverageMap):
 def run_loop(manifest, *, master_seed=1, iterations=1000, batched=True, round_size=256,
              stop_on_first_finding=False, stop_bug_class=None, budget=1_000_000,
              mem_cfg: MemCfg | None = None, max_ops=3, granule=4, redzone=32,
-             window=256, weight=4.0, keep_records=True, extra_seeds=(), fanout=0):
-    """Shared body of ``sequential_loop`` / ``batched_loop``."""
+             window=256, weight=4.0, keep_records=True, extra_seeds=(), fanout=0, on_exec=None):
+    """Shared body of ``sequential_loop`` / ``batched_loop``.  ``on_exec()``
+    (bench CPU baseline only) is called after every input; True stops the loop."""
     specs = manifest.argspecs
     res = OracleCampaign()
     gcov = CoverageMap.for_program(manifest.program)
@@ -277,6 +278,9 @@ def run_loop(manifest, *, master_seed=1, iterations=1000, batched=True, round_si
             res.records.append(rec)
         if stop:
             res.stop_reason = stop
+            break
+        if on_exec is not None and on_exec():
+            res.stop_reason = "on_exec"
             break
     return res
 

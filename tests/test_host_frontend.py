@@ -193,3 +193,20 @@ def test_control_taint_mask():
     assert "n" in amax and "x" in amax
     # copy only bounds its loop by n
     assert _control_args(bench_manifest("copy")) == {"n"}
+
+
+def test_bench_reference_arm_cpu():
+    """bench.py --impl reference: the CPU port of the reference loop on the bench
+    workload in clock-bounded windows; one JSON line with the contract's keys."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "2", "--warmup", "1",
+                          "--ref-seconds", "1"], cwd=root, capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "execs/s"
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and 900 <= line["ms_per_step"] <= 1500
