@@ -323,10 +323,12 @@ extern "C" __global__ void sfg_plan_kernel(sfg_prog P, CorpusView C, int64_t it0
 // One child of the mutation stage (mutation.py:499-518 mutate_testcase + the
 // work layout): parent pick, picks, op generation, descriptor-level apply, child
 // values written once.  s: the input's Philox stream (its own in the batched
-// contract, the worker's in the sequential one); cnt_of[c]: MutationSchedule
-// rotation count of int column c as this input sees it; picks out.
+// contract, the worker's in the sequential one); cnt_of[c] + (cnt_pre ? cnt_pre[c] : 0):
+// MutationSchedule rotation count of int column c as this input sees it (read
+// where a pick needs it: no per-thread array); picks out.
 __device__ __forceinline__ void mutate_child(const sfg_prog& P, const CorpusView& C, int64_t it, SfgStream& s,
-                                             const uint64_t* cnt_of, int8_t* picks, sfg_child& ch,
+                                             const uint64_t* cnt_of, const uint64_t* cnt_pre, int8_t* picks,
+                                             sfg_child& ch,
                                              sfg_val* vout) {
   memset(&ch, 0, sizeof(ch));
   ch.it = it;
@@ -353,7 +355,8 @@ __device__ __forceinline__ void mutate_child(const sfg_prog& P, const CorpusView
       op.arg = (uint8_t)a;
       sfg_val v = pv[a];
       if (v.kind == SFG_V_I32) {  // MutationSchedule.next_int_op (mutation.py:378-386)
-        const uint64_t cnt = cnt_of[P.int_slot[a]];
+        const int c = P.int_slot[a];
+        const uint64_t cnt = cnt_of[c] + (cnt_pre ? cnt_pre[c] : 0ull);
         if (cnt < 3) {
           op.kind = SFG_M_INT_BOUNDARY;
           op.sub = (uint8_t)cnt;
@@ -418,13 +421,12 @@ extern "C" __global__ void __launch_bounds__(128, 8) sfg_mutate_kernel(sfg_prog 
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int64_t it = it0 + i;
-  uint64_t cnt[8];
-  for (int c = 0; c < P.n_int_args && c < 8; ++c) cnt[c] = counts_base[c] + counts_prefix[(size_t)i * P.n_int_args + c];
   SfgStream s;
   s.init(P.master_seed, P.keybase + (uint64_t)it);
   int8_t picks[SFG_MAX_OPS] = {-1, -1, -1};
   sfg_child ch;
-  mutate_child(P, C, it, s, cnt, picks, ch, vals_out + (size_t)i * P.n_args);
+  mutate_child(P, C, it, s, counts_base, counts_prefix + (size_t)i * P.n_int_args, picks, ch,
+               vals_out + (size_t)i * P.n_args);
   child_out[i] = ch;
 }
 
@@ -446,7 +448,7 @@ extern "C" __global__ void sfg_plan_seq_kernel(sfg_prog P, CorpusView C, int64_t
     const int64_t it = it0 + i;
     int8_t picks[SFG_MAX_OPS] = {-1, -1, -1};
     sfg_child ch;
-    mutate_child(P, C, it, s, cnt, picks, ch, vals_out + (size_t)i * P.n_args);
+    mutate_child(P, C, it, s, cnt, nullptr, picks, ch, vals_out + (size_t)i * P.n_args);
     child_out[i] = ch;
     for (int c = 0; c < P.n_int_args; ++c) flags_out[(size_t)i * P.n_int_args + c] = 0;
     for (int k = 0; k < SFG_MAX_OPS; ++k)

@@ -49,7 +49,13 @@ struct SfgStream {
   }
 
   __device__ __forceinline__ uint64_t next64() {
-    if (pos < 4) return buf[pos++];
+    if (pos < 4) {
+      // constant indices only: the buffer stays in registers (buf[pos] would put
+      // the whole stream state in local memory)
+      const uint64_t v = pos == 0 ? buf[0] : pos == 1 ? buf[1] : pos == 2 ? buf[2] : buf[3];
+      ++pos;
+      return v;
+    }
     if (++ctr[0] == 0 && ++ctr[1] == 0 && ++ctr[2] == 0) ++ctr[3];
     block();
     pos = 1;
