@@ -284,6 +284,17 @@ def run_ours(a):
              "ncu_warp_cycles_per_issued": prof.get("warp_cycles_per_issued"),
              "ncu_active_threads_per_warp": prof.get("active_threads_per_warp"),
              "lane_instr_peak_per_s": 148 * 4 * 32 * sm_mhz * 1e6}
+    # the long-input pass (sfg_jit_tail): most of the serialized kernel time, few SMs
+    # at a time; same issue/latency bound (ncu figures of one launch run alone)
+    tf = REPO / "profiles" / "r01_ncu_tail_execute.json"
+    tprof = json.loads(tf.read_text()) if tf.exists() else {}
+    issue["tail_pass"] = {"kernel": "sfg_jit_tail", "ms_per_round_after_bulk": statistics.mean(
+        e - b for e, b in zip(k3_ms, bulk_ms)) if bulk_ms else None,
+        "ncu_duration_ms_alone": (tprof.get("duration_ns") or 0) / 1e6 or None,
+        "ncu_issue_slots_busy_pct": tprof.get("issue_slots_busy_pct"),
+        "ncu_warp_cycles_per_issued": tprof.get("warp_cycles_per_issued"),
+        "ncu_achieved_warps_per_sm": tprof.get("achieved_warps_per_sm"),
+        "ncu_dram_bytes_per_launch": tprof.get("dram_bytes_per_launch")}
 
     # ---- end to end through the public API with host buffers (the device-timed
     # campaign's buffers go back to the allocator first)
