@@ -149,7 +149,10 @@ struct Gen {
   void emit_mem(const sfg_ins& x, int kidx, int iid, int j, bool slow, int tag) {
     const int W = x.width;
     const bool st = x.op == SFG_ST;
-    o << "    { const i128 A_ = " << a(x.s1) << " + (i128)" << i64lit(x.imm2) << "; const int64_t lo_ = (int64_t)A_;\n";
+    if (narrow)   // 64-bit pointer registers (see narrow_ok): the address is exact in int64
+      o << "    { const int64_t lo_ = " << a(x.s1) << " + " << i64lit(x.imm2) << "; const i128 A_ = (i128)lo_;\n";
+    else
+      o << "    { const i128 A_ = " << a(x.s1) << " + (i128)" << i64lit(x.imm2) << "; const int64_t lo_ = (int64_t)A_;\n";
     std::string val;
     if (st) {
       if (x.mode == SFG_MK_F32) val = (x.flags & SFG_F_S2_IMM) ? std::string("(uint64_t)") + u32lit(x.imm1) : "(uint64_t)" + f(x.s2);
@@ -166,8 +169,8 @@ struct Gen {
     // W-byte access and its last valid offset, computed once per simulated thread)
     auto fast = [&](int q) {
       const std::string Q = std::to_string(q);
-      std::string c = "(pk" + Q + "_" + SP + "_" + W_s + " && (i128)lo_ == A_ && (uint64_t)(lo_ - pb" + Q + ") <= pl" +
-                      Q + "_" + W_s;
+      std::string c = "(pk" + Q + "_" + SP + "_" + W_s + (narrow ? "" : " && (i128)lo_ == A_") + " && (uint64_t)(lo_ - pb" +
+                      Q + ") <= pl" + Q + "_" + W_s;
       if (W > 1) c += " && ((lo_ - pb" + Q + ") & " + std::to_string(W - 1) + ") == 0";
       return c + ")";
     };
@@ -213,13 +216,38 @@ struct Gen {
     }
     if (!st) {
       if (x.mode == SFG_MK_F32) o << "      " << f(x.dst) << " = sfg_quiet((uint32_t)v_);\n";
-      else if (x.mode == SFG_MK_B64) o << "      " << a(x.dst) << " = (i128)(uint64_t)v_; " << t(x.dst) << " = 0;\n";
+      else if (x.mode == SFG_MK_B64) o << "      " << a(x.dst) << " = (" << AT() << ")(uint64_t)v_; " << t(x.dst) << " = 0;\n";
       else o << "      " << r(x.dst) << " = (uint32_t)v_;\n";
     }
     o << "    }\n";
   }
 
   int cur_na = 0;
+  // Pointer registers hold unbounded integers in the reference (executor.py:297-310).
+  // A kernel whose pointer registers only ever receive pointer parameters
+  // (simulated addresses, < 2^40), small immediates and sums with i32 registers or
+  // immediates below 2^31 stays below 2^40 + budget * 2^31 < 2^62 in magnitude
+  // for budgets below 2^30: such kernels ("narrow") keep them in int64 and drop
+  // the 128-bit arithmetic and high-word checks.  A 64-bit load into a pointer
+  // register (values up to 2^64) or any larger immediate keeps the 128-bit form.
+  bool narrow = false;
+  std::string AT() const { return narrow ? "int64_t" : "i128"; }
+  bool narrow_ok(const sfg_ins* I, int n) const {
+    if (P.budget >= (1ull << 30)) return false;
+    const int64_t small = 1ll << 31, addr = 1ll << 40;
+    for (int i = 0; i < n; ++i) {
+      const sfg_ins& x = I[i];
+      if ((x.op == SFG_LD || x.op == SFG_ST) && (x.imm2 >= small || x.imm2 <= -small)) return false;
+      if (x.op == SFG_LD && x.mode == SFG_MK_B64) return false;
+      if (x.op == SFG_MOV && x.mode == SFG_CLS_A && (x.flags & SFG_F_S1_IMM) &&
+          ((x.flags & SFG_F_U64IMM) || x.imm1 >= addr || x.imm1 <= -addr)) return false;
+      if ((x.op == SFG_ADD || x.op == SFG_SUB || x.op == SFG_MUL) && x.mode == SFG_CLS_A) {
+        if (x.op == SFG_MUL) return false;
+        if ((x.flags & SFG_F_S2_IMM) && (x.imm2 >= small || x.imm2 <= -small)) return false;
+      }
+    }
+    return true;
+  }
   // stores of the kernel being emitted: written[q] = some store's base carries the
   // tag of pointer parameter q; any_untagged_store = some store's base has no
   // static tag (could reach any record)
@@ -259,8 +287,8 @@ struct Gen {
         else if (x.mode == SFG_CLS_F) o << "    " << f(x.dst) << " = " << src_f(x, 1) << ";\n";
         else if (x.mode == SFG_CLS_A) {
           if (x.flags & SFG_F_S1_IMM) {
-            if (x.flags & SFG_F_U64IMM) o << "    " << a(x.dst) << " = (i128)(uint64_t)" << hex64(x.imm1) << "; ";
-            else o << "    " << a(x.dst) << " = (i128)" << i64lit(x.imm1) << "; ";
+            if (x.flags & SFG_F_U64IMM) o << "    " << a(x.dst) << " = (" << AT() << ")(uint64_t)" << hex64(x.imm1) << "; ";
+            else o << "    " << a(x.dst) << " = (" << AT() << ")" << i64lit(x.imm1) << "; ";
             o << t(x.dst) << " = 0;\n";
           } else {
             o << "    " << a(x.dst) << " = " << a(x.s1) << "; " << t(x.dst) << " = " << t(x.s1) << ";\n";
@@ -274,7 +302,7 @@ struct Gen {
       case SFG_MUL: {
         const char* opc = x.op == SFG_ADD ? "+" : x.op == SFG_SUB ? "-" : "*";
         if (x.mode == SFG_CLS_A) {
-          o << "    " << a(x.dst) << " = " << a(x.s1) << " " << opc << " (i128)" << src_i64(x, 2) << "; " << t(x.dst)
+          o << "    " << a(x.dst) << " = " << a(x.s1) << " " << opc << " (" << AT() << ")" << src_i64(x, 2) << "; " << t(x.dst)
             << " = " << t(x.s1) << ";\n";
         } else {
           o << "    " << r(x.dst) << " = (uint32_t)(" << src_r(x, 1) << " " << opc << " " << src_r(x, 2) << ");\n";
@@ -325,6 +353,7 @@ struct Gen {
     }
     cur_na = K.na;
     const sfg_ins* I = ins + K.base;
+    narrow = narrow_ok(I, K.n);
     const std::vector<int> starts = block_starts(I, K.n);
     std::vector<int> blk_of;
     const auto tags = tag_flow(I, K.n, K, starts, blk_of);
@@ -347,7 +376,7 @@ struct Gen {
     for (int q = 0; q < K.regs; ++q) {
       o << "  uint32_t " << r(q) << " = " << (q < K.nr ? "pre.r[" + std::to_string(q) + "]" : std::string("0u"))
         << ", " << f(q) << " = " << (q < K.nf ? "pre.f[" + std::to_string(q) + "]" : std::string("0u")) << ";\n";
-      o << "  i128 " << a(q) << " = " << (q < K.na ? "(i128)pre.a[" + std::to_string(q) + "]" : std::string("0"))
+      o << "  " << AT() << " " << a(q) << " = " << (q < K.na ? "(" + AT() + ")pre.a[" + std::to_string(q) + "]" : std::string("0"))
         << "; int32_t " << t(q) << " = " << (q < K.na ? "pre.ap[" + std::to_string(q) + "]" : std::string("0"))
         << "; bool " << p(q) << " = false;\n";
     }

@@ -360,3 +360,76 @@ def test_sequential_fuzz_loop_matches_reference_output_dir(engine_cls, key, roun
     assert sorted(p.name for p in (d / "corpus").iterdir()) == want["corpus"]
     assert sorted(p.name for p in (d / "crashes").iterdir()) == want["crashes"]
     assert s.to_rec() == want["summary"]
+
+
+WIDE_SIR = """\
+# pointer registers beyond int64: a 64-bit load into a pointer register and a
+# near-2^63 immediate plus i32 offsets (the 128-bit register form of the
+# specialized kernel; addresses in reports must stay exact)
+kernel widereg(x:ptr.global, n:i32, k:i32) regs=8
+  ld.global.b64 %a1, [%a0]
+  setp.lt %p0, %r0, 4
+  bra %p0, small
+  mov %a2, 9223372036854775792
+  add %a2, %a2, %r0
+  add %a2, %a2, %r1
+  ld.global.b32 %r2, [%a2]
+  exit
+small:
+  add %a1, %a1, %r1
+  ld.global.b32 %r3, [%a1]
+  mov %a3, %a0
+  add %a3, %a3, %r0
+  st.global.b32 [%a3], %r1
+  exit
+"""
+
+WIDE_MAN = """\
+program widereg.sir
+
+argspec x ptr global i32 count=4 seed=seq lo=-4 hi=4
+argspec n i32 seed=0 lo=0 hi=8
+argspec k i32 seed=0 lo=-8 hi=8
+
+init:
+  alloc ws global 4096
+  copy_in ws zeros:4096
+compute:
+  launch widereg grid=1 block=2 args=arg:0,arg:1,arg:2
+term:
+  free ws
+"""
+
+
+def test_wide_pointer_registers_match_oracle(engine_cls):
+    """A kernel whose pointer registers leave int64 (a 64-bit load into one, a
+    near-2^63 immediate plus offsets) keeps the specialized kernel's 128-bit
+    register form; every input of a batched campaign equals the CPU oracle:
+    child, verdict line (exact wild addresses), retired count, edges, admission."""
+    from oracle.loop import batched_loop
+    from paper_2603_05725_b200.manifest import harness_from_text
+    m = harness_from_text(WIDE_MAN, WIDE_SIR, "widereg/harness.man")
+    n, R = 1024, 256
+    want = batched_loop(m, master_seed=5, iterations=n, round_size=R).records
+    dc = engine_cls(m, master_seed=5)
+    import ctypes
+    nb = dc.L.sfg_program_jit_source(dc.h, None, 0)
+    buf = ctypes.create_string_buffer(nb + 1)
+    dc.L.sfg_program_jit_source(dc.h, buf, nb + 1)
+    assert "i128 a1 =" in buf.value.decode()   # the 128-bit register form was generated
+    got = []
+    dc.run_rounds(1, n + 1, R, depth=2, on_round=lambda res: got.extend(dc.round_records(res)))
+    assert len(got) == len(want)
+    kinds = set()
+    for g, w in zip(got, want):
+        assert _digest(g["child"]) == _digest(w["child"]), g["it"]
+        assert (g["status"], g["report"], g["retired"]) == (w["status"], w["report"], w["retired"]), g["it"]
+        assert (g["edges"], g["admitted"], g["allocs"]) == (w["edges"], w["admitted"], w["allocs"]), g["it"]
+        if w["report"]:
+            f = dict(t.split("=", 1) for t in w["report"].split()[1:] if "=" in t)
+            a = f["addr"][2:]
+            a = -int(a[1:], 16) if a.startswith("-") else int(a, 16)
+            kinds.add((f["class"], f["iid"], a >= 1 << 63, a < 0))
+    # wild addresses past 2^63 and below 0, out-of-bounds and space mismatches
+    assert len(kinds) >= 5 and any(k[2] for k in kinds) and any(k[3] for k in kinds)
+    dc.close()

@@ -210,3 +210,22 @@ def test_bench_reference_arm_cpu():
     assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "execs/s"
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and 900 <= line["ms_per_step"] <= 1500
+
+
+def test_jit_pointer_register_width():
+    """The specializer keeps simulated pointer registers in int64 only when the
+    kernel cannot push them past 2^62 (pointer params, small immediates, i32
+    offsets, budget < 2^30): matmul is narrow; a 64-bit load into a pointer
+    register or a near-2^63 immediate keeps the 128-bit form (csrc/jit.cu narrow_ok)."""
+    import ctypes
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "tools"))
+    import jit_check
+    from paper_2603_05725_b200.manifest import harness_from_text
+    from paper_2603_05725_b200.workloads import load
+    from test_gpu_parity import WIDE_MAN, WIDE_SIR
+    rc, _, src = jit_check.check(load("matmul"))
+    assert rc == 0 and "int64_t a0 =" in src and "i128 a0 =" not in src
+    rc, _, src = jit_check.check(harness_from_text(WIDE_MAN, WIDE_SIR, "widereg/harness.man"))
+    assert rc == 0 and "i128 a1 =" in src
