@@ -767,7 +767,8 @@ class DeviceCampaign:
 
         # Speculation depth adapts: an admission invalidates every round in flight, and
         # admissions cluster at the start of a campaign (new coverage), so the depth
-        # drops to 2 after an admitting round and doubles after each clean one.
+        # drops to 2 after an admitting round and quadruples after each clean one
+        # (2 -> 8 -> 32: a campaign's pipeline is full after two clean rounds).
         def fill():
             nonlocal nxt
             while len(inflight) < min(depth, self.spec_depth) and more():
@@ -793,7 +794,7 @@ class DeviceCampaign:
                     self._submit(SS, SS.round_it0, SS.round_n, SS.round_index, resubmit=True)
                     inflight.append((kk, SS))
             else:
-                self.spec_depth = min(2 * self.spec_depth, 1 << 20)
+                self.spec_depth = min(4 * self.spec_depth, 1 << 20)
             fill()
         return results
 
