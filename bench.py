@@ -335,7 +335,7 @@ def run_ours(a):
                            "rounds_in_flight": D, "engine": "jit" if dc.jit else "interpreter",
                            "l2": f"inputs larger than L2: {D} rounds in flight hold ~{D * R * 1900 >> 20} MiB of "
                                  "round buffers (126 MB L2)", "parallelism": f"shard{world}",
-                           "merge": f"per-round NCCL MIN/SUM all-reduce + all-gather ({collectives} collectives)"
+                           "merge": f"per-round {backend.upper()} MIN/SUM all-reduce + all-gather ({collectives} collectives)"
                            if world > 1 else "none (1 GPU)"},
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(), "roofline": roof,
                 "issue_roofline": issue, "cpu_baseline": cpu}
