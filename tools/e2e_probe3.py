@@ -25,15 +25,28 @@ def fin(self, S):
 
 
 engine.DeviceCampaign._finalize = fin
+if "--after-bench" in sys.argv:
+    # the bench's order: a device-timed campaign first, its buffers released
+    import gc
+    dc = engine.DeviceCampaign(m, master_seed=11)
+    dc.run_rounds(1, 1 + 99 * R, R, depth=D)
+    dc.close(); dc.slots.clear(); dc._aux = None
+    del dc
+    gc.collect()
+gc_off = "--gc-off" in sys.argv
 runs = []
 for rep in range(reps):
     log.clear()
     torch.cuda.synchronize()
     a0 = torch.cuda.memory_stats().get("num_device_alloc", 0)
+    import gc
+    if gc_off:
+        gc.disable()
     t0 = time.perf_counter()
     s = fuzz_loop(m, CampaignConfig(master_seed=11, iterations=K * R, round_size=R, pipeline_depth=D))
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
+    gc.enable()
     gaps = [b[0] - a[0] for a, b in zip(log, log[1:])]
     adm = [k for k, x in enumerate(log) if x[1]]
     runs.append((dt, list(log), t0))
