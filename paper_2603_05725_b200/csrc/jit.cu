@@ -215,7 +215,8 @@ struct Gen {
       o << "      " << slow_path << "\n";
     }
     if (!st) {
-      if (x.mode == SFG_MK_F32) o << "      " << f(x.dst) << " = sfg_quiet((uint32_t)v_);\n";
+      if (x.mode == SFG_MK_F32)
+        o << "      " << f(x.dst) << " = " << (fbits[x.dst] ? "sfg_quiet((uint32_t)v_)" : "(uint32_t)v_") << ";\n";
       else if (x.mode == SFG_MK_B64) o << "      " << a(x.dst) << " = (" << AT() << ")(uint64_t)v_; " << t(x.dst) << " = 0;\n";
       else o << "      " << r(x.dst) << " = (uint32_t)v_;\n";
     }
@@ -231,6 +232,20 @@ struct Gen {
   // the 128-bit arithmetic and high-word checks.  A 64-bit load into a pointer
   // register (values up to 2^64) or any larger immediate keeps the 128-bit form.
   bool narrow = false;
+  // fbits[r]: the exact bits of f-register r can be observed (it is copied by a
+  // mov or stored).  A loaded f32 is quieted (sNaN -> qNaN, executor.py loads
+  // through a double) only then: fadd/fsub/fmul (sfg_fop quiets its first NaN
+  // operand itself), float setp and cvt cannot tell a signaling NaN from its
+  // quieted form.
+  std::vector<char> fbits;
+  void f_observers(const sfg_ins* I, int n, int regs) {
+    fbits.assign(regs > 0 ? regs : 1, 0);
+    for (int i = 0; i < n; ++i) {
+      const sfg_ins& x = I[i];
+      if (x.op == SFG_MOV && x.mode == SFG_CLS_F && !(x.flags & SFG_F_S1_IMM)) fbits[x.s1] = 1;
+      if (x.op == SFG_ST && x.mode == SFG_MK_F32 && !(x.flags & SFG_F_S2_IMM)) fbits[x.s2] = 1;
+    }
+  }
   std::string AT() const { return narrow ? "int64_t" : "i128"; }
   bool narrow_ok(const sfg_ins* I, int n) const {
     if (P.budget >= (1ull << 30)) return false;
@@ -354,6 +369,7 @@ struct Gen {
     cur_na = K.na;
     const sfg_ins* I = ins + K.base;
     narrow = narrow_ok(I, K.n);
+    f_observers(I, K.n, K.regs);
     const std::vector<int> starts = block_starts(I, K.n);
     std::vector<int> blk_of;
     const auto tags = tag_flow(I, K.n, K, starts, blk_of);

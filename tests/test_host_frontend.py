@@ -229,3 +229,20 @@ def test_jit_pointer_register_width():
     assert rc == 0 and "int64_t a0 =" in src and "i128 a0 =" not in src
     rc, _, src = jit_check.check(harness_from_text(WIDE_MAN, WIDE_SIR, "widereg/harness.man"))
     assert rc == 0 and "i128 a1 =" in src
+
+
+def test_jit_load_quieting_only_when_observable():
+    """A loaded f32 is quieted (the reference loads through a double) only when
+    its register's bits can be observed -- copied by a mov or stored; operands
+    of fadd/fmul/setp/cvt cannot tell a signaling NaN from its quieted form
+    (csrc/jit.cu f_observers).  matmul feeds its loads to fmul only; copy
+    stores what it loads."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "tools"))
+    import jit_check
+    from paper_2603_05725_b200.workloads import load
+    rc, _, src = jit_check.check(load("matmul"))
+    assert rc == 0 and "sfg_quiet((uint32_t)v_)" not in src and "= (uint32_t)v_;" in src
+    rc, _, src = jit_check.check(bench_manifest("copy"))
+    assert rc == 0 and "sfg_quiet((uint32_t)v_)" in src
