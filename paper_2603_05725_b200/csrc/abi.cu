@@ -60,8 +60,10 @@ static thread_local std::string g_err;
 
 // Harness arguments that can steer the simulated kernels' control flow: taint of
 // every kernel parameter propagated (flow-insensitively, to a fixpoint) through
-// moves, arithmetic, conversions and load addresses into setp sources; the
-// launches' bindings map tainted parameters to harness arguments.
+// moves, arithmetic, conversions and load addresses into setp sources and into
+// load/store addresses (the sanitizer's verdict stops a thread at its first
+// finding); the launches' bindings map tainted parameters to harness arguments.
+// Pure data (e.g. a float scale factor) stays out.
 static uint32_t control_arg_mask(const sfg_prog& P, const sfg_ins* ins, const sfg_hostop* H, size_t nh,
                                  const sfg_binding* B) {
   uint32_t args = 0;
@@ -101,9 +103,15 @@ static uint32_t control_arg_mask(const sfg_prog& P, const sfg_ins* ins, const sf
             flow(SFG_CLS_P, x.dst, m);
             break;
           }
-          case SFG_LD: {
-            const int c = x.mode == SFG_MK_F32 ? SFG_CLS_F : x.mode == SFG_MK_B64 ? SFG_CLS_A : SFG_CLS_R;
-            flow(c, x.dst, src(SFG_CLS_A, x.s1, false));
+          case SFG_LD: case SFG_ST: {
+            // the sanitizer's verdict on the address is a control decision too (a
+            // finding stops the thread): whatever reaches an address steers control
+            const uint32_t am = src(SFG_CLS_A, x.s1, false);
+            if ((ctrl | am) != ctrl) { ctrl |= am; changed = true; }
+            if (x.op == SFG_LD) {
+              const int c = x.mode == SFG_MK_F32 ? SFG_CLS_F : x.mode == SFG_MK_B64 ? SFG_CLS_A : SFG_CLS_R;
+              flow(c, x.dst, am);
+            }
             break;
           }
           case SFG_CVT:

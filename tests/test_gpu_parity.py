@@ -269,13 +269,19 @@ def test_group_parallel_bulk_matches_reference(engine_cls, name, monkeypatch):
 
 def test_order_mask_is_control_taint(engine_cls):
     """sfg_order groups inputs by the arguments that can steer control flow: for the
-    matmul target those are m, n, k (loop bounds); a, b, c and the leading dimensions
-    only move addresses and data."""
+    matmul target the loop bounds m, n, k and, through the sanitizer's verdicts on
+    the addresses they form, a, b, c and the leading dimensions; structcfg's f32
+    alpha is pure data."""
     from conftest import workload_manifest
     dc = engine_cls(workload_manifest("matmul"), master_seed=11)
     names = [s.name for s in dc.specs]
     mask = dc.L.sfg_program_order_mask(dc.h)
-    assert {names[a] for a in range(len(names)) if mask >> a & 1} == {"m", "n", "k"}
+    assert {names[a] for a in range(len(names)) if mask >> a & 1} == set(names)
+    dc.close()
+    dc = engine_cls(workload_manifest("structcfg"), master_seed=11)
+    names = [s.name for s in dc.specs]
+    mask = dc.L.sfg_program_order_mask(dc.h)
+    assert {names[a] for a in range(len(names)) if mask >> a & 1} == {"cfg", "x", "y"}
     dc.close()
 
 

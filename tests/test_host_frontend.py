@@ -183,16 +183,20 @@ def _control_args(m):
 
 
 def test_control_taint_mask():
-    """sfg_order's signature covers the arguments that reach a setp (loop bounds,
-    compared values), not strides or stored data (csrc/abi.cu control_arg_mask)."""
+    """sfg_order's signature covers the arguments that can steer control: those
+    reaching a setp (loop bounds, compared values) and those reaching a load or
+    store address (the sanitizer's verdict stops the thread), not pure data such
+    as float scale factors (csrc/abi.cu control_arg_mask)."""
     from paper_2603_05725_b200.workloads import load
-    assert _control_args(load("matmul")) == {"m", "n", "k"}
-    assert _control_args(load("vadd")) == {"n"}
+    assert _control_args(load("matmul")) == {"a", "b", "c", "m", "n", "k", "lda", "ldb", "ldc"}
+    assert _control_args(load("vadd")) == {"x", "y", "z", "n"}
+    assert _control_args(load("structcfg")) == {"cfg", "x", "y"}      # not the f32 alpha
     # amax compares loaded elements: the array steers control through its contents
     amax = _control_args(bench_manifest("amax"))
     assert "n" in amax and "x" in amax
-    # copy only bounds its loop by n
-    assert _control_args(bench_manifest("copy")) == {"n"}
+    assert _control_args(bench_manifest("copy")) == {"x", "y", "n"}
+    assert _control_args(bench_manifest("rotm")) == {"x", "y", "flag", "n"}   # not h11..h22
+    assert _control_args(bench_manifest("axpy")) == {"x", "y", "n"}          # not the scale a
 
 
 def test_bench_reference_arm_cpu():
