@@ -35,6 +35,10 @@ class OutOfSpaceError(Exception):
     pass
 
 
+class LoweringError(Exception):
+    """Harness feature the device path does not lower (raised before any device work)."""
+
+
 class InitFailure(Exception):
     """INIT produced a finding / error on the seed input (reference: CampaignFatalError)."""
 
@@ -186,7 +190,7 @@ def build_baseline(manifest, seed_tc, mem: MemConfig) -> Baseline:
                 free.append((v.slot_start - SPACE_BASE[v.space], v.slot_end - v.slot_start, v.space))
                 qbytes[v.space] -= v.slot_end - v.slot_start
         elif op.kind == "launch":
-            raise InitFailure("INIT-phase launches are not lowered to the device path")
+            raise LoweringError("INIT-phase launches are not lowered to the device path")
     blob = bytearray()
     phys = []
     for r in recs:

@@ -168,18 +168,20 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
     if config.distributed:
         from .shard import RoundComm
         comm = RoundComm()
-    t_setup = time.perf_counter()
-    try:
-        dc = _device_campaign(manifest, config, comm)
-    except InitFailure as e:   # campaign.py:723-725: the init phase failed on the seed input
-        raise CampaignFatalError(str(e)) from e
+    # the seed corpus entry is written before anything can fail (campaign.py:700-703)
     if out_dir is not None:
-        _write_corpus_entry(out_dir, dc.host_entries[0][0], specs)
-    t_setup = time.perf_counter() - t_setup
+        _write_corpus_entry(out_dir, manifest.seed(config.master_seed), specs)
     stop_reason = "iterations"
     executed = 0
     init_runs = term_runs = 0
+    dc = None
     try:
+        t_setup = time.perf_counter()
+        try:
+            dc = _device_campaign(manifest, config, comm)
+        except InitFailure as e:   # campaign.py:723-725: the init phase failed on the seed input
+            raise CampaignFatalError(str(e)) from e
+        t_setup = time.perf_counter() - t_setup
         for w, rng_ in enumerate(_worker_ranges(config.iterations, config.workers)):
             if stop_reason != "iterations":
                 break
@@ -239,6 +241,12 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
     except CampaignFatalError:
         if out_dir is not None:
             (out_dir / "FAILED").write_text("campaign fatal\n")
+        if dc is not None:
+            dc.close()
+        raise
+    except BaseException:
+        if dc is not None:    # release the round buffers now, not at garbage collection
+            dc.close()
         raise
     wall = time.perf_counter() - t0
     corpus = Corpus([CorpusEntry(tc, adm, seed) for tc, adm, seed in dc.host_entries])

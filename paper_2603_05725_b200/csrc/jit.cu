@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <sstream>
@@ -221,6 +222,357 @@ struct Gen {
       else o << "      " << r(x.dst) << " = (uint32_t)v_;\n";
     }
     o << "    }\n";
+  }
+
+  // ---------------------------------------------------------------------------
+  // Loop summarization.  A simple cycle of blocks whose instructions are register
+  // arithmetic, integer setp and branches only (no ld/st) is a pure function of
+  // its registers: every register carried from one trip to the next must be a
+  // basic induction variable (x += loop-invariant per trip), every exit branch an
+  // integer compare of an induction variable (or an invariant) against an
+  // invariant.  At a window check of the cycle's head block the summary computes
+  // the first trip T whose exit condition holds (closed form over a horizon in
+  // which no compared i32 value wraps and the budget cannot be reached), skips
+  // trips 0 .. T-2 at once -- induction variables advanced with i32 / pointer
+  // wraparound exactly as executor.py:297-318 would, each edge of the cycle
+  // counted T-1 times, T-1 trips x trip length retired -- and lets the
+  // generated code run trip T-1 (which recomputes every derived register) and
+  // the exiting trip T instruction by instruction, so budget exhaustion and
+  // exits mid-trip are exactly the reference's (executor.py:411-415).
+  struct Opnd {       // r-class (i32) value at a program point, as a function of the trip t
+    int kind = 0;     // 0 unknown, 1 invariant expr, 2 IV(x) + offset expr, 3 i64 immediate
+    std::string e;    // kind 1: u32 expression; kind 2: u32 offset expression
+    int iv = -1;
+    int64_t imm = 0;
+  };
+  struct AVal {       // abstract register value
+    int kind = 0;     // 0 unknown, 1 invariant, 2 IV(iv) + e, 4 compare (predicates)
+    std::string e;
+    int iv = -1;
+    int cmp = 0;
+    Opnd l, r;
+  };
+  struct Exit {
+    int cmp;          // exits when  l <cmp> r  (already oriented)
+    Opnd l, r;
+    bool konst;       // predicate invariant over the cycle: exits iff the expr `pe` holds
+    std::string pe;
+  };
+  struct Cycle {
+    std::vector<int> blocks;
+    int64_t len = 0;
+    std::vector<int> edges;                 // edge ids counted once per trip
+    std::vector<std::pair<int, std::string>> r_iv, a_iv;  // register, per-trip step expr
+    std::vector<Exit> exits;
+    std::vector<std::string> guards;        // stable carried registers: current value == invariant
+  };
+
+  static int neg_cmp(int c) {
+    static const int n[] = {SFG_CMP_NE, SFG_CMP_EQ, SFG_CMP_GE, SFG_CMP_GT, SFG_CMP_LE, SFG_CMP_LT};
+    return n[c];
+  }
+
+  // successors of block b: (block, edge id)
+  struct Succ { int blk, edge; bool taken; };
+  std::vector<Succ> succs(const sfg_ins* I, int n, const std::vector<int>& starts, const std::vector<int>& blk_of, int b) {
+    const int nb = (int)starts.size();
+    const int e = b + 1 < nb ? starts[b + 1] : n;
+    const sfg_ins& last = I[e - 1];
+    std::vector<Succ> s;
+    if (last.op == SFG_EXIT) return s;
+    if (last.op == SFG_BRA) {
+      s.push_back({blk_of[last.target], last.edge_tk, true});
+      if ((last.flags & SFG_F_PRED) && e < n) s.push_back({blk_of[e], last.edge_ft, false});
+    } else if (e < n) {
+      s.push_back({blk_of[e], last.edge_ft, false});
+    }
+    return s;
+  }
+
+  // analyse one simple cycle (blocks in trip order starting at the head)
+  bool analyse_cycle(const sfg_ins* I, int n, const std::vector<int>& starts, const std::vector<int>& blk_of,
+                     int regs, Cycle& C) {
+    const int nb = (int)starts.size();
+    const int R = regs > 0 ? regs : 1;
+    // pass 1: which registers (per class) are read before written in the trip, which are written
+    std::vector<char> wr(4 * R, 0), er(4 * R, 0);
+    auto rd = [&](int cls, int q) { if (!wr[cls * R + q]) er[cls * R + q] = 1; };
+    auto wt = [&](int cls, int q) { wr[cls * R + q] = 1; };
+    C.len = 0;
+    for (size_t bi = 0; bi < C.blocks.size(); ++bi) {
+      const int b = C.blocks[bi];
+      const int s0 = starts[b], e = b + 1 < nb ? starts[b + 1] : n;
+      C.len += e - s0;
+      for (int i = s0; i < e; ++i) {
+        const sfg_ins& x = I[i];
+        const bool i1 = x.flags & SFG_F_S1_IMM, i2 = x.flags & SFG_F_S2_IMM;
+        switch (x.op) {
+          case SFG_MOV:
+            if (!i1 || x.mode == SFG_CLS_P) rd(x.mode, x.s1);
+            wt(x.mode, x.dst);
+            break;
+          case SFG_ADD: case SFG_SUB: case SFG_MUL:
+            if (x.mode == SFG_CLS_A) { rd(SFG_CLS_A, x.s1); if (!i2) rd(SFG_CLS_R, x.s2); wt(SFG_CLS_A, x.dst); }
+            else { if (!i1) rd(SFG_CLS_R, x.s1); if (!i2) rd(SFG_CLS_R, x.s2); wt(SFG_CLS_R, x.dst); }
+            break;
+          case SFG_FADD: case SFG_FSUB: case SFG_FMUL:
+            if (!i1) rd(SFG_CLS_F, x.s1);
+            if (!i2) rd(SFG_CLS_F, x.s2);
+            wt(SFG_CLS_F, x.dst);
+            break;
+          case SFG_SETP: {
+            const int c = (x.flags & SFG_F_FLOAT) ? SFG_CLS_F : SFG_CLS_R;
+            if (!i1) rd(c, x.s1);
+            if (!i2) rd(c, x.s2);
+            wt(SFG_CLS_P, x.dst);
+            break;
+          }
+          case SFG_CVT:
+            if (!i1) rd(x.mode == SFG_CVT_F_FROM_I ? SFG_CLS_R : SFG_CLS_F, x.s1);
+            wt(x.mode == SFG_CVT_F_FROM_I ? SFG_CLS_F : SFG_CLS_R, x.dst);
+            break;
+          case SFG_SREG: wt(SFG_CLS_R, x.dst); break;
+          case SFG_BRA: if (x.flags & SFG_F_PRED) rd(SFG_CLS_P, x.s1); break;
+          default: return false;  // ld / st / exit: not a pure register cycle
+        }
+      }
+    }
+    // pass 2: abstract values through one trip.  A carried register whose value at
+    // the end of the trip is loop-invariant ("stable", e.g. a counter reset inside
+    // the cycle) is treated as invariant, guarded at run time by its current value
+    // equalling the invariant (then every trip sees the same value).
+    std::vector<char> stable(4 * R, 0);
+    for (int attempt = 0; attempt < 2; ++attempt) {
+    C.edges.clear(); C.exits.clear(); C.r_iv.clear(); C.a_iv.clear(); C.guards.clear();
+    bool retry = false;
+    std::vector<AVal> v(4 * R);
+    for (int c = 0; c < 4; ++c)
+      for (int q = 0; q < R; ++q) {
+        AVal& a = v[c * R + q];
+        if (!wr[c * R + q] || stable[c * R + q]) {
+          a.kind = 1;
+          a.e = c == SFG_CLS_R ? r(q) : c == SFG_CLS_F ? f(q) : c == SFG_CLS_A ? a_name(q) : p(q);
+        } else if (er[c * R + q]) {
+          if (c != SFG_CLS_R && c != SFG_CLS_A) return false;  // carried f / p register
+          a.kind = 2; a.iv = q; a.e = c == SFG_CLS_R ? "0u" : "(int64_t)0";
+        }
+      }
+    auto Rv = [&](int q) -> AVal& { return v[SFG_CLS_R * R + q]; };
+    auto ropnd = [&](const sfg_ins& x, int slot) -> AVal {   // u32 operand
+      const bool imm = slot == 1 ? (x.flags & SFG_F_S1_IMM) : (x.flags & SFG_F_S2_IMM);
+      if (imm) { AVal a; a.kind = 1; a.e = u32lit(slot == 1 ? x.imm1 : x.imm2); return a; }
+      return Rv(slot == 1 ? x.s1 : x.s2);
+    };
+    auto cmp_opnd = [&](const sfg_ins& x, int slot) -> Opnd {  // src_i64 operand of an int setp
+      Opnd o;
+      const bool imm = slot == 1 ? (x.flags & SFG_F_S1_IMM) : (x.flags & SFG_F_S2_IMM);
+      if (imm) {
+        int64_t m = slot == 1 ? x.imm1 : x.imm2;
+        const int64_t cl = 1ll << 40;   // i32 values never reach it: the compare is unchanged
+        o.kind = 3; o.imm = m > cl ? cl : m < -cl ? -cl : m;
+        return o;
+      }
+      const AVal& a = Rv(slot == 1 ? x.s1 : x.s2);
+      if (a.kind == 1) { o.kind = 1; o.e = a.e; }
+      else if (a.kind == 2) { o.kind = 2; o.iv = a.iv; o.e = a.e; }
+      return o;
+    };
+    for (size_t bi = 0; bi < C.blocks.size(); ++bi) {
+      const int b = C.blocks[bi];
+      const int nxt = C.blocks[(bi + 1) % C.blocks.size()];
+      const int s0 = starts[b], e = b + 1 < nb ? starts[b + 1] : n;
+      for (int i = s0; i < e; ++i) {
+        const sfg_ins& x = I[i];
+        const bool i1 = x.flags & SFG_F_S1_IMM;
+        AVal res;
+        switch (x.op) {
+          case SFG_MOV:
+            if (x.mode == SFG_CLS_R) res = ropnd(x, 1);
+            else if (x.mode == SFG_CLS_F) {
+              if (i1) { res.kind = 1; res.e = u32lit(x.imm1); } else res = v[SFG_CLS_F * R + x.s1];
+            } else if (x.mode == SFG_CLS_A) {
+              if (i1) {
+                res.kind = 1;
+                res.e = (x.flags & SFG_F_U64IMM) ? "(" + AT() + ")(uint64_t)" + hex64(x.imm1) : "(" + AT() + ")" + i64lit(x.imm1);
+              } else res = v[SFG_CLS_A * R + x.s1];
+            } else res = v[SFG_CLS_P * R + x.s1];
+            v[x.mode * R + x.dst] = res;
+            break;
+          case SFG_ADD: case SFG_SUB: case SFG_MUL: {
+            const char* opc = x.op == SFG_ADD ? "+" : x.op == SFG_SUB ? "-" : "*";
+            if (x.mode == SFG_CLS_A) {
+              if (x.op == SFG_MUL) { v[SFG_CLS_A * R + x.dst] = AVal(); break; }
+              std::string o2;
+              if (x.flags & SFG_F_S2_IMM) o2 = i64lit(x.imm2);
+              else if (Rv(x.s2).kind == 1) o2 = "(int64_t)(int32_t)(" + Rv(x.s2).e + ")";
+              const AVal& s = v[SFG_CLS_A * R + x.s1];
+              if (!o2.empty() && (s.kind == 1 || s.kind == 2)) {
+                res = s;
+                res.e = "(" + (s.kind == 1 ? s.e : s.e) + " " + opc + " (" + (s.kind == 1 ? AT() : std::string("int64_t")) +
+                        ")" + o2 + ")";
+              }
+              v[SFG_CLS_A * R + x.dst] = res;
+              break;
+            }
+            const AVal a1 = ropnd(x, 1), a2 = ropnd(x, 2);
+            if (a1.kind == 1 && a2.kind == 1) { res.kind = 1; res.e = "(uint32_t)(" + a1.e + " " + opc + " " + a2.e + ")"; }
+            else if (x.op != SFG_MUL && a1.kind == 2 && a2.kind == 1) {
+              res = a1; res.e = "(uint32_t)(" + a1.e + " " + opc + " " + a2.e + ")";
+            } else if (x.op == SFG_ADD && a1.kind == 1 && a2.kind == 2) {
+              res = a2; res.e = "(uint32_t)(" + a2.e + " + " + a1.e + ")";
+            }
+            Rv(x.dst) = res;
+            break;
+          }
+          case SFG_FADD: case SFG_FSUB: case SFG_FMUL: v[SFG_CLS_F * R + x.dst] = AVal(); break;
+          case SFG_CVT:
+            v[(x.mode == SFG_CVT_F_FROM_I ? SFG_CLS_F : SFG_CLS_R) * R + x.dst] = AVal();
+            break;
+          case SFG_SREG: {
+            static const char* names[] = {"tid", "block", "ctaid", "grid"};
+            res.kind = 1; res.e = std::string("(uint32_t)") + names[x.mode];
+            Rv(x.dst) = res;
+            break;
+          }
+          case SFG_SETP:
+            if (!(x.flags & SFG_F_FLOAT)) {
+              const Opnd l = cmp_opnd(x, 1), rr = cmp_opnd(x, 2);
+              if (l.kind && rr.kind) { res.kind = 4; res.cmp = x.mode; res.l = l; res.r = rr; }
+            }
+            v[SFG_CLS_P * R + x.dst] = res;
+            break;
+          case SFG_BRA: {
+            const auto ss = succs(I, n, starts, blk_of, b);
+            int stay_tk = -1;  // which direction stays on the cycle: 1 taken, 0 fallthrough
+            for (const Succ& sc : ss)
+              if (sc.blk == nxt) {
+                if (stay_tk >= 0) return false;   // both directions reach the next block
+                stay_tk = sc.taken ? 1 : 0;
+                if (sc.edge >= 0) C.edges.push_back(sc.edge);
+              }
+            if (stay_tk < 0) return false;
+            if (!(x.flags & SFG_F_PRED)) break;
+            // exits when (pneg ? !p : p) != stay_tk, i.e. when p == exit_p
+            const bool exit_p = (stay_tk == 1) == ((x.flags & SFG_F_PNEG) != 0);
+            const AVal& pv = v[SFG_CLS_P * R + x.s1];
+            Exit X;
+            if (pv.kind == 1) { X.konst = true; X.pe = exit_p ? pv.e : "!" + pv.e; X.cmp = 0; }
+            else if (pv.kind == 4) { X.konst = false; X.cmp = exit_p ? pv.cmp : neg_cmp(pv.cmp); X.l = pv.l; X.r = pv.r; }
+            else return false;
+            C.exits.push_back(X);
+            break;
+          }
+          default: return false;
+        }
+        if (i == e - 1 && x.op != SFG_BRA) {   // falls through into the next leader
+          if (blk_of[i + 1 < n ? i + 1 : 0] != nxt || i + 1 >= n) return false;
+          if (x.edge_ft >= 0) C.edges.push_back(x.edge_ft);
+        }
+      }
+    }
+    // carried registers must be basic induction variables: IV(x) + invariant step,
+    // or stable (invariant at the end of the trip)
+    for (int c : {SFG_CLS_R, SFG_CLS_A})
+      for (int q = 0; q < R; ++q) {
+        if (!(wr[c * R + q] && er[c * R + q])) continue;
+        const AVal& a = v[c * R + q];
+        if (stable[c * R + q]) {
+          if (a.kind != 1) return false;
+          C.guards.push_back((c == SFG_CLS_R ? r(q) : a_name(q)) + " == " + a.e);
+          continue;
+        }
+        if (a.kind == 1 && attempt == 0) { stable[c * R + q] = 1; retry = true; continue; }
+        if (a.kind != 2 || a.iv != q) return false;
+        (c == SFG_CLS_R ? C.r_iv : C.a_iv).push_back({q, a.e});
+      }
+    if (!retry) return !C.exits.empty();
+    }
+    return false;
+  }
+
+  std::string a_name(int i) { return a(i); }
+
+  // all summarizable simple cycles through check block h (trip order starting at h)
+  std::vector<Cycle> cycles_at(const sfg_ins* I, int n, const std::vector<int>& starts, const std::vector<int>& blk_of,
+                               int regs, int h) {
+    std::vector<Cycle> out;
+    std::vector<int> path{h};
+    std::vector<char> on((size_t)starts.size(), 0);
+    on[h] = 1;
+    int budget = 256;   // DFS steps
+    std::function<void(int)> dfs = [&](int b) {
+      if (--budget < 0 || out.size() >= 4) return;
+      for (const Succ& s : succs(I, n, starts, blk_of, b)) {
+        if (s.blk == h) {
+          Cycle C;
+          C.blocks = path;
+          const bool ok_ = analyse_cycle(I, n, starts, blk_of, regs, C);
+          if (getenv("SFG_LOOPSUM_DEBUG")) {
+            fprintf(stderr, "cycle at %d:", h);
+            for (int x : C.blocks) fprintf(stderr, " %d", x);
+            fprintf(stderr, " -> %s\n", ok_ ? "summary" : "no");
+          }
+          if (ok_) out.push_back(C);
+        } else if (!on[s.blk] && path.size() < 24) {
+          on[s.blk] = 1;
+          path.push_back(s.blk);
+          dfs(s.blk);
+          path.pop_back();
+          on[s.blk] = 0;
+        }
+      }
+    };
+    dfs(h);
+    return out;
+  }
+
+  // C++ of the summaries at a window check of block h
+  std::string summary_code(const std::vector<Cycle>& cs, const char* RT) {
+    std::ostringstream s;
+    for (const Cycle& C : cs) {
+      s << "    { // loop summary: blocks";
+      for (int b : C.blocks) s << " " << b;
+      s << "\n      const int64_t LEN_ = " << C.len << ";\n"
+        << "      int64_t H_ = HARD > ret ? (int64_t)((uint64_t)(HARD - 1u - ret) / (uint64_t)LEN_) : -1;\n";
+      for (auto& iv : C.r_iv) s << "      const uint32_t dr" << iv.first << "_ = " << iv.second << ";\n";
+      for (auto& iv : C.a_iv) s << "      const int64_t da" << iv.first << "_ = (int64_t)(" << iv.second << ");\n";
+      auto val = [&](const Opnd& o, std::string& v0, std::string& d) {
+        if (o.kind == 3) { v0 = i64lit(o.imm); d = "0ll"; }
+        else if (o.kind == 1) { v0 = "(int64_t)(int32_t)(" + o.e + ")"; d = "0ll"; }
+        else { v0 = "(int64_t)(int32_t)(uint32_t)(" + r(o.iv) + " + " + o.e + ")"; d = "(int64_t)(int32_t)dr" + std::to_string(o.iv) + "_"; }
+      };
+      std::vector<std::string> l0, ld, r0, rdl;
+      for (size_t k = 0; k < C.exits.size(); ++k) {
+        const Exit& X = C.exits[k];
+        std::string a, b, c, d;
+        if (!X.konst) { val(X.l, a, b); val(X.r, c, d); }
+        l0.push_back(a); ld.push_back(b); r0.push_back(c); rdl.push_back(d);
+        if (!X.konst) {
+          if (X.l.kind == 2) s << "      H_ = sfg_min64(H_, sfg_wrap_h(" << a << ", " << b << "));\n";
+          if (X.r.kind == 2) s << "      H_ = sfg_min64(H_, sfg_wrap_h(" << c << ", " << d << "));\n";
+        }
+      }
+      s << "      if (H_ >= 2";
+      for (const std::string& gd : C.guards) s << " && " << gd;
+      s << ") {\n        int64_t T_ = SFG_I64MAX;\n";
+      for (size_t k = 0; k < C.exits.size(); ++k) {
+        const Exit& X = C.exits[k];
+        if (X.konst) s << "        if (" << X.pe << ") T_ = 0;\n";
+        else
+          s << "        T_ = sfg_min64(T_, sfg_first_t(" << X.cmp << ", (" << l0[k] << ") - (" << r0[k] << "), (" << ld[k]
+            << ") - (" << rdl[k] << "), H_));\n";
+      }
+      s << "        const int64_t s_ = (T_ <= H_ ? T_ : H_ + 1) - 1;\n"
+        << "        if (s_ >= 2) {\n";
+      for (auto& iv : C.r_iv) s << "          " << r(iv.first) << " = (uint32_t)(" << r(iv.first) << " + (uint32_t)s_ * dr" << iv.first << "_);\n";
+      for (auto& iv : C.a_iv)
+        s << "          " << a(iv.first) << " = " << a(iv.first) << " + (" << AT() << ")s_ * (" << AT() << ")da" << iv.first << "_;\n";
+      for (int e : C.edges)
+        s << "          { const uint64_t o_ = J.ec[" << e << "]; if (o_ + (uint64_t)s_ > 0xFFFFFFFFull) J.ovf = true; J.ec[" << e
+          << "] = (uint32_t)(o_ + (uint64_t)s_); }\n";
+      s << "          ret += (" << RT << ")(s_ * LEN_);\n        }\n      }\n    }\n";
+    }
+    return s.str();
   }
 
   int cur_na = 0;
@@ -458,8 +810,20 @@ struct Gen {
     // whether this thread can still matter (run_launch_group)
     // bulk pass (soft cap on): poll every kStrag retired instructions whether the rest of
     // the warp's batch has finished; a straggler past kStragMin is deferred then
+    // loop summaries at the window checks of check blocks (analyse_cycle); a kernel
+    // with any runs windowed in every mode so that a long pure-register loop is met
+    std::vector<std::vector<Cycle>> sums(nb);
+    bool has_sum = false;
+    if (loop_summaries)
+      for (int b = 0; b < nb; ++b)
+        if (chk[b] && span[b] > 0) {
+          sums[b] = cycles_at(I, K.n, starts, blk_of, K.regs, b);
+          has_sum |= !sums[b].empty();
+        }
+    for (auto& v : sums) n_summaries += (int)v.size();
     o << "  " << RT << " LIM = PAR ? ((HARD > (" << RT << ")kPoll) ? (" << RT << ")kPoll : HARD)\n"
-         "            : ((J.done != nullptr && HARD > (" << RT << ")kStrag) ? (" << RT << ")kStrag : HARD);\n";
+         "            : (((J.done != nullptr || " << (has_sum ? "true" : "false") << ") && HARD > (" << RT << ")kStrag) ? ("
+      << RT << ")kStrag : HARD);\n";
     o << "  (void)grid; (void)block; (void)ctaid; (void)tid;\n";
     for (int b = 0; b < nb; ++b) {
       const int s0 = starts[b], e = b + 1 < nb ? starts[b + 1] : K.n;
@@ -471,8 +835,10 @@ struct Gen {
         if (!slow && chk[b] && span[b] > 0)
           o << "  if (ret + " << sp << " >= LIM) {\n"
             << "    if constexpr (PAR) { if (LIM < HARD) { if (J.poll()) { rc = RUN_ABORT; goto done; }\n"
+            << summary_code(sums[b], RT)
             << "      LIM = (HARD - ret > " << sp << " + kPoll) ? ret + " << sp << " + kPoll : HARD; goto B" << b << "; } }\n"
-            << "    else { if (LIM < HARD) { if (J.straggler(total + ret)) { rc = RUN_DEFER; goto done; }\n"
+            << "    else { if (LIM < HARD) { if (J.done != nullptr && J.straggler(total + ret)) { rc = RUN_DEFER; goto done; }\n"
+            << summary_code(sums[b], RT)
             << "      LIM = (HARD - ret > " << sp << " + kStrag) ? ret + " << sp << " + kStrag : HARD; goto B" << b << "; } }\n"
             << "    if (SFT) { rc = RUN_DEFER; goto done; } goto S" << b << "; }\n";
         for (int i = s0; i < e; ++i) {
@@ -514,6 +880,8 @@ struct Gen {
     o << "done:\n  total += ret;\n  return rc;\n}\n\n";
   }
 
+  bool loop_summaries = true;
+  int n_summaries = 0;
   int tail_minb = 12;
   int bulk_minb = 3;
 
@@ -522,6 +890,25 @@ struct Gen {
     const int NE = n_edges > 0 ? n_edges : 1;
     o << "#include \"exec_core.cuh\"\n\nnamespace {\n\n";
     o << "constexpr uint32_t kPoll = 4096u;\n";
+    // loop-summary helpers (see analyse_cycle)
+    o << "#define SFG_I64MAX 0x7FFFFFFFFFFFFFFFll\n";
+    o << "SFG_DEV int64_t sfg_min64(int64_t a, int64_t b) { return a < b ? a : b; }\n"
+         "// trips t >= 0 for which x0 + t*d stays inside int32 (x0 an int32 value)\n"
+         "SFG_DEV int64_t sfg_wrap_h(int64_t x0, int64_t d) {\n"
+         "  if (d > 0) return (2147483647ll - x0) / d;\n"
+         "  if (d < 0) return (x0 + 2147483648ll) / (-d);\n"
+         "  return SFG_I64MAX;\n}\n"
+         "// first t in [0, H] with  a + t*b <cmp> 0  (cmp: == != < <= > >=), else SFG_I64MAX\n"
+         "SFG_DEV int64_t sfg_first_t(int cmp, int64_t a, int64_t b, int64_t H) {\n"
+         "  int64_t t = SFG_I64MAX;\n"
+         "  if (cmp == 4 || cmp == 5) { a = -a; b = -b; cmp = cmp == 4 ? 2 : 3; }\n"
+         "  switch (cmp) {\n"
+         "    case 0: if (b == 0) t = a == 0 ? 0 : SFG_I64MAX; else if ((-a) % b == 0 && (-a) / b >= 0) t = (-a) / b; break;\n"
+         "    case 1: t = a != 0 ? 0 : (b != 0 ? 1 : SFG_I64MAX); break;\n"
+         "    case 2: t = a < 0 ? 0 : (b < 0 ? a / (-b) + 1 : SFG_I64MAX); break;\n"
+         "    default: t = a <= 0 ? 0 : (b < 0 ? (a + (-b) - 1) / (-b) : SFG_I64MAX); break;\n"
+         "  }\n"
+         "  return t <= H ? t : SFG_I64MAX;\n}\n";
     o << "constexpr uint32_t kStrag = 2048u;\nconstexpr uint64_t kStragMin = 8192ull;\n\n";
     o << "struct JitRunner {\n  uint32_t ec[" << NE << "], ecs[" << NE
       << "];\n  bool ovf, ovfs;\n  uint64_t soft_cap;\n"
@@ -656,6 +1043,7 @@ static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_e
                            std::string& log, std::vector<char>& cubin) {
   sfgjit::Gen g(P, ins);
   g.dead_kernels = dead_kernels;
+  if (const char* ls = getenv("SFG_LOOPSUM")) g.loop_summaries = atoi(ls) != 0;
   if (const char* tb = getenv("SFG_TAIL_MINB")) g.tail_minb = atoi(tb) >= 1 ? atoi(tb) : 12;
   if (const char* bb = getenv("SFG_BULK_MINB")) g.bulk_minb = atoi(bb) >= 1 ? atoi(bb) : 3;
   source = g.run(P.n_edges, max_edge_events);

@@ -159,7 +159,17 @@ class Slot:
     def ensure_work(self, nbytes: int, dev):
         if nbytes > self.work_cap:
             self.work_cap = int(nbytes * 1.1) + 4096
-            self.work = torch.empty(self.work_cap, dtype=torch.uint8, device=dev)
+            self.work = self.alloc_on_stream(self.work, self.work_cap, dev)
+
+    def alloc_on_stream(self, old, nbytes: int, dev):
+        """A new buffer for this slot's stream, replacing ``old``: superseded kernels
+        queued on the stream may still use the old one, so it is recorded on the stream
+        (the caching allocator reuses it only after that work completes), and the new
+        one is allocated in the stream's pool (reuse is stream-ordered)."""
+        if old is not None:
+            old.record_stream(self.stream)
+        with torch.cuda.stream(self.stream):
+            return torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=dev)
 
 
 class DeviceCampaign:
@@ -393,8 +403,10 @@ class DeviceCampaign:
             self._scan64(S, S.children.view(torch.int64), n, cw, CHILD.fields["readout_bytes"][1] // 8, S.ro_base, 1)
             with torch.cuda.stream(st):
                 S.tot[:2].cpu()  # host needs the readout size (diff mode only; tests)
-            S.readouts = self._u8(int(S.tot[1].item()) + 16)
+            S.readouts = S.alloc_on_stream(S.readouts, int(S.tot[1].item()) + 16, self.dev)
         else:
+            if S.readouts is not None:
+                S.readouts.record_stream(st)
             S.readouts = None
         _native.check(L.sfg_apply(hp, ctypes.byref(cd), n, S.children.data_ptr(), S.vals.data_ptr(),
                                   S.work_base.data_ptr(), S.work.data_ptr(), s), "apply")
@@ -419,12 +431,15 @@ class DeviceCampaign:
         cw = CHILD.itemsize // 8
         self._scan64(S, S.children.view(torch.int64), n, cw, CHILD.fields["work_bytes"][1] // 8, S.work_base, 0)
         S.ensure_work(n * self.max_entry_work + 64, self.dev)
-        S.readouts = None
         if self.diff:
             self._scan64(S, S.children.view(torch.int64), n, cw, CHILD.fields["readout_bytes"][1] // 8, S.ro_base, 1)
             with torch.cuda.stream(st):
                 S.tot[:2].cpu()
-            S.readouts = self._u8(int(S.tot[1].item()) + 16)
+            S.readouts = S.alloc_on_stream(S.readouts, int(S.tot[1].item()) + 16, self.dev)
+        else:
+            if S.readouts is not None:
+                S.readouts.record_stream(st)
+            S.readouts = None
         _native.check(L.sfg_apply(hp, ctypes.byref(cd), n, S.children.data_ptr(), S.vals.data_ptr(),
                                   S.work_base.data_ptr(), S.work.data_ptr(), s), "apply")
         self._execute(S, n, self.soft_cap, cd)
@@ -600,6 +615,12 @@ class DeviceCampaign:
         T = int(per_rank.sum())
         mx = int(per_rank.max())
         self.launches += 1
+        with torch.cuda.stream(st):   # temporaries in the slot stream's pool: reuse is stream-ordered
+            return self._admit_on_stream(S, per_rank, A, CB, VB, mine, T, mx)
+
+    def _admit_on_stream(self, S, per_rank, A, CB, VB, mine, T, mx):
+        L, hp, st, comm = self.L, self.h, S.stream, self.comm
+        s = st.cuda_stream
         stage = self._u8(max(mx, 1) * (CB + VB))
         _native.check(L.sfg_select(hp, S.children.data_ptr(), S.vals.data_ptr(), S.admit.data_ptr(),
                                    S.pos.data_ptr(), S.n, stage.data_ptr(), stage.data_ptr() + max(mx, 1) * CB, s),

@@ -111,8 +111,7 @@ M_KINDS = ("int_boundary", "int_byte", "float_sign", "float_exponent", "float_ma
 M_INDEX = {k: i for i, k in enumerate(M_KINDS)}
 
 
-class LoweringError(Exception):
-    """The harness uses a construct this device path does not lower."""
+from .baseline import LoweringError  # noqa: E402,F401  (the harness uses a construct this path does not lower)
 
 
 def wrap_i32(v: int) -> int:
@@ -497,6 +496,11 @@ def pack_values(tc: TestCase, specs):
             vals[j]["ext"][:len(v.extents)] = v.extents
             vals[j]["count"] = v.count
             vals[j]["nbytes"] = len(v.data)
+            if not -(1 << 40) < v.base_offset < (1 << 40):
+                # the specialized kernels keep pointer registers in 64 bits when the
+                # pointer parameters (base + base_offset) stay below 2^40 (jit.cu narrow_ok);
+                # mutation keeps offsets within 2 * max(len, 4) (mutation.py:338-347)
+                raise LoweringError(f"array base_offset {v.base_offset} outside +-2^40 is not lowered")
             vals[j]["base_offset"] = v.base_offset
             vals[j]["size_override"] = NO_OVERRIDE if v.size_override is None else v.size_override
             vals[j]["data_off"] = len(payload)

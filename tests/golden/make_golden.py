@@ -131,7 +131,7 @@ def sampled():
 
 
 def batched(m, *, master_seed, iterations, round_size, stop_bug_class=None,
-            stop_on_first_finding=False, extra_seeds=(), fanout=0, hooks=None):
+            stop_on_first_finding=False, extra_seeds=(), fanout=0, hooks=None, budget=1_000_000):
     """Batched-round contract on the reference's own functions.  fanout > 0: input
     it mutates round-corpus entry ((it - 1) // fanout) % len (no scheduling draw)."""
     specs = m.argspecs
@@ -144,7 +144,7 @@ def batched(m, *, master_seed, iterations, round_size, stop_bug_class=None,
     gcov = CoverageMap.for_program(m.program)
     sched = MutationSchedule()
     image = DeviceMemoryImage(rng=Stream(master_seed, 2000))
-    runner = rc.PhaseRunner(m, image, hooks=hooks)
+    runner = rc.PhaseRunner(m, image, hooks=hooks, instruction_budget=budget)
     assert runner.run_phase(rc.INIT, seed_tc, iteration=0).status == "ok"
     runner.mark_baseline()
     snap = image.snapshot()
@@ -327,6 +327,111 @@ def errors(tmp):
                                                  **out[k]} for k, v in ERROR_CASES.items()}}
 
 
+# Long pure-register loops (the JIT's loop summaries, csrc/jit.cu analyse_cycle):
+# exits by == / != / <= / > compares of wrapping i32 induction variables, and
+# budget exhaustion at every position of the loop body (budgets 10^6 + k).
+LOOP_SIR = """\
+kernel spin(out:ptr.global, x:i32, step:i32, lim:i32, stop:i32) regs=8
+  mov %r5, 0
+top:
+  setp.eq %p1, %r0, %r3
+  bra %p1, hit
+  add %r0, %r0, %r1
+  sub %r5, %r5, -1
+  setp.gt %p0, %r5, %r2
+  bra %p0, fin
+  bra top
+hit:
+  st.global.b32 [%a0], %r5
+  exit
+fin:
+  st.global.b32 [%a0+4], %r0
+  exit
+
+kernel spin2(out:ptr.global, x:i32, step:i32, lim:i32, stop:i32) regs=8
+  mov %r6, 7
+again:
+  add %r0, %r0, %r1
+  setp.ne %p2, %r0, %r3
+  bra !%p2, found
+  mov %r6, 9
+  setp.le %p3, %r0, %r2
+  bra !%p3, again
+  st.global.b32 [%a0+8], %r6
+  exit
+found:
+  st.global.b32 [%a0+12], %r0
+  exit
+"""
+
+
+def loop_manifest(kernel: str) -> str:
+    return ("program loops.sir\n\n"
+            "argspec out ptr global i32 count=4 seed=zeros lo=0 hi=9\n"
+            "argspec x i32 seed=0 lo=-100 hi=100\n"
+            "argspec step i32 seed=8 lo=-9 hi=9\n"
+            "argspec lim i32 seed=400 lo=0 hi=1000\n"
+            "argspec stop i32 seed=4000 lo=0 hi=1000\n\n"
+            "compute:\n"
+            f"  launch {kernel} grid=1 block=2 args=arg:0,arg:1,arg:2,arg:3,arg:4\n"
+            "  copy_out arg:0\n")
+
+
+M31 = (1 << 31) - 1
+LOOP_INPUTS = {
+    # (x, step, lim, stop)
+    "spin": [(0, 8, 10 ** 9, 8 * 50000), (5, 0x10000001, 10 ** 9, (5 + 1000 * 0x10000001) & 0xFFFFFFFF),
+             (0, 3, 200000, 1), (0, 0, M31, 1), (-(1 << 31) + 100, -7, 10 ** 9, 2000000),
+             (7, 1, 30000, 30007 + 1), (0, -1, 10 ** 6, -123457)],
+    "spin2": [(M31, -1, M31 - 100000, -5), (M31, -1, M31 - 300000, -5), (100, 1, 50, -7),
+              (100, 0x7FFFFFFF, 50, 3), (0, 4, -100, 400000), (-5, 3, -10, 2 ** 31 - 2)],
+}
+LOOP_BUDGETS = [10 ** 6 + k for k in range(7)] + [200003]
+MATMUL_LOOPS = [(M31, 0), (M31, -8), (400000, 0), (M31, -(1 << 31))]   # (m, n)
+LOOP_CAMPAIGN = dict(master_seed=7, iterations=2048, round_size=512, budget=50000)
+
+
+def loops():
+    from simt_forge.mutation import IntValue
+    import tempfile
+    out = {"kernel": LOOP_SIR, "manifests": {}, "inputs": {}, "campaigns": {}, "campaign_config": LOOP_CAMPAIGN,
+           "budgets": LOOP_BUDGETS}
+    with tempfile.TemporaryDirectory() as tmp:
+        (Path(tmp) / "loops.sir").write_text(LOOP_SIR)
+        cases = []
+        for kern in ("spin", "spin2"):
+            man = loop_manifest(kern)
+            out["manifests"][kern] = man
+            (Path(tmp) / f"{kern}.man").write_text(man)
+            m = rc.load_harness(Path(tmp) / f"{kern}.man")
+            seed = m.seed(1)
+            for vals in LOOP_INPUTS[kern]:
+                args = (seed.args[0],) + tuple(IntValue(v) for v in vals)
+                cases.append((kern, m, TestCase(args, seed.rng_seed)))
+        mm = rc.load_harness(REPO / "paper_2603_05725_b200" / "workloads" / "matmul.man")
+        for mv, nv in MATMUL_LOOPS:
+            s = mm.seed(1)
+            args = list(s.args)
+            args[3], args[4] = IntValue(mv), IntValue(nv)
+            cases.append(("matmul", mm, TestCase(tuple(args), s.rng_seed)))
+        for budget in LOOP_BUDGETS:
+            for kern, m, tc in cases:
+                image = DeviceMemoryImage()
+                runner = rc.PhaseRunner(m, image, instruction_budget=budget, diff_readback=True)
+                runner.run_phase(rc.INIT, m.seed(1), iteration=0)
+                runner.mark_baseline()
+                cov = CoverageMap.for_program(m.program)
+                res = runner.run_phase(rc.COMPUTE, tc, coverage=cov, iteration=1)
+                out["inputs"].setdefault(kern, []).append({
+                    "budget": budget, "testcase": serialize_testcase(tc, with_id=False), "status": res.status,
+                    "retired": res.retired, "report": res.report.to_line() if res.report else None,
+                    "readouts": {k: v.hex() for k, v in res.readouts.items()}, "edges": edges_json(cov)})
+        for kern in ("spin", "spin2"):
+            m = rc.load_harness(Path(tmp) / f"{kern}.man")
+            out["campaigns"][kern] = batched(m, **LOOP_CAMPAIGN)
+    return out
+
+
 def _dump(obj) -> str:
     return json.dumps(obj, sort_keys=True, separators=(",", ":"))
 
@@ -334,7 +439,7 @@ def _dump(obj) -> str:
 def main():
     import tempfile
     which = sys.argv[1:] or ["assets", "variants", "sampled", "batched", "fuzzloop", "workloads", "traces",
-                             "errors"]
+                             "errors", "loops"]
     if "assets" in which:
         (HERE / "bench_assets.json").write_text(_dump(assets()))
     if "variants" in which:
@@ -351,6 +456,8 @@ def main():
         (HERE / "ref_workloads.json").write_text(_dump(workloads()))
     if "traces" in which:
         (HERE / "ref_traces.json").write_text(_dump(traces()))
+    if "loops" in which:
+        (HERE / "ref_loops.json").write_text(_dump(loops()))
     if "errors" in which:
         with tempfile.TemporaryDirectory() as tmp:
             (HERE / "ref_errors.json").write_text(_dump(errors(tmp)))
