@@ -72,6 +72,9 @@ size_t sfg_program_jit_source(const sfg_program* p, char* buf, size_t cap);
  * loading it (no GPU needed).  out receives the source (and log on failure). */
 int sfg_jit_check(const void* prog, size_t prog_bytes, const void* ins, uint64_t max_edge_events, char* out,
                   size_t cap, size_t* cubin_bytes);
+/* Process-wide counts of NVRTC compiles and of programs loaded from the on-disk
+ * cubin cache ($SFG_JIT_CACHE, default ~/.cache/sfg_b200_jit; "0" disables). */
+void sfg_jit_stats(int* compiles, int* disk_hits);
 
 int sfg_plan(const sfg_program* p, const sfg_corpus_dev* c, int64_t it0, int n, int32_t* parent,
              int8_t* picks, uint32_t* int_flags, void* stream);
@@ -119,13 +122,13 @@ int sfg_regen(const sfg_program* p, const sfg_corpus_dev* c, int n_sel, const in
  * sequential execution (executor.py:405-424). */
 int sfg_execute(const sfg_program* p, int n, const void* children, const void* vals,
                 const uint64_t* work_base, uint8_t* work, void* verdicts, uint32_t* edge_counts,
-                uint8_t* readouts, const uint64_t* readout_base, uint64_t* overlay, int* work_counter,
+                uint8_t* readouts, const uint64_t* readout_base, int* work_counter,
                 uint64_t soft_cap, int32_t* deferred, int64_t max_work_bytes, const int32_t* order,
                 void* stream);
 int sfg_execute_deferred(const sfg_program* p, const sfg_corpus_dev* c, int n, const void* children,
                          const void* vals, const uint64_t* work_base, uint8_t* work, void* verdicts,
                          uint32_t* edge_counts, uint8_t* readouts, const uint64_t* readout_base,
-                         uint64_t* overlay, int* work_counter, int32_t* deferred, int64_t max_work_bytes,
+                         int* work_counter, int32_t* deferred, int64_t max_work_bytes,
                          void* stream);
 /* Trace mode (replaces the reference's ExecHooks / TraceHooks per event,
  * executor.py:108-135, cli.py:42-45): run the inputs through the generic
@@ -134,7 +137,7 @@ int sfg_execute_deferred(const sfg_program* p, const sfg_corpus_dev* c, int n, c
  * csrc/execute.cu); trace_count[i] = events produced (> trace_cap: truncated). */
 int sfg_execute_trace(const sfg_program* p, int n, const void* children, const void* vals,
                       const uint64_t* work_base, uint8_t* work, void* verdicts, uint32_t* edge_counts,
-                      uint8_t* readouts, const uint64_t* readout_base, uint64_t* overlay, uint64_t* trace,
+                      uint8_t* readouts, const uint64_t* readout_base, uint64_t* trace,
                       uint32_t trace_cap, uint32_t* trace_count, void* stream);
 /* A non-blocking CUDA stream (cudaStreamCreateWithPriority).  The Python host keeps
  * one process-wide ring of them, created back to back, so that each round in

@@ -15,12 +15,20 @@ records the result as
 
 This replaces the per-iteration ``image.restore(snapshot)`` of the reference
 loop (``campaign.py:729-736``): on the device every input starts from these
-immutable tables.  INIT launches are not lowered (no bundled harness has one).
+immutable tables.
+
+INIT launches run on the device (``init_launch``, supplied by the engine): the
+launch's array arguments are materialized here first, exactly as
+``PhaseRunner._bind_launch``/``_materialize`` would (campaign.py:440-479: in
+binding order, fresh ids, the seed's bytes), so that every byte the launch can
+touch is an allocation record of the state so far; the engine runs the launch
+on a one-input device program over that state and returns the final bytes of
+every live record, which become the records' data.
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 
@@ -109,7 +117,14 @@ def _up(n: int, a: int) -> int:
     return (n + a - 1) // a * a
 
 
-def build_baseline(manifest, seed_tc, mem: MemConfig) -> Baseline:
+INTERNAL_ARG = "\0arg{}"    # named handle of an array argument materialized by an INIT launch
+
+
+def build_baseline(manifest, seed_tc, mem: MemConfig, init_launch=None) -> Baseline:
+    """``init_launch(op, state, names) -> {name: bytes}`` runs one INIT launch on the
+    device over ``state`` (a Baseline of everything so far) and returns the final
+    payload of each named live record in ``names``; it raises InitFailure when the
+    launch stops on a finding or the budget."""
     recs: list[Record] = []
     cursor = {sp: 0 for sp in SPACE_ORDER}
     qbytes = {sp: 0 for sp in SPACE_ORDER}
@@ -118,11 +133,41 @@ def build_baseline(manifest, seed_tc, mem: MemConfig) -> Baseline:
     named: dict = {}
     next_id = 1
 
+    materialized: dict = {}        # arg index -> record index (INIT launches)
+
     def live_at(addr: int, n: int):
         for j, r in enumerate(recs):
             if r.resident and not r.freed and r.base <= addr and addr + n <= r.base + r.size:
                 return j
         return None
+
+    def alloc(sp, size: int, label: str) -> int:
+        """_alloc_common (device_memory.py:407-440), scope 0; size 0 = alloc_empty."""
+        nonlocal next_id
+        slot = mem.redzone + _up(size, mem.granule) + mem.redzone
+        cands = [k for k, e in enumerate(free) if e[1] == slot and e[2] == sp]
+        if cands:
+            k = min(cands, key=lambda j: free[j][0])
+            off = free.pop(k)[0]
+        else:
+            if cursor[sp] + slot > mem.scope_size(sp):
+                raise OutOfSpaceError(f"{sp.value} scope 0: need {slot} bytes, "
+                                      f"{mem.scope_size(sp) - cursor[sp]} remain")
+            off = cursor[sp]
+            cursor[sp] += slot
+        start = SPACE_BASE[sp] + off
+        recs.append(Record(next_id, sp, start + mem.redzone, size, start, start + slot, label,
+                           data=bytearray(size)))
+        next_id += 1
+        return len(recs) - 1
+
+    def state() -> Baseline:
+        blob, phys = bytearray(), []
+        for r in recs:
+            phys.append(len(blob))
+            blob += r.data + bytes((-len(r.data)) % 16)
+        return Baseline(list(recs), dict(named), dict(cursor), dict(qbytes), list(quar), list(free), next_id,
+                        bytes(blob) or b"\0", phys)
 
     for op in manifest.phases[INIT]:
         if op.kind == "sync":
@@ -130,23 +175,8 @@ def build_baseline(manifest, seed_tc, mem: MemConfig) -> Baseline:
         if op.kind == "alloc":
             if op.size <= 0:
                 raise InitFailure(f"allocation size must be positive, got {op.size}")
-            sp = op.space
-            slot = mem.redzone + _up(op.size, mem.granule) + mem.redzone
-            cands = [k for k, e in enumerate(free) if e[1] == slot and e[2] == sp]
-            if cands:
-                k = min(cands, key=lambda j: free[j][0])
-                off = free.pop(k)[0]
-            else:
-                if cursor[sp] + slot > mem.scope_size(sp):
-                    raise OutOfSpaceError(f"{sp.value} scope 0: need {slot} bytes, "
-                                          f"{mem.scope_size(sp) - cursor[sp]} remain")
-                off = cursor[sp]
-                cursor[sp] += slot
-            start = SPACE_BASE[sp] + off
-            recs.append(Record(next_id, sp, start + mem.redzone, op.size, start, start + slot, op.name,
-                               data=bytearray(op.size)))
-            named[op.name] = (start + mem.redzone, next_id, len(recs) - 1)
-            next_id += 1
+            j = alloc(op.space, op.size, op.name)
+            named[op.name] = (recs[j].base, recs[j].alloc_id, j)
         elif op.kind == "copy_in":
             addr = named[op.name][0]
             form, payload = op.source
@@ -169,7 +199,12 @@ def build_baseline(manifest, seed_tc, mem: MemConfig) -> Baseline:
             r = recs[j]
             r.data[addr - r.base:addr - r.base + len(data)] = data
         elif op.kind == "copy_out":
-            if op.arg_ref >= 0:
+            if op.arg_ref >= 0:       # only after an INIT launch materialized it (campaign.py:517-520)
+                if op.arg_ref in materialized:
+                    r = recs[materialized[op.arg_ref]]
+                    n = len(seed_tc.args[op.arg_ref].data)
+                    if n and live_at(r.base, n) is None:
+                        raise InitFailure("init phase failed on the seed input: finding")
                 continue
             addr = named[op.name][0]
             if op.size and live_at(addr, op.size) is None:
@@ -190,13 +225,53 @@ def build_baseline(manifest, seed_tc, mem: MemConfig) -> Baseline:
                 free.append((v.slot_start - SPACE_BASE[v.space], v.slot_end - v.slot_start, v.space))
                 qbytes[v.space] -= v.slot_end - v.slot_start
         elif op.kind == "launch":
-            raise LoweringError("INIT-phase launches are not lowered to the device path")
+            if init_launch is None:
+                raise LoweringError("INIT-phase launches need the device (init_launch)")
+            binds = []
+            for b in op.bindings:
+                v = seed_tc.args[b[1]] if b[0] == "arg" else None
+                if isinstance(v, ArrayValue):      # _bind_launch / _materialize, binding order
+                    k = b[1]
+                    if v.base_offset:
+                        raise LoweringError("INIT launch of an array with a base offset")
+                    if k not in materialized:
+                        size = v.size_override if v.size_override is not None else len(v.data)
+                        j = alloc(v.space, max(size, 0), f"arg{k}")
+                        if size > 0:
+                            recs[j].data[:] = v.data[:size]
+                        materialized[k] = j
+                        named[INTERNAL_ARG.format(k)] = (recs[j].base, recs[j].alloc_id, j)
+                    binds.append(("buf", INTERNAL_ARG.format(k)))
+                else:
+                    binds.append(b)
+            live = [n for n, (_, _, j) in named.items() if recs[j].resident and not recs[j].freed]
+            out = init_launch(replace(op, bindings=tuple(binds)), state(), live)
+            for n, data in out.items():
+                r = recs[named[n][2]]
+                r.data[:] = data
     blob = bytearray()
     phys = []
     for r in recs:
         phys.append(len(blob))
         blob += r.data + bytes((-len(r.data)) % 16)
     return Baseline(recs, named, cursor, qbytes, quar, free, next_id, bytes(blob) or b"\0", phys)
+
+
+def term_frees_clean(b: Baseline, term_ops) -> bool:
+    """A TERM script of frees (and syncs) only, on the post-INIT state, frees live
+    allocations or skips already-freed ones (campaign.py:538-541) -- no report.
+    Anything else is run on the device (engine.DeviceCampaign.run_term)."""
+    seen = set()
+    for op in term_ops:
+        if op.kind == "sync":
+            continue
+        if op.kind != "free" or op.name not in b.named or op.name in seen:
+            return False     # (a repeated free may meet an evicted record: the device decides)
+        seen.add(op.name)
+        addr = b.named[op.name][0]
+        if not any(r.resident and r.base == addr for r in b.records):
+            return False
+    return True
 
 
 def record_table(b: Baseline, labels: list):

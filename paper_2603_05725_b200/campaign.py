@@ -150,9 +150,9 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
     if config.discipline not in ("batched", "sequential"):
         raise CampaignFatalError(f"unknown discipline {config.discipline!r}")
     hooks = config.hooks
-    for op in manifest.phases["term"]:
-        if op.kind not in ("free", "sync"):
-            raise LoweringError("TERM phases other than frees are not lowered")
+    if config.mode == "reinit" and any(op.kind not in ("free", "sync") for op in manifest.phases["term"]):
+        # reinit runs TERM after every input on that input's post-COMPUTE state
+        raise LoweringError("reinit mode: TERM phases other than frees are not lowered")
     out_dir = Path(config.out_dir) if config.out_dir is not None else None
     specs = manifest.argspecs
     if out_dir is not None:
@@ -237,7 +237,11 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
             if state["stop"] is not None:
                 stop_reason = state["stop"]
             if config.mode == "amortized":
+                # TERM once per worker on the restored state (campaign.py:756-762)
+                rep = dc.run_term()
                 term_runs += 1
+                if rep is not None and dc.findings.add(rep) and out_dir is not None:
+                    _write_crash(out_dir, rep, dc.seed_tc, specs, manifest)
     except CampaignFatalError:
         if out_dir is not None:
             (out_dir / "FAILED").write_text("campaign fatal\n")

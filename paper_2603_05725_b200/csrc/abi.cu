@@ -34,6 +34,8 @@ struct sfg_program {
   uint8_t* const_blob;
   const uint8_t* base_blob;  // caller-owned device buffer
   size_t smem;
+  int gen_warps = 4;                  // warps per block of the generic interpreter
+  bool gen_ok = true;                 // its shared memory fits
 };
 
 static_assert(sizeof(sfg_ins) == 32, "sfg_ins layout");
@@ -164,12 +166,14 @@ static cudaError_t dupe(T** dst, const void* src, size_t count) {
   return cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice);
 }
 
-static size_t exec_smem(const sfg_prog& P) {
+// generic interpreter: instructions + per warp register files and edge counters
+static size_t exec_smem(const sfg_prog& P, int warps) {
   int maxregs = 1;
   for (int k = 0; k < P.n_kernels; ++k) maxregs = P.kernels[k].regs > maxregs ? P.kernels[k].regs : maxregs;
   const size_t ins = ((size_t)P.total_ins * sizeof(sfg_ins) + 15) & ~(size_t)15;
-  return ins + 4 * (size_t)32 * (maxregs * 24 + P.n_edges * 4);
+  return ins + (size_t)warps * 32 * (maxregs * 24 + P.n_edges * 4);
 }
+constexpr int kGenSmemMax = 227 * 1024;
 
 template <typename T>
 static int scan_impl(const T* in, int64_t n, int stride, int col, uint64_t* out, int out_stride, int out_col,
@@ -233,9 +237,12 @@ int sfg_program_create(const void* prog, size_t prog_bytes, const void* ins, siz
     return fail("sfg_program_create", e);
   }
   p->base_blob = (const uint8_t*)base_blob_dev;
-  p->smem = exec_smem(p->P);
+  // warps per block of the generic interpreter: as many (<= 4) as fit in shared memory
+  p->gen_warps = 4;
+  while (p->gen_warps > 1 && exec_smem(p->P, p->gen_warps) > (size_t)kGenSmemMax) --p->gen_warps;
+  p->smem = exec_smem(p->P, p->gen_warps);
   const char* jit_env = getenv("SFG_JIT");
-  if (!(jit_env && jit_env[0] == '0')) {
+  if (!(jit_env && jit_env[0] == '0') && !p->P.jit_off) {
     // bound on per-input edge events decides whether counters need overflow checks
     uint64_t events = 0;
     const sfg_hostop* H = (const sfg_hostop*)hostops;
@@ -320,10 +327,17 @@ int sfg_program_create(const void* prog, size_t prog_bytes, const void* ins, siz
     p->tail_grid = sms * per_sm;
 
   }
-  e = cudaFuncSetAttribute(sfg_execute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem);
-  if (e != cudaSuccess) {
+  // the generic interpreter (trace mode, one-input INIT/TERM programs) needs its
+  // register files in shared memory; with the JIT a program too large for it still
+  // runs (sfg_execute_trace then fails)
+  e = p->smem <= (size_t)kGenSmemMax
+          ? cudaFuncSetAttribute(sfg_execute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem)
+          : cudaErrorInvalidValue;
+  p->gen_ok = e == cudaSuccess;
+  if (!p->gen_ok && !p->jit_kernel) {
     sfg_program_destroy(p);
-    return fail("sfg_program_create: execute smem", e);
+    g_err = "sfg_program_create: the program's registers / edges exceed the interpreter's shared memory";
+    return 1;
   }
   *out = p;
   return 0;
@@ -350,6 +364,11 @@ void sfg_program_destroy(sfg_program* p) {
 }
 
 size_t sfg_execute_smem_bytes(const sfg_program* p) { return p->smem; }
+
+void sfg_jit_stats(int* compiles, int* disk_hits) {
+  if (compiles) *compiles = jit_compiles;
+  if (disk_hits) *disk_hits = jit_disk_hits;
+}
 
 int sfg_jit_check(const void* prog, size_t prog_bytes, const void* ins, uint64_t max_edge_events, char* out,
                   size_t cap, size_t* cubin_bytes) {
@@ -481,7 +500,7 @@ int sfg_order(const sfg_program* p, int n, const void* vals, int32_t* order, int
 
 int sfg_execute(const sfg_program* p, int n, const void* children, const void* vals, const uint64_t* work_base,
                 uint8_t* work, void* verdicts, uint32_t* edge_counts, uint8_t* readouts,
-                const uint64_t* readout_base, uint64_t* overlay, int* work_counter, uint64_t soft_cap,
+                const uint64_t* readout_base, int* work_counter, uint64_t soft_cap,
                 int32_t* deferred, int64_t max_work_bytes, const int32_t* order, void* stream) {
   if (n <= 0) {
     if (work_counter) cudaMemsetAsync(work_counter, 0, 8 * sizeof(int), S(stream));
@@ -489,7 +508,7 @@ int sfg_execute(const sfg_program* p, int n, const void* children, const void* v
   }
   ExecView E{p->ins, p->hostops, p->binds, p->recs, p->base_blob, p->const_blob,
              (const sfg_child*)children, (const sfg_val*)vals, work_base, work,
-             (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, overlay, n,
+             (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, n,
              0ull, deferred, work_counter ? work_counter + 1 : nullptr,
              deferred ? deferred + n : nullptr, work_counter ? work_counter + 3 : nullptr, 1, 0, order,
              nullptr, 0, nullptr};
@@ -531,33 +550,41 @@ int sfg_execute(const sfg_program* p, int n, const void* children, const void* v
     return 0;
   }
   if (work_counter) cudaMemsetAsync(work_counter, 0, 8 * sizeof(int), S(stream));
-  sfg_execute_kernel<<<blocks_for(n, 128), 128, p->smem, S(stream)>>>(p->P, E);
+  if (!p->gen_ok) {
+    g_err = "the program's registers / edges exceed the generic interpreter's shared memory";
+    return 1;
+  }
+  sfg_execute_kernel<<<blocks_for(n, 32 * p->gen_warps), 32 * p->gen_warps, p->smem, S(stream)>>>(p->P, E);
   SFG_CHECK_LAUNCH("sfg_execute");
   return 0;
 }
 
 int sfg_execute_trace(const sfg_program* p, int n, const void* children, const void* vals, const uint64_t* work_base,
                       uint8_t* work, void* verdicts, uint32_t* edge_counts, uint8_t* readouts,
-                      const uint64_t* readout_base, uint64_t* overlay, uint64_t* trace, uint32_t trace_cap,
+                      const uint64_t* readout_base, uint64_t* trace, uint32_t trace_cap,
                       uint32_t* trace_count, void* stream) {
   if (n <= 0) return 0;
   ExecView E{p->ins, p->hostops, p->binds, p->recs, p->base_blob, p->const_blob,
              (const sfg_child*)children, (const sfg_val*)vals, work_base, work,
-             (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, overlay, n,
+             (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, n,
              0ull, nullptr, nullptr, nullptr, nullptr, 1, 0, nullptr, trace, trace_cap, trace_count};
-  sfg_execute_kernel<<<blocks_for(n, 128), 128, p->smem, S(stream)>>>(p->P, E);
+  if (!p->gen_ok) {
+    g_err = "the program's registers / edges exceed the generic interpreter's shared memory";
+    return 1;
+  }
+  sfg_execute_kernel<<<blocks_for(n, 32 * p->gen_warps), 32 * p->gen_warps, p->smem, S(stream)>>>(p->P, E);
   SFG_CHECK_LAUNCH("sfg_execute_trace");
   return 0;
 }
 
 int sfg_execute_deferred(const sfg_program* p, const sfg_corpus_dev* c, int n, const void* children,
                          const void* vals, const uint64_t* work_base, uint8_t* work, void* verdicts,
-                         uint32_t* edge_counts, uint8_t* readouts, const uint64_t* readout_base, uint64_t* overlay,
+                         uint32_t* edge_counts, uint8_t* readouts, const uint64_t* readout_base,
                          int* work_counter, int32_t* deferred, int64_t max_work_bytes, void* stream) {
   if (n <= 0 || !p->jit_kernel) return 0;  // the interpreter never defers
   ExecView E{p->ins, p->hostops, p->binds, p->recs, p->base_blob, p->const_blob,
              (const sfg_child*)children, (const sfg_val*)vals, work_base, work,
-             (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, overlay, n,
+             (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, n,
              0ull, deferred, work_counter + 1, deferred + n, work_counter + 3, p->group, 0, nullptr,
              nullptr, 0, nullptr};
   for (int pass = 0; pass < 2; ++pass) {

@@ -16,7 +16,10 @@
 //     shadow == f(registry, quarantine)), so nothing is staged per granule;
 //   * payload bytes: the input's materialized arrays and COMPUTE allocs live in
 //     its work region (written by sfg_apply_kernel); INIT buffers are read from
-//     the shared baseline blob with a per-input byte overlay for writes.
+//     the shared baseline blob; a write copies the touched 256-byte chunk into
+//     the input's copy-on-write overlay at the tail of its work region first
+//     (the reference's dirty-chunk restore, device_memory.py:551-618, becomes
+//     "start every input with an empty overlay").
 //   * simulated register files live in shared memory, [reg][lane] so that a
 //     converged warp touches 32 consecutive banks; per-edge hit counters too.
 //
@@ -72,7 +75,6 @@ struct ExecView {
   uint32_t* edge_counts;       // [n][n_edges]
   uint8_t* readouts;
   const uint64_t* readout_base;
-  uint64_t* overlay;           // [n][SFG_OVERLAY] packed (addr << 8 | byte)
   int n;
   // long-input deferral (specialized kernel only): an input whose retired count
   // would reach soft_cap is abandoned and appended to deferred[] (count in
@@ -254,14 +256,16 @@ SFG_DEV void oos_detail(const sfg_prog& P, const Lane& L, sfg_verdict& V, int sp
   V.alloc_base = P.scope_size[sp] - L.cursor[sp];
 }
 
-// free (device_memory.py:442-487); returns 0 ok, 1 invalid free, -status fatal
+// free (device_memory.py:442-487); returns 0 ok, 1 invalid free, 2 invalid free of an
+// allocation already freed, -status fatal
 SFG_DEV int lane_free(const sfg_prog& P, Lane& L, int64_t addr) {
   const int sp = space_of(P, addr);
   if (sp < 0) return 1;
   int k = -1;
   for (int j = 0; j < L.nrec; ++j)
     if ((L.rec[j].flags & R_RES) && L.rec[j].space == sp && L.rec[j].base == addr) k = j;
-  if (k < 0 || (L.rec[k].flags & R_FREED)) return 1;
+  if (k < 0) return 1;
+  if (L.rec[k].flags & R_FREED) return 2;
   LRec& r = L.rec[k];
   r.flags |= R_FREED;
   if (L.nq >= kMaxQ) return -SFG_ST_LANE_RECS;
@@ -288,16 +292,23 @@ SFG_DEV int lane_free(const sfg_prog& P, Lane& L, int64_t addr) {
 struct Mem {
   const ExecView* E;
   uint8_t* work;               // this input's work region
-  const uint8_t* blob;
-  uint64_t* ov;                // this input's overlay entries
+  const uint8_t* blob;         // baseline payloads, padded to a multiple of SFG_OV_CHUNK
+  int64_t* ov_idx;             // copy-on-write overlay: blob chunk index of each copied chunk
+  uint8_t* ov_data;            // ... and the chunks (ov_cap of them)
+  int ov_cap;
 };
 
+// overlay slot holding blob chunk c, or -1
+SFG_DEV int ov_find(const Mem& M, const Lane& L, int64_t c) {
+  for (int k = 0; k < L.nov; ++k)
+    if (M.ov_idx[k] == c) return k;
+  return -1;
+}
+
 SFG_DEV uint8_t base_byte(const Mem& M, const Lane& L, const LRec& r, int64_t a) {
-  for (int k = L.nov - 1; k >= 0; --k) {
-    const uint64_t e = M.ov[k];
-    if ((int64_t)(e >> 8) == a) return (uint8_t)e;
-  }
-  return M.blob[r.phys + (a - r.base)];
+  const int64_t o = r.phys + (a - r.base);
+  const int k = L.nov ? ov_find(M, L, o / SFG_OV_CHUNK) : -1;
+  return k >= 0 ? M.ov_data[(size_t)k * SFG_OV_CHUNK + (o % SFG_OV_CHUNK)] : M.blob[o];
 }
 
 SFG_SLOW uint64_t mem_read(const Mem& M, const Lane& L, const LRec& r, int64_t a, int w) {
@@ -330,9 +341,21 @@ SFG_SLOW bool mem_write(const Mem& M, Lane& L, const LRec& r, int64_t a, int w, 
     for (int k = 0; k < w; ++k) p[k] = (uint8_t)(v >> (8 * k));
     return true;
   }
+  // INIT buffer: write into the input's copy of the touched chunk (copied on first
+  // write); false = the overlay is full (the host grows ov_cap and re-runs the round)
   for (int k = 0; k < w; ++k) {
-    if (M.ov == nullptr || L.nov >= SFG_OVERLAY) return false;
-    M.ov[L.nov++] = ((uint64_t)(a + k) << 8) | ((v >> (8 * k)) & 0xFF);
+    const int64_t o = r.phys + (a + k - r.base);
+    const int64_t c = o / SFG_OV_CHUNK;
+    int j = ov_find(M, L, c);
+    if (j < 0) {
+      if (L.nov >= M.ov_cap) return false;
+      j = L.nov++;
+      M.ov_idx[j] = c;
+      const uint4* src = reinterpret_cast<const uint4*>(M.blob + c * SFG_OV_CHUNK);
+      uint4* dst = reinterpret_cast<uint4*>(M.ov_data + (size_t)j * SFG_OV_CHUNK);
+      for (int q = 0; q < SFG_OV_CHUNK / 16; ++q) dst[q] = src[q];
+    }
+    M.ov_data[(size_t)j * SFG_OV_CHUNK + (o % SFG_OV_CHUNK)] = (uint8_t)(v >> (8 * k));
   }
   return true;
 }
@@ -628,7 +651,13 @@ SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R, c
   uint64_t t_start;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   Lane L;
-  Mem M{&E, E.work + E.work_base[i], E.base_blob, E.overlay ? E.overlay + (size_t)i * SFG_OVERLAY : nullptr};
+  const uint64_t ovb = sfg_ov_bytes(P.ov_cap);
+  uint8_t* wk = E.work + E.work_base[i];
+  uint64_t pri_tot = 0;
+  if (P.copy_src_mask) sfg_pristine_off(&P, cv, ch.work_bytes, 0, &pri_tot);
+  int64_t* ovi = reinterpret_cast<int64_t*>(wk + ch.work_bytes - pri_tot - ovb);
+  Mem M{&E, wk, E.base_blob, ovi, reinterpret_cast<uint8_t*>(ovi) + (((uint64_t)P.ov_cap * 8ull + 15ull) & ~15ull),
+        P.ov_cap};
   sfg_verdict V{};
   V.status = SFG_ST_OK;
   V.key = -1;
@@ -659,7 +688,7 @@ SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R, c
   R.set_input(E, i);
   uint64_t total_retired = 0;
   uint8_t* ro = (P.diff_readback && E.readouts) ? E.readouts + E.readout_base[i] : nullptr;
-  const uint64_t arrays_end = ch.work_bytes - (uint64_t)P.named_work_bytes;
+  const uint64_t arrays_end = ch.work_bytes - (uint64_t)P.named_work_bytes - ovb - pri_tot;
   const int ntags = (int)((ch.work_bytes + 3) / 4);
   int defer_kind = 0;  // 1: soft cap reached (deferred), 2: re-run thread-sequentially (deferred_seq)
   int seq_reruns = 0;  // group-parallel chunks undone and re-run sequentially (diagnostics)
@@ -683,9 +712,15 @@ SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R, c
       const int64_t addr = L.named_addr[op.buf];
       int64_t len = op.size;
       const sfg_val* src_v = nullptr;
+      const uint8_t* src_p = nullptr;   // array source: its pristine copy
       if (op.src_form == SFG_SRC_ARG) {
         src_v = &cv[op.src_arg];
-        len = 4;  // scalar args only (lowering rejects array sources)
+        if (src_v->kind == SFG_V_ARR) {   // value.data (campaign.py:404-409)
+          len = src_v->nbytes;
+          src_p = M.work + sfg_pristine_off(&P, cv, ch.work_bytes, op.src_arg, nullptr);
+        } else {
+          len = 4;
+        }
       }
       if (len == 0) continue;
       int hit = -1;
@@ -695,7 +730,7 @@ SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R, c
         uint8_t byte = 0;
         if (op.src_form == SFG_SRC_SEQ32) byte = (uint8_t)((uint32_t)(b >> 2) >> (8 * (b & 3)));
         else if (op.src_form == SFG_SRC_HEX) byte = E.const_blob[op.blob_off + b];
-        else if (op.src_form == SFG_SRC_ARG) byte = (uint8_t)(src_v->bits >> (8 * b));
+        else if (op.src_form == SFG_SRC_ARG) byte = src_p ? src_p[b] : (uint8_t)(src_v->bits >> (8 * b));
         if (!mem_write(M, L, r, addr + b, 1, byte)) { V.status = SFG_ST_OVERLAY; stop = true; break; }
       }
       continue;
@@ -725,7 +760,8 @@ SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R, c
       const int64_t addr = L.named_addr[op.buf];
       const int res = lane_free(P, L, addr);
       if (res < 0) { V.status = -res; break; }
-      if (res == 1) {  // invalid_free_report (sanitizer.py:199-205)
+      if (res == 2 && P.term_phase) continue;  // TERM teardown is idempotent (campaign.py:538-541)
+      if (res >= 1) {  // invalid_free_report (sanitizer.py:199-205)
         const int sp = space_of(P, addr);
         int r = sp >= 0 ? resolve_payload(L, sp, addr) : -1;
         if (r < 0 && sp >= 0) r = resolve_slot(L, sp, addr);

@@ -17,9 +17,12 @@
 // The host-op driver, allocator and sanitizer are exec_core.cuh, shared with
 // the generic interpreter (execute.cu).
 #include <nvrtc.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cstdio>
+#include <filesystem>
+#include <fstream>
 #include <functional>
 #include <map>
 #include <mutex>
@@ -1037,6 +1040,63 @@ struct Gen {
 
 }  // namespace sfgjit
 
+static int jit_compiles = 0, jit_disk_hits = 0;   // NVRTC compiles / on-disk cache hits (sfg_jit_stats)
+
+// On-disk cubin cache: NVRTC takes seconds per harness, so a compiled program is
+// kept in $SFG_JIT_CACHE (default ~/.cache/sfg_b200_jit; "0" disables), keyed by a
+// hash of the generated source and the compile options.  An entry stores the
+// source it was compiled from and is used only if that matches exactly.
+static std::string jit_cache_dir() {
+  const char* d = getenv("SFG_JIT_CACHE");
+  if (d && d[0] == '0' && d[1] == 0) return "";
+  if (d && d[0]) return d;
+  const char* h = getenv("HOME");
+  return std::string(h && h[0] ? h : "/tmp") + "/.cache/sfg_b200_jit";
+}
+
+static uint64_t fnv1a(const std::string& s) {
+  uint64_t x = 1469598103934665603ull;
+  for (unsigned char c : s) { x ^= c; x *= 1099511628211ull; }
+  return x;
+}
+
+static bool jit_cache_load(const std::string& key, std::vector<char>& cubin) {
+  const std::string dir = jit_cache_dir();
+  if (dir.empty()) return false;
+  char name[32];
+  snprintf(name, sizeof name, "/%016llx.sfgc", (unsigned long long)fnv1a(key));
+  std::ifstream f(dir + name, std::ios::binary);
+  if (!f) return false;
+  uint64_t n = 0;
+  if (!f.read(reinterpret_cast<char*>(&n), 8) || n != key.size()) return false;
+  std::string k(n, '\0');
+  if (!f.read(&k[0], (std::streamsize)n) || k != key) return false;
+  std::vector<char> data((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+  if (data.empty()) return false;
+  cubin.swap(data);
+  return true;
+}
+
+static void jit_cache_store(const std::string& key, const std::vector<char>& cubin) {
+  const std::string dir = jit_cache_dir();
+  if (dir.empty()) return;
+  std::error_code ec;
+  std::filesystem::create_directories(dir, ec);
+  char name[32];
+  snprintf(name, sizeof name, "/%016llx.sfgc", (unsigned long long)fnv1a(key));
+  const std::string path = dir + name, tmp = path + ".tmp" + std::to_string((long long)getpid());
+  {
+    std::ofstream f(tmp, std::ios::binary);
+    if (!f) return;
+    const uint64_t n = key.size();
+    f.write(reinterpret_cast<const char*>(&n), 8);
+    f.write(key.data(), (std::streamsize)n);
+    f.write(cubin.data(), (std::streamsize)cubin.size());
+    if (!f) return;
+  }
+  std::filesystem::rename(tmp, path, ec);   // atomic: concurrent processes never read a torn entry
+}
+
 // Generate and compile; on success `cubin` holds the sm_100a image.  Returns 0 on success.
 static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_edge_events, uint32_t dead_kernels,
                            std::string& source,
@@ -1047,9 +1107,21 @@ static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_e
   if (const char* tb = getenv("SFG_TAIL_MINB")) g.tail_minb = atoi(tb) >= 1 ? atoi(tb) : 12;
   if (const char* bb = getenv("SFG_BULK_MINB")) g.bulk_minb = atoi(bb) >= 1 ? atoi(bb) : 3;
   source = g.run(P.n_edges, max_edge_events);
-  // process-wide cache: identical programs (same generated source) compile once
+  // process-wide cache: identical programs (same generated source) compile once;
+  // then the on-disk cache across processes
   static std::mutex mu;
   static std::map<std::string, std::vector<char>> cache;
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false", "-default-device",
+                        "-lineinfo", "-DSFG_JIT=1", "--device-int128", "--maxrregcount=255"};
+  std::string key;
+  for (const char* op : opts) key += std::string(op) + " ";
+  {
+    int ver[2] = {0, 0};
+    nvrtcVersion(&ver[0], &ver[1]);
+    key += "nvrtc " + std::to_string(ver[0]) + "." + std::to_string(ver[1]) + "\n";
+    for (int e = 0; e < kEmbeddedCount; ++e) key += kEmbeddedSources[e];
+  }
+  key += source;
   {
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(source);
@@ -1058,14 +1130,18 @@ static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_e
       return 0;
     }
   }
+  if (jit_cache_load(key, cubin)) {
+    std::lock_guard<std::mutex> lk(mu);
+    cache[source] = cubin;
+    jit_disk_hits++;
+    return 0;
+  }
   nvrtcProgram prog;
   if (nvrtcCreateProgram(&prog, source.c_str(), "sfg_jit.cu", kEmbeddedCount, kEmbeddedSources, kEmbeddedNames) !=
       NVRTC_SUCCESS) {
     log = "nvrtcCreateProgram failed";
     return 1;
   }
-  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false", "-default-device",
-                        "-lineinfo", "-DSFG_JIT=1", "--device-int128", "--maxrregcount=255"};
   const nvrtcResult cr = nvrtcCompileProgram(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
   size_t lsz = 0;
   nvrtcGetProgramLogSize(prog, &lsz);
@@ -1080,6 +1156,8 @@ static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_e
   cubin.resize(csz);
   nvrtcGetCUBIN(prog, cubin.data());
   nvrtcDestroyProgram(&prog);
+  jit_compiles++;
+  jit_cache_store(key, cubin);
   std::lock_guard<std::mutex> lk(mu);
   cache[source] = cubin;
   return 0;

@@ -384,7 +384,7 @@ __device__ __forceinline__ void mutate_child(const sfg_prog& P, const CorpusView
   // one pass over the child's values: parent value or its mutation, work layout
   // (array regions at materialized size, 16-aligned, then COMPUTE named allocs),
   // readout sizes; each value written once
-  uint64_t off = 0, rb = P.diff_readback ? (uint64_t)P.readout_bytes_fixed : 0ull;
+  uint64_t off = 0, pri = 0, rb = P.diff_readback ? (uint64_t)P.readout_bytes_fixed : 0ull;
   for (int a = 0; a < P.n_args; ++a) {
     int m = -1;
 #pragma unroll
@@ -409,8 +409,9 @@ __device__ __forceinline__ void mutate_child(const sfg_prog& P, const CorpusView
     if (P.diff_readback)
       for (int k = 0; k < P.n_copyout_arg; ++k)
         if (P.copyout_arg[k] == a) rb += sfg_align16(nb);
+    if ((P.copy_src_mask >> a) & 1u) pri += sfg_align16(nb);
   }
-  ch.work_bytes = off + (uint64_t)P.named_work_bytes;
+  ch.work_bytes = off + (uint64_t)P.named_work_bytes + sfg_ov_bytes(P.ov_cap) + pri;
   ch.readout_bytes = rb;
   ch.readout_bytes = rb;
 }
@@ -441,8 +442,8 @@ extern "C" __global__ void sfg_plan_seq_kernel(sfg_prog P, CorpusView C, int64_t
                                                uint32_t* flags_out, SfgStream* states) {
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
   SfgStream s = *state;
-  uint64_t cnt[8];
-  for (int c = 0; c < P.n_int_args && c < 8; ++c) cnt[c] = counts_base[c];
+  uint64_t cnt[SFG_MAX_ARGS];
+  for (int c = 0; c < P.n_int_args && c < SFG_MAX_ARGS; ++c) cnt[c] = counts_base[c];
   for (int i = 0; i < n; ++i) {
     states[i] = s;
     const int64_t it = it0 + i;
@@ -489,6 +490,9 @@ extern "C" __global__ void sfg_apply_kernel(sfg_prog P, CorpusView C, int n, con
         if (ch.ops[k].arg == a) op = &ch.ops[k];
       emit_child(base + cv[a].data_off, sfg_mat_size(cv[a]), C.data + pv[a].data_off, pv[a].nbytes, cv[a],
                  op, lane, kApplyLanes);
+      if ((P.copy_src_mask >> a) & 1u)   // the test case's own bytes for copy_in (campaign.py:404-409)
+        emit_child(base + sfg_pristine_off(&P, cv, ch.work_bytes, a, nullptr), cv[a].nbytes, C.data + pv[a].data_off,
+                   pv[a].nbytes, cv[a], op, lane, kApplyLanes);
     }
   }
 }

@@ -18,7 +18,7 @@ typedef unsigned long uintptr_t;
 #include <stdint.h>
 #endif
 
-#define SFG_ABI_VERSION 3
+#define SFG_ABI_VERSION 4
 
 #define SFG_MAX_ARGS 16      // argspecs per harness
 #define SFG_MAX_OPS 3        // MutationConfig.max_ops ceiling (reference default 3)
@@ -27,9 +27,9 @@ typedef unsigned long uintptr_t;
 #define SFG_MAX_BASE_RECS 32 // allocation records alive after INIT
 #define SFG_MAX_FREE 32      // baseline free-list entries
 #define SFG_MAX_LANE_RECS 40 // baseline + per-input allocation records
-#define SFG_MAX_REGS 32      // kernel register_count ceiling
+#define SFG_MAX_REGS 64      // kernel register_count ceiling (the generic interpreter's register files)
 #define SFG_MAX_EDGES 1024   // static edges over all kernels
-#define SFG_OVERLAY 32       // per-input byte writes into INIT buffers
+#define SFG_OV_CHUNK 256     // copy-on-write granule of INIT-buffer writes (device_memory.py:551-618 dirty chunks)
 
 // opcodes == sir.Opcode
 enum { SFG_MOV = 0, SFG_ADD, SFG_SUB, SFG_MUL, SFG_FADD, SFG_FSUB, SFG_FMUL, SFG_SETP,
@@ -192,7 +192,7 @@ typedef struct sfg_prog {
   int8_t mutable_args[SFG_MAX_ARGS];
   int8_t int_slot[SFG_MAX_ARGS];         // arg -> rotation-count column, -1 if not i32
   int32_t n_hostops, n_edges, n_labels, n_keys;
-  int32_t label_arg_base, total_ins, named_work_bytes, overlay;
+  int32_t label_arg_base, total_ins, named_work_bytes, ov_cap;  // ov_cap: copy-on-write chunks per input
   sfg_kernel kernels[SFG_MAX_KERNELS];
   // mutation / campaign config
   int32_t max_ops, mut_granule, mut_redzone, window;
@@ -206,4 +206,39 @@ typedef struct sfg_prog {
   // k > 0 = fixed fan-out, input it mutates corpus entry ((it - 1) / k) mod n (no draw;
   // BASELINE.json configs[3]: k children per seed of a large seed corpus)
   int32_t fanout;
+  // array args that are the source of a COMPUTE `copy_in <buf> arg:k`: their
+  // unmodified bytes (the test case's data, campaign.py:404-409) are kept in a
+  // pristine copy at the very end of the work region
+  uint32_t copy_src_mask;
+  // the script is a TERM phase (campaign.py:538-541: freeing an already freed
+  // allocation is skipped); jit_off: run on the generic interpreter (no NVRTC) --
+  // the one-input INIT-launch / TERM programs
+  int32_t term_phase, jit_off;
 } sfg_prog;
+
+// Tail of every input's work region: the copy-on-write overlay of INIT buffers,
+// int64 blob-chunk index[ov_cap] (16-aligned) then ov_cap chunks of SFG_OV_CHUNK bytes.
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+static inline uint64_t sfg_ov_bytes(int32_t cap) {
+  return cap <= 0 ? 0ull : (((uint64_t)cap * 8ull + 15ull) & ~15ull) + (uint64_t)cap * SFG_OV_CHUNK;
+}
+
+// Work region of one input: array args at their materialized sizes | COMPUTE named
+// allocs | copy-on-write overlay | pristine copies of copy_in source arrays.
+// Offset of arg a's pristine copy given the input's values (vals[n_args]).
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+static inline uint64_t sfg_pristine_off(const sfg_prog* P, const sfg_val* v, uint64_t work_bytes, int a,
+                                        uint64_t* total) {
+  uint64_t tot = 0, off = 0;
+  for (int k = 0; k < P->n_args; ++k)
+    if ((P->copy_src_mask >> k) & 1u) {
+      if (k == a) off = tot;
+      tot += ((uint64_t)v[k].nbytes + 15ull) & ~15ull;
+    }
+  if (total) *total = tot;
+  return work_bytes - tot + off;
+}

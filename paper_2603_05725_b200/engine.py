@@ -34,9 +34,9 @@ from .baseline import MemConfig, OutOfSpaceError, build_baseline, record_table
 from .coverage import CoverageMap
 from .findings import FindingsLog
 from .sir import SPACE_ORDER
-from .lowering import (CHILD, ENTRY, ST_COUNTER, MAX_KERNELS, ctx_edge_hashes, ST_FINDING, ST_LANE_RECS, ST_OUT_OF_SPACE, ST_OVERLAY,
-                       ST_ZERO_ALLOC, VAL, VERDICT, Lowered, LoweringError, decode_op, decode_verdict,
-                       pack_values, unpack_values)
+from .lowering import (CHILD, ENTRY, ST_COUNTER, MAX_KERNELS, OV_CAP0, OV_CHUNK, ctx_edge_hashes, ST_FINDING,
+                       ST_LANE_RECS, ST_OUT_OF_SPACE, ST_OVERLAY, ST_ZERO_ALLOC, VAL, VERDICT, Lowered, LoweringError,
+                       decode_op, decode_verdict, ov_bytes, pack_values, unpack_values)
 from .shard import RoundComm, owner_of
 from .testcase import MutationError, TestCase
 
@@ -121,10 +121,10 @@ class Slot:
         self.children, self.vals = u8(cap * CHILD.itemsize), u8(cap * A * VAL.itemsize)
         self.work_base, self.ro_base = i64(cap), i64(cap)
         self.verdicts, self.ecnt = u8(cap * VERDICT.itemsize), i32(cap * E)
-        self.overlay = i64(cap * 32) if dc.low.overlay else None
         self.allocs, self.allocs_prefix, self.admit, self.pos = i64(cap), i64(cap), i64(cap), i64(cap)
         self.bytes, self.boff, self.sel, self.dst_off = i64(cap), i64(cap), i32(cap), i64(cap * A)
-        self.tmp, self.tot = i64((cap + 2047) // 2048 + 8), i64(16)
+        # scan totals: [0..8) layout/admission scans, [8..8+C) rotation-count columns
+        self.tmp, self.tot = i64((cap + 2047) // 2048 + 8), i64(8 + 16)
         self.counter = i32(8)            # work counters of this slot's execute launches
         self.deferred = i32(2 * cap)     # tail-pass lists: soft-cap deferrals, sequential re-runs
         self.order = i32(cap)            # bulk-pass schedule (sfg_order)
@@ -140,7 +140,7 @@ class Slot:
         self.edelta, self.kcount, self.ent = self.sums[:E0], self.sums[E0:E0 + K0], self.sums[E0 + K0:]
         self.small = i64(2)              # [admitted, allocs] of this rank, all-gathered
         self.counts_base = torch.zeros(C, dtype=torch.int64, device=dev)
-        self.pin_tot = torch.empty(16, dtype=torch.int64, pin_memory=True)
+        self.pin_tot = torch.empty(8 + 16, dtype=torch.int64, pin_memory=True)
         self.pin_sc = torch.empty(2, dtype=torch.int32, pin_memory=True)
         self.pin_gath = torch.empty((dc.comm.world, 2), dtype=torch.int64, pin_memory=True)
         self.pin_kc = torch.empty(max(K0, 1), dtype=torch.int64, pin_memory=True)
@@ -177,7 +177,8 @@ class DeviceCampaign:
                  mutation: MutationConfig | None = None, budget=1_000_000, window=256, recent_weight=4.0,
                  diff_readback=False, stop_on_first_finding=False, stop_bug_class=None, device=None,
                  extra_seeds=(), ids_reset_per_input=False, comm: RoundComm | None = None,
-                 soft_cap: int | None = None, ctx_map_bits: int = 0, fanout: int = 0, sequential: bool = False):
+                 soft_cap: int | None = None, ctx_map_bits: int = 0, fanout: int = 0, sequential: bool = False,
+                 baseline=None, jit: bool = True, term_phase: bool = False):
         if not torch.cuda.is_available():
             raise _native.NativeError("no CUDA device: the fuzzing inner loop runs only on the GPU")
         self.L = _native.lib()
@@ -200,24 +201,30 @@ class DeviceCampaign:
         self.mutation = mutation or MutationConfig()
         self.master_seed = master_seed
         self.seed_tc = manifest.seed(master_seed)
-        self.base = build_baseline(manifest, self.seed_tc, self.mem)
+        self.budget = budget
+        # the post-INIT state; INIT launches run on the device (_init_launch)
+        self.base = baseline if baseline is not None else build_baseline(manifest, self.seed_tc, self.mem,
+                                                                            init_launch=self._init_launch)
         stop_class = None
         if stop_bug_class is not None:
             stop_class = getattr(stop_bug_class, "value", str(stop_bug_class))
         self.low = Lowered(manifest, self.base, mem=self.mem, mutation=self.mutation, master_seed=master_seed,
                            budget=budget, window=window, recent_weight=recent_weight,
                            diff_readback=diff_readback, stop_first=stop_on_first_finding, stop_class=stop_class,
-                           fanout=fanout)
+                           fanout=fanout, term_phase=term_phase, jit=jit)
         self.diff = bool(diff_readback)
         self.specs = manifest.argspecs
         self.n_args = len(self.specs)
         self.C = len(self.low.int_args)
-        if self.C > 8:
-            raise LoweringError("more than 8 i32 arguments")
+        if self.C > 16:     # sfg_prog.int_slot columns (SFG_MAX_ARGS)
+            raise LoweringError("more than 16 i32 arguments")
         self.E = self.low.n_edges
         self.K = self.low.n_keys
         recs = record_table(self.base, self.low.labels)
-        self.blob = torch.frombuffer(bytearray(self.base.blob), dtype=torch.uint8).to(self.dev)
+        # padded to whole copy-on-write chunks (a chunk is copied whole on its first write)
+        blob = bytearray(self.base.blob)
+        blob += bytes(-len(blob) % OV_CHUNK or (OV_CHUNK if not blob else 0))
+        self.blob = torch.frombuffer(blob, dtype=torch.uint8).to(self.dev)
         # host<->device bytes moved by the campaign (bench e2e accounting)
         self.h2d_bytes = len(self.base.blob)
         self.d2h_bytes = 0
@@ -262,8 +269,57 @@ class DeviceCampaign:
         self.rounds = 0
         self.spec_depth = 2              # adaptive speculation depth (run_rounds)
         self.launches = 0                # kernels launched through the C ABI (bench evidence)
+        self.ov_grows = 0                # copy-on-write overlay enlargements (rounds re-run)
         self.timing = False              # record CUDA events around each execute kernel
         self.exec_events: list = []
+
+    # ---- INIT launches / TERM phase: one-input device programs ------------------------
+    def _phase_program(self, script, baseline, *, term=False):
+        """A device program whose COMPUTE script is ``script`` over ``baseline``
+        (generic interpreter, no NVRTC: it runs once)."""
+        from dataclasses import replace
+        from .manifest import COMPUTE, INIT, TERM, HostOp
+        allocs = [o for o in self.manifest.phases[INIT] if o.kind == "alloc"]
+        allocs += [HostOp("alloc", 0, name=n) for n in baseline.named if n.startswith("\0")]
+        m2 = replace(self.manifest, phases={INIT: allocs, COMPUTE: list(script), TERM: []})
+        return DeviceCampaign(m2, master_seed=self.master_seed, mem=self.mem, mutation=self.mutation,
+                              budget=self.budget, diff_readback=True, device=self.dev, baseline=baseline,
+                              jit=False, term_phase=term)
+
+    def _init_launch(self, op, state, live):
+        """One INIT launch (build_baseline): run it on the device over the state so
+        far and read back the final bytes of every live record (campaign.py:483-561
+        with phase INIT: no coverage, the seed input, iteration 0)."""
+        from .baseline import InitFailure
+        from .manifest import HostOp
+        recs = state.records
+        outs = [HostOp("copy_out", op.line, name=n, size=recs[state.named[n][2]].size) for n in live]
+        dc = self._phase_program([op] + outs, state)
+        try:
+            (res,) = dc.execute_testcases([self.seed_tc], iteration0=0)
+        finally:
+            dc.close()
+        if res["status"] != "ok":   # campaign.py:723-725
+            raise InitFailure(f"init phase failed on the seed input: {res['status']}")
+        return {n: res["readouts"][n] for n in live}
+
+    def run_term(self):
+        """The TERM phase of a worker (campaign.py:756-762): on the restored post-INIT
+        state with the seed input, iteration -1; returns its BugReport or None.
+        Allocation ids continue the worker's counter."""
+        from .baseline import term_frees_clean
+        from .manifest import TERM
+        ops = self.manifest.phases[TERM]
+        if not ops or term_frees_clean(self.base, ops):
+            return None
+        dc = self._phase_program(ops, self.base, term=True)
+        try:
+            (res,) = dc.execute_testcases([self.seed_tc], iteration0=-1, id_base=self.next_alloc_id)
+        finally:
+            dc.close()
+        if res["status"].startswith("fatal"):
+            raise DeviceFatal(f"TERM phase: {res['status']}")
+        return res["report"]
 
     # ---- corpus ---------------------------------------------------------------------
     def _u8(self, n):
@@ -289,12 +345,15 @@ class DeviceCampaign:
         array mutations at most double an array (array_dim), or set 4*count
         (array_extreme), so bound each array by max(2*nbytes, 8*count) + 16."""
         b = 0
-        for v in vals:
+        mask = int(self.low.prog["copy_src_mask"])
+        for a, v in enumerate(vals):
             if v["kind"] == 2:
                 ov = int(v["size_override"])
                 grow = max(2 * int(v["nbytes"]), 8 * int(v["count"])) + 16
                 b += _align16(max(grow, ov if ov != -(1 << 63) else 0))
-        return b + int(self.low.prog["named_work_bytes"])
+                if mask >> a & 1:     # pristine copy of a copy_in source
+                    b += _align16(grow)
+        return b + int(self.low.prog["named_work_bytes"]) + ov_bytes(int(self.low.prog["ov_cap"]))
 
     def _upload_seeds(self, seeds):
         metas = np.zeros(len(seeds), ENTRY)
@@ -464,7 +523,7 @@ class DeviceCampaign:
             order = S.order.data_ptr()
         _native.check(self.L.sfg_execute(
             self.h, n, S.children.data_ptr(), S.vals.data_ptr(), S.work_base.data_ptr(), S.work.data_ptr(),
-            S.verdicts.data_ptr(), S.ecnt.data_ptr(), _ptr(S.readouts), S.ro_base.data_ptr(), _ptr(S.overlay),
+            S.verdicts.data_ptr(), S.ecnt.data_ptr(), _ptr(S.readouts), S.ro_base.data_ptr(),
             S.counter.data_ptr(), soft, S.deferred.data_ptr() if tail else None, self.max_entry_work, order,
             st.cuda_stream), "execute")
         if tail:
@@ -479,7 +538,7 @@ class DeviceCampaign:
             _native.check(self.L.sfg_execute_deferred(
                 self.h, ctypes.byref(cd), n, S.children.data_ptr(), S.vals.data_ptr(), S.work_base.data_ptr(),
                 S.work.data_ptr(), S.verdicts.data_ptr(), S.ecnt.data_ptr(), _ptr(S.readouts),
-                S.ro_base.data_ptr(), _ptr(S.overlay), S.counter.data_ptr(), S.deferred.data_ptr(),
+                S.ro_base.data_ptr(), S.counter.data_ptr(), S.deferred.data_ptr(),
                 self.max_entry_work, ts.cuda_stream), "execute_deferred")
             if ts is not st:
                 st.wait_stream(ts)
@@ -544,6 +603,12 @@ class DeviceCampaign:
             if self._last_done is not None:
                 st.wait_event(self._last_done)
         stop, fatal, gathered = self._triage_pass(S)
+        # an input that overflowed its copy-on-write overlay: grow the overlay and run
+        # the round again (deterministic, so the results are those of a large overlay)
+        while fatal != NONE and fatal <= stop and self._fatal_status(S, fatal)[0] == ST_OVERLAY:
+            self._grow_overlay()
+            self._submit(S, S.round_it0, S.round_n, S.round_index, resubmit=True)
+            stop, fatal, gathered = self._triage_pass(S)
         N = S.round_n
         cut = None
         if self.sequential and int(gathered[:, 0].sum()):
@@ -586,15 +651,32 @@ class DeviceCampaign:
         self.rounds += 1
         return RoundResult(S.round_it0, N, None if stop == NONE else stop, executed, n_adm, new_keys, S)
 
-    def _raise_fatal(self, S: Slot, g):
-        """The first fatal input (global round index g) raises the reference's
-        exception on every rank; its owner reads the status."""
+    def _fatal_status(self, S: Slot, g):
+        """(status, space, alloc_size, alloc_base) of the first fatal input (global
+        round index g), read by its owner and shared with every rank."""
         st = None
         if S.i_base <= g < S.i_base + S.n:
             i = g - S.i_base
             v = _np(S.verdicts[i * VERDICT.itemsize:(i + 1) * VERDICT.itemsize], VERDICT)[0]
             st = (int(v["status"]), int(v["space"]), int(v["alloc_size"]), int(v["alloc_base"]))
-        st, space, need, remain = next(x for x in self.comm.all_gather_object(st) if x is not None)
+        if self.comm.world > 1:
+            st = next(x for x in self.comm.all_gather_object(st) if x is not None)
+        return st
+
+    def _grow_overlay(self):
+        """Double the per-input copy-on-write overlay (sfg_prog.ov_cap)."""
+        old = int(self.low.prog["ov_cap"])
+        new = max(2 * old, OV_CAP0)
+        self.low.prog["ov_cap"] = new
+        P = self.low.prog_bytes()
+        _native.check(self.L.sfg_program_update(self.h, P, len(P)), "sfg_program_update")
+        self.max_entry_work += ov_bytes(new) - ov_bytes(old)
+        self.ov_grows += 1
+
+    def _raise_fatal(self, S: Slot, g):
+        """The first fatal input (global round index g) raises the reference's
+        exception on every rank; its owner reads the status."""
+        st, space, need, remain = self._fatal_status(S, g)
         if st == ST_OUT_OF_SPACE:   # the reference's message (device_memory.py:428-430)
             raise OutOfSpaceError(f"{SPACE_ORDER[space].value} scope 0: need {need} bytes, {remain} remain")
         if st == ST_ZERO_ALLOC:
@@ -945,7 +1027,8 @@ class DeviceCampaign:
         return out
 
     # ---- one-shot execution of given test cases (execute_once analogue) -------------------
-    def execute_testcases(self, tcs, iteration0: int = 0, trace: bool = False, trace_cap: int = 1 << 16):
+    def execute_testcases(self, tcs, iteration0: int = 0, trace: bool = False, trace_cap: int = 1 << 16,
+                          id_base: int | None = None):
         """Run COMPUTE for explicit inputs (no mutation); returns per-input dicts.
         trace: also return each input's ExecHooks event stream ("events": tuples
         ("mem", kernel, iid, ctaid, tid, space, addr, width, is_store) /
@@ -973,7 +1056,11 @@ class DeviceCampaign:
                 vals[a]["data_off"] = off
                 region += chunk + bytes((-len(chunk)) % 16)
                 off += _align16(size)
-            region += bytes(int(self.low.prog["named_work_bytes"]))
+            region += bytes(int(self.low.prog["named_work_bytes"]) + ov_bytes(int(self.low.prog["ov_cap"])))
+            mask = int(self.low.prog["copy_src_mask"])
+            for a, v in enumerate(tc.args):     # pristine copies of copy_in sources (sfg_pristine_off)
+                if mask >> a & 1:
+                    region += v.data + bytes((-len(v.data)) % 16)
             work += region
             chld[i]["it"], chld[i]["parent"], chld[i]["work_bytes"] = iteration0 + i, -1, len(region)
             ro = int(self.low.prog["readout_bytes_fixed"])
@@ -1000,7 +1087,7 @@ class DeviceCampaign:
             self.launches += 1
             _native.check(self.L.sfg_execute_trace(
                 self.h, n, S.children.data_ptr(), S.vals.data_ptr(), S.work_base.data_ptr(), S.work.data_ptr(),
-                S.verdicts.data_ptr(), S.ecnt.data_ptr(), _ptr(S.readouts), S.ro_base.data_ptr(), _ptr(S.overlay),
+                S.verdicts.data_ptr(), S.ecnt.data_ptr(), _ptr(S.readouts), S.ro_base.data_ptr(),
                 tbuf.data_ptr(), trace_cap, tcnt.data_ptr(), S.stream.cuda_stream), "execute_trace")
             self.drain()
             cnt = tcnt.cpu().numpy()
@@ -1012,6 +1099,9 @@ class DeviceCampaign:
             self._execute(S, n)
         self.drain()
         verd = _np(S.verdicts[:n * VERDICT.itemsize], VERDICT)
+        if n and (verd["status"] == ST_OVERLAY).any():   # overlay too small: grow, run again
+            self._grow_overlay()
+            return self.execute_testcases(tcs, iteration0, trace, trace_cap, id_base)
         E1 = max(self.E, 1)
         ecnt = S.ecnt[:n * E1].cpu().numpy().view(np.uint32).reshape(n, E1)
         rod = S.readouts.cpu().numpy().tobytes() if S.readouts is not None else b""
@@ -1019,7 +1109,8 @@ class DeviceCampaign:
         for i in range(n):
             v = verd[i]
             st = int(v["status"])
-            rep = decode_verdict(v, self.low, iteration0 + i, self.base.next_id) if st == ST_FINDING else None
+            rep = decode_verdict(v, self.low, iteration0 + i, self.base.next_id if id_base is None else id_base) \
+                if st == ST_FINDING else None
             readouts = {}
             if S.readouts is not None and st == 0:
                 cur = int(ro_base[i])

@@ -33,9 +33,10 @@ MAX_KERNELS = 16
 MAX_NAMED = 32
 MAX_BASE_RECS = 32
 MAX_FREE = 32
-MAX_REGS = 32
+MAX_REGS = 64
 MAX_EDGES = 1024
-OVERLAY = 32
+MAX_LANE_RECS = 40   # sfg_types.h SFG_MAX_LANE_RECS: baseline + one input's own allocation records
+MAX_QUAR = 32        # exec_core.cuh kMaxQ / kMaxFree: one input's quarantine and free list
 NO_OVERRIDE = -(1 << 63)
 
 # ---- struct dtypes (mirror csrc/sfg_types.h; sizes checked against the .so) ----
@@ -82,12 +83,13 @@ PROG = np.dtype([
     ("arg_kind", "u1", (MAX_ARGS,)), ("arg_elem", "u1", (MAX_ARGS,)), ("arg_fixed", "u1", (MAX_ARGS,)),
     ("mutable_args", "i1", (MAX_ARGS,)), ("int_slot", "i1", (MAX_ARGS,)),
     ("n_hostops", "<i4"), ("n_edges", "<i4"), ("n_labels", "<i4"), ("n_keys", "<i4"),
-    ("label_arg_base", "<i4"), ("total_ins", "<i4"), ("named_work_bytes", "<i4"), ("overlay", "<i4"),
+    ("label_arg_base", "<i4"), ("total_ins", "<i4"), ("named_work_bytes", "<i4"), ("ov_cap", "<i4"),
     ("kernels", KERNEL, (MAX_KERNELS,)),
     ("max_ops", "<i4"), ("mut_granule", "<i4"), ("mut_redzone", "<i4"), ("window", "<i4"),
     ("recent_weight", "<f8"), ("master_seed", "<u8"), ("keybase", "<u8"), ("budget", "<u8"),
     ("diff_readback", "<i4"), ("stop_first", "<i4"), ("stop_class", "<i4"), ("n_copyout_arg", "<i4"),
-    ("readout_bytes_fixed", "<i8"), ("copyout_arg", "i1", (MAX_ARGS,)), ("fanout", "<i4")], align=True)
+    ("readout_bytes_fixed", "<i8"), ("copyout_arg", "i1", (MAX_ARGS,)), ("fanout", "<i4"),
+    ("copy_src_mask", "<u4"), ("term_phase", "<i4"), ("jit_off", "<i4")], align=True)
 
 LAYOUTS = {"ins": INS, "kernel": KERNEL, "hostop": HOSTOP, "binding": BINDING, "rec": REC, "val": VAL,
            "op": OP, "child": CHILD, "entry": ENTRY, "verdict": VERDICT, "prog": PROG}
@@ -112,6 +114,15 @@ M_INDEX = {k: i for i, k in enumerate(M_KINDS)}
 
 
 from .baseline import LoweringError  # noqa: E402,F401  (the harness uses a construct this path does not lower)
+
+
+OV_CHUNK = 256    # sfg_types.h SFG_OV_CHUNK
+OV_CAP0 = 4       # initial overlay chunks per input of a harness that can write INIT buffers
+
+
+def ov_bytes(cap: int) -> int:
+    """Bytes of the copy-on-write overlay at the tail of a work region (sfg_ov_bytes)."""
+    return 0 if cap <= 0 else ((cap * 8 + 15) & ~15) + cap * OV_CHUNK
 
 
 def wrap_i32(v: int) -> int:
@@ -288,7 +299,8 @@ class Lowered:
     """Everything the device needs for one harness + campaign configuration."""
 
     def __init__(self, manifest, baseline, *, mem, mutation, master_seed, budget, window, recent_weight,
-                 diff_readback=False, stop_first=False, stop_class=None, fanout=0):
+                 diff_readback=False, stop_first=False, stop_class=None, fanout=0, term_phase=False,
+                 jit=True):
         self.manifest = manifest
         prog = manifest.program
         specs = manifest.argspecs
@@ -320,6 +332,7 @@ class Lowered:
         hops, binds = [], []
         const_blob = bytearray()
         named_work = 0
+        self.copy_src_mask = 0      # array args that are COMPUTE copy_in sources
         copyout_args = []
         readout_fixed = 0
         for op in manifest.phases[COMPUTE]:
@@ -342,8 +355,10 @@ class Lowered:
                     const_blob += data
                 else:
                     k = int(payload)
+                    # an array source copies the test case's own bytes (campaign.py:404-409,
+                    # 497-513): the work region keeps a pristine copy of that argument
                     if specs[k].kind == ScalarType.PTR:
-                        raise LoweringError("COMPUTE copy_in from an array argument is not lowered")
+                        self.copy_src_mask |= 1 << k
                     h.update(src_arg=k, size=4)
             elif op.kind == "copy_out":
                 if op.arg_ref >= 0:
@@ -388,6 +403,18 @@ class Lowered:
                         {o.name for o in manifest.phases[COMPUTE] if o.kind == "alloc"}
                         for op in manifest.phases[COMPUTE])
         self.overlay = bool(untagged or buf_bound or init_copy)
+        # per-input table capacities, checked here at load time: an input allocates at
+        # most one record per array argument (materialized once per phase,
+        # campaign.py:440-450) and per COMPUTE alloc, and frees at most once per free op
+        n_allocs = sum(1 for s in specs if s.kind == ScalarType.PTR) + \
+            sum(1 for op in manifest.phases[COMPUTE] if op.kind == "alloc")
+        n_frees = sum(1 for op in manifest.phases[COMPUTE] if op.kind == "free")
+        if len(baseline.records) + n_allocs > MAX_LANE_RECS:
+            raise LoweringError(f"INIT records + per-input allocations ({len(baseline.records)} + {n_allocs}) "
+                                f"exceed the per-input table ({MAX_LANE_RECS})")
+        if len(baseline.quarantine) + n_frees > MAX_QUAR or \
+                len(baseline.free_entries) + len(baseline.quarantine) + n_frees > MAX_QUAR:
+            raise LoweringError(f"quarantine / free list of an input can exceed {MAX_QUAR} entries")
         # header
         P = np.zeros(1, PROG)[0]
         for s, sp in enumerate(SPACE_ORDER):
@@ -427,7 +454,9 @@ class Lowered:
             P["int_slot"][a] = c
         P["n_hostops"], P["n_edges"], P["n_labels"], P["n_keys"] = len(hops), self.n_edges, len(self.labels), self.n_keys
         P["label_arg_base"], P["total_ins"], P["named_work_bytes"] = self.label_arg_base, total_ins, named_work
-        P["overlay"] = int(self.overlay)
+        # copy-on-write overlay chunks per input (grown by the engine when a round
+        # overflows it; the round is then re-run, so no input ever fails on it)
+        P["ov_cap"] = OV_CAP0 if self.overlay else 0
         for j, kd in enumerate(kernels):
             for key, v in kd.items():
                 if key == "ptype":
@@ -439,6 +468,8 @@ class Lowered:
             raise LoweringError(f"max_ops > {MAX_OPS}")
         P["window"], P["recent_weight"] = window, float(recent_weight)
         P["fanout"] = int(fanout)
+        P["copy_src_mask"] = self.copy_src_mask
+        P["term_phase"], P["jit_off"] = int(term_phase), int(not jit)
         P["master_seed"], P["keybase"], P["budget"] = master_seed & ((1 << 64) - 1), KEYBASE, budget
         P["diff_readback"], P["stop_first"] = int(diff_readback), int(stop_first)
         P["stop_class"] = -1 if stop_class is None else [c.value for c in CLASS_BY_CODE].index(stop_class)

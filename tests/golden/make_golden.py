@@ -432,6 +432,165 @@ def loops():
     return out
 
 
+# Phase features beyond the bundled harnesses (campaign.py:483-561, 723-762):
+# kernels storing >= 4 KB per exec into an INIT (`buf:`) buffer, an INIT-phase
+# launch (with an array argument materialized in INIT), a TERM-phase launch that
+# reports (iteration -1) plus an idempotent double free, and a COMPUTE
+# `copy_in <buf> arg:N` of an array argument after a launch modified it.
+FEATURES_SIR = """\
+kernel fill(ws:ptr.global, x:ptr.global, n:i32, k:i32) regs=12
+  sreg %r2, tid
+  sreg %r3, ntid
+  sreg %r4, ctaid
+  mul %r5, %r4, %r3
+  add %r5, %r5, %r2
+  mul %r6, %r5, %r0
+  mul %r6, %r6, 4
+  mov %a2, %a0
+  add %a2, %a2, %r6
+  mov %r7, 0
+loop:
+  setp.ge %p0, %r7, %r0
+  bra %p0, done
+  ld.global.b32 %r8, [%a2]
+  add %r8, %r8, %r1
+  st.global.b32 [%a2], %r8
+  add %a2, %a2, 4
+  add %r7, %r7, 1
+  bra loop
+done:
+  ld.global.f32 %f0, [%a1]
+  exit
+
+kernel prep(tab:ptr.global, x:ptr.global) regs=8
+  sreg %r0, tid
+  sreg %r1, ntid
+  ld.global.b32 %r4, [%a1]
+top:
+  setp.ge %p0, %r0, 1024
+  bra %p0, fin
+  mul %r2, %r0, 4
+  mov %a2, %a0
+  add %a2, %a2, %r2
+  ld.global.b32 %r3, [%a2]
+  mul %r3, %r3, 3
+  add %r3, %r3, %r4
+  st.global.b32 [%a2], %r3
+  add %r0, %r0, %r1
+  bra top
+fin:
+  st.global.b32 [%a1], %r1
+  exit
+
+kernel use(tab:ptr.global, x:ptr.global, n:i32) regs=8
+  mul %r1, %r0, 4
+  mov %a2, %a0
+  add %a2, %a2, %r1
+  ld.global.b32 %r2, [%a2]
+  setp.lt %p0, %r2, 100
+  bra %p0, small
+  st.global.b32 [%a1], %r2
+  exit
+small:
+  st.global.b32 [%a1+4], %r2
+  exit
+
+kernel check(tab:ptr.global, n:i32) regs=4
+  mul %r1, %r0, 4
+  mov %a1, %a0
+  add %a1, %a1, %r1
+  ld.global.b32 %r2, [%a1]
+  exit
+
+kernel scribble(x:ptr.global, n:i32) regs=6
+  mov %r1, 0
+  mov %a1, %a0
+s_top:
+  setp.ge %p0, %r1, %r0
+  bra %p0, s_end
+  st.global.b32 [%a1], 7
+  add %a1, %a1, 4
+  add %r1, %r1, 1
+  bra s_top
+s_end:
+  exit
+
+kernel cmp(c:ptr.global, x:ptr.global, n:i32) regs=10
+  mov %r1, 0
+  mov %r2, 0
+  mov %a2, %a0
+  mov %a3, %a1
+c_top:
+  setp.ge %p0, %r1, 4
+  bra %p0, c_end
+  ld.global.b32 %r3, [%a2]
+  ld.global.b32 %r4, [%a3]
+  setp.eq %p1, %r3, %r4
+  bra !%p1, c_next
+  add %r2, %r2, 1
+c_next:
+  add %a2, %a2, 4
+  add %a3, %a3, 4
+  add %r1, %r1, 1
+  bra c_top
+c_end:
+  setp.gt %p2, %r2, 2
+  bra %p2, c_same
+  exit
+c_same:
+  st.global.b32 [%a0], %r2
+  exit
+"""
+
+FEATURE_MANIFESTS = {
+    "bufwrite": ("argspec x ptr global f32 count=16 seed=seq flo=-4 fhi=4\n"
+                 "argspec n i32 seed=160 lo=0 hi=400\n"
+                 "argspec k i32 seed=3 lo=-5 hi=5\n\n"
+                 "init:\n  alloc ws global 65536\n  copy_in ws seq32:16384\n"
+                 "compute:\n  launch fill grid=2 block=4 args=buf:ws,arg:0,arg:1,arg:2\n  copy_out ws 64\n"
+                 "term:\n  free ws\n"),
+    "initlaunch": ("argspec x ptr global i32 count=4 seed=seq lo=0 hi=9\n"
+                   "argspec n i32 seed=5 lo=0 hi=1100\n\n"
+                   "init:\n  alloc tab global 4096\n  copy_in tab seq32:1024\n"
+                   "  launch prep grid=1 block=4 args=buf:tab,arg:0\n  copy_out arg:0\n"
+                   "compute:\n  launch use grid=1 block=1 args=buf:tab,arg:0,arg:1\n  copy_out arg:0\n"
+                   "term:\n  free tab\n"),
+    "termlaunch": ("argspec x ptr global i32 count=4 seed=seq lo=0 hi=9\n"
+                   "argspec n i32 seed=5 lo=0 hi=1100\n\n"
+                   "init:\n  alloc tab global 4096\n  copy_in tab seq32:1024\n"
+                   "compute:\n  launch use grid=1 block=1 args=buf:tab,arg:0,arg:1\n"
+                   "term:\n  launch check grid=1 block=1 args=buf:tab,lit:i32:1024\n  free tab\n  free tab\n"),
+    "copyarg": ("argspec x ptr global i32 count=4 seed=seq lo=0 hi=9\n"
+                "argspec n i32 seed=2 lo=0 hi=4\n\n"
+                "compute:\n  alloc cbuf global 256\n  launch scribble grid=1 block=1 args=arg:0,arg:1\n"
+                "  copy_in cbuf arg:0\n  launch cmp grid=1 block=1 args=buf:cbuf,arg:0,arg:1\n  free cbuf\n"
+                "  copy_out arg:0\n"),
+}
+FEATURE_CAMPAIGN = dict(master_seed=11, iterations=600, round_size=128)
+
+
+def features():
+    import tempfile
+    out = {"kernel": FEATURES_SIR, "manifests": {}, "campaigns": {}, "fuzzloops": {},
+           "campaign_config": FEATURE_CAMPAIGN}
+    with tempfile.TemporaryDirectory() as tmp:
+        (Path(tmp) / "features.sir").write_text(FEATURES_SIR)
+        for name, body in FEATURE_MANIFESTS.items():
+            man = "program features.sir\n\n" + body
+            out["manifests"][name] = man
+            (Path(tmp) / f"{name}.man").write_text(man)
+            m = rc.load_harness(Path(tmp) / f"{name}.man")
+            out["campaigns"][name] = batched(m, **FEATURE_CAMPAIGN)
+            d = Path(tmp) / f"out-{name}"
+            s = rc.fuzz_loop(m, rc.CampaignConfig(master_seed=5, iterations=300, out_dir=d))
+            out["fuzzloops"][name] = {
+                "summary": s.to_rec(), "findings": (d / "findings.txt").read_text(),
+                "coverage_rec": (d / "coverage.rec").read_text(),
+                "corpus": sorted(p.name for p in (d / "corpus").iterdir()),
+                "crashes": sorted(p.name for p in (d / "crashes").iterdir())}
+    return out
+
+
 def _dump(obj) -> str:
     return json.dumps(obj, sort_keys=True, separators=(",", ":"))
 
@@ -439,7 +598,7 @@ def _dump(obj) -> str:
 def main():
     import tempfile
     which = sys.argv[1:] or ["assets", "variants", "sampled", "batched", "fuzzloop", "workloads", "traces",
-                             "errors", "loops"]
+                             "errors", "loops", "features"]
     if "assets" in which:
         (HERE / "bench_assets.json").write_text(_dump(assets()))
     if "variants" in which:
@@ -456,6 +615,8 @@ def main():
         (HERE / "ref_workloads.json").write_text(_dump(workloads()))
     if "traces" in which:
         (HERE / "ref_traces.json").write_text(_dump(traces()))
+    if "features" in which:
+        (HERE / "ref_features.json").write_text(_dump(features()))
     if "loops" in which:
         (HERE / "ref_loops.json").write_text(_dump(loops()))
     if "errors" in which:
