@@ -11,9 +11,10 @@ master_seed 11, batched rounds of R inputs.  One step = one round.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--round R] [--impl ours|reference]
 
---impl reference times the CPU port of the reference loop (oracle/, test
-infrastructure; the Python reference itself cannot travel to the GPU box) on
-all host cores, same metric and workload.
+--impl reference times the reference's own CPU loop on all host cores, same
+metric and workload: the unmodified reference ``fuzz_loop`` (installed offline
+into baseline/_ref, which travels with the repo) in one process per core, or,
+when that is absent, the CPU port of the loop (oracle/, test infrastructure).
 """
 
 from __future__ import annotations
@@ -103,7 +104,86 @@ def cpu_rate(workload: str, seconds: float, round_size: int, warm: float = 3.0):
     return execs / wall, execs, wall, pool.procs
 
 
+REF_PATH = REPO / "baseline" / "_ref"
+
+
+def reference_available() -> bool:
+    return (REF_PATH / "simt_forge" / "campaign.py").exists()
+
+
+def _ref_worker(workload, seed, seconds, q):
+    """One process of the reference arm: the reference's own fuzz_loop (public API,
+    amortized, one worker) on the bench workload until its wall-clock limit
+    (campaign.py:733-735); reports (compute_runs, wall_seconds)."""
+    sys.path.insert(0, str(REF_PATH))
+    from simt_forge import campaign as rc
+    m = rc.load_harness(REPO / "paper_2603_05725_b200" / "workloads" / f"{workload}.man")
+    s = rc.fuzz_loop(m, rc.CampaignConfig(master_seed=seed, iterations=10 ** 12, max_wall_seconds=seconds))
+    q.put((s.compute_runs, s.wall_seconds))
+
+
+def ref_rate(workload: str, seconds: float, procs: int | None = None):
+    """Aggregate execs/s of the unmodified reference fuzz_loop in ``procs`` processes
+    (master seeds 11, 12, ...), each one campaign of ``seconds`` (INIT included, as
+    in the reference's own execs_per_second, campaign.py:648-652)."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    procs = procs or os.cpu_count() or 1
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_ref_worker, args=(workload, 11 + i, seconds, q), daemon=True) for i in range(procs)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=seconds + 600) for _ in ps]
+    for p in ps:
+        p.join(timeout=5)
+    execs = sum(r[0] for r in res)
+    wall = max(r[1] for r in res)
+    return execs / wall, execs, wall, procs
+
+
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference(a):
+    if reference_available() and not a.ref_port:
+        return run_reference_fuzz_loop(a)
+    return run_reference_port(a)
+
+
+def run_reference_fuzz_loop(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    # each step: one wall-clock-bounded reference campaign per host core, sized so the
+    # whole --steps K --warmup W run takes a few minutes (3-10 s per step)
+    sec = a.ref_seconds if a.ref_seconds else min(10.0, max(3.0, 150.0 / (a.steps + a.warmup)))
+    per_step, total = [], 0
+    for s in range(a.warmup + a.steps):
+        rate, execs, wall, procs = ref_rate(a.workload, sec)
+        if s >= a.warmup:
+            per_step.append(wall)
+            total += execs
+    value = total / sum(per_step)
+    sample = (f"unmodified reference fuzz_loop (baseline/_ref, amortized, 1 worker) on {a.workload}, one "
+              f"{sec:.1f} s campaign per process per step, {procs} processes, master seeds 11..{10 + procs}; "
+              f"CPU {_cpu_model()}")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1000 * statistics.mean(per_step),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "i32/f32",
+            "data": "synthetic", "config": {"workload": WORKLOAD, "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def run_reference_port(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -215,7 +295,9 @@ def run_ours(a):
     # one campaign, each global round sharded over the ranks (R inputs per GPU per
     # round, weak scaling); per-round merge over NCCL
     comm = RoundComm()
-    R = a.round * world
+    # weak (default): R inputs per GPU per round; strong: R inputs per round in total
+    # (each rank R / N), so every N runs the same campaign (equal campaign digests)
+    R = a.round if a.scaling == "strong" else a.round * world
     dc = DeviceCampaign(m, master_seed=11, comm=comm)
     dc.timing = True
 
@@ -249,6 +331,7 @@ def run_ours(a):
         torch.cuda.synchronize()
     it += a.steps * R
     launches = dc.launches - launches0
+    digest = campaign_digest(dc)          # findings / coverage / corpus after the timed rounds
     executed = sum(r.executed for r in results)
     # K3 per round: bulk pass (every input, long ones deferred) and the whole execute
     bulk_ms = [s.elapsed_time(b) for s, b, e in dc.exec_events if b is not None]
@@ -304,6 +387,21 @@ def run_ours(a):
         "ncu_achieved_warps_per_sm": tprof.get("achieved_warps_per_sm"),
         "ncu_dram_bytes_per_launch": tprof.get("dram_bytes_per_launch")}
 
+    # ---- per-kernel rooflines from an isolated pass: a few more rounds one at a time
+    # (depth 1, nothing overlapping), CUDA events at every stage boundary
+    kernels = stage_profile(dc, it, R, a, peaks, torch) if world == 1 else None
+    if kernels:
+        dom = max(kernels, key=lambda k: k["ms_per_round"])
+        roof = {"bound": "hbm", "achieved": dom["achieved_gbs"], "peak": hbm_peak, "unit": "GB/s",
+                "frac": dom["achieved_gbs"] / hbm_peak, "traffic": dom.get("traffic"), "kernel": dom["kernel"],
+                "bytes_per_exec": dom["bytes_per_exec"], "launch_ms": dom["ms_per_round"],
+                "share_of_round": dom["share"],
+                "peak_source": ("MEASURED_PEAKS.json hbm_gbs (of measured)" if peaks else "fallback 6.65 TB/s"),
+                "traffic_source": dom.get("traffic_source"),
+                "timing": "isolated pass: rounds one at a time after the timed region, CUDA events on the round's "
+                          "stream around the stage",
+                "note": dom.get("note", "")}
+
     # ---- end to end through the public API with host buffers (the device-timed
     # campaign's buffers go back to the allocator first)
     if os.environ.get("SFG_BENCH_TIMELINE"):
@@ -319,18 +417,27 @@ def run_ours(a):
     import gc
     gc.collect()
     e2e = run_e2e(a, m, torch, R, world)
+    if world == 1 and not a.no_cold:
+        e2e["cold"] = run_e2e_cold(a, R, cache=True)
+        e2e["cold_no_jit_cache"] = run_e2e_cold(a, R, cache=False)
 
     if rank == 0:
         cpu = None
         if world == 1 and not a.no_cpu:
-            rate, execs, wall, procs = cpu_rate(a.workload, a.cpu_seconds, a.round)
-            cpu = {"value": rate, "unit": UNIT, "cores": procs, "kind": "port",
-                   "sample": f"oracle port of the reference loop on {a.workload} (batched contract, rounds of "
-                             f"{a.round}) in {procs} processes, one {a.cpu_seconds}s window after 3 s of start-up, "
-                             f"{execs} execs"}
+            if reference_available() and not a.ref_port:
+                rate, execs, wall, procs = ref_rate(a.workload, a.cpu_seconds)
+                cpu = {"value": rate, "unit": UNIT, "cores": procs, "kind": "reference",
+                       "sample": f"unmodified reference fuzz_loop (baseline/_ref) on {a.workload}, one {a.cpu_seconds}"
+                                 f" s campaign per process, {procs} processes, {execs} execs; CPU {_cpu_model()}"}
+            else:
+                rate, execs, wall, procs = cpu_rate(a.workload, a.cpu_seconds, a.round)
+                cpu = {"value": rate, "unit": UNIT, "cores": procs, "kind": "port",
+                       "sample": f"oracle port of the reference loop on {a.workload} (batched contract, rounds of "
+                                 f"{a.round}) in {procs} processes, one {a.cpu_seconds}s window after 3 s of "
+                                 f"start-up, {execs} execs; CPU {_cpu_model()}"}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": t_max * 1000 / a.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "i32/f32", "data": "synthetic",
+                "scaling": a.scaling, "vs_baseline": None, "dtype": "i32/f32", "data": "synthetic",
                 "config": {"workload": WORKLOAD, "round_size": R, "execs_per_step": R,
                            "rounds_in_flight": D, "engine": "jit" if dc.jit else "interpreter",
                            "l2": f"inputs larger than L2: {D} rounds in flight hold ~{D * R * 1900 >> 20} MiB of "
@@ -338,7 +445,7 @@ def run_ours(a):
                            "merge": f"per-round {backend.upper()} MIN/SUM all-reduce + all-gather ({collectives} collectives)"
                            if world > 1 else "none (1 GPU)"},
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(), "roofline": roof,
-                "issue_roofline": issue, "cpu_baseline": cpu}
+                "kernels": kernels, "issue_roofline": issue, "cpu_baseline": cpu, "campaign_digest": digest}
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
@@ -378,6 +485,127 @@ def run_e2e(a, m, torch, R, world):
             "findings_unique": len(s.findings), "stop": s.stop_reason, "setup_s": tr.get("setup_s")}
 
 
+def campaign_digest(dc) -> dict:
+    """sha256 of the campaign state: findings.txt, coverage.rec and the corpus ids
+    (equal across GPU counts with --scaling strong; tests/test_bench_parity.py pins
+    the same state against the reference for the first rounds)."""
+    import hashlib
+    from paper_2603_05725_b200.coverage import build_report, report_to_rec
+    findings = dc.findings.render_text()
+    cov = report_to_rec(build_report(dc.coverage_map()))
+    corpus = "\n".join(e[0].id for e in dc.host_entries)
+    h = hashlib.sha256((findings + "\0" + cov + "\0" + corpus).encode()).hexdigest()
+    return {"sha256": h, "findings_unique": len(dc.findings), "findings_total": dc.findings.total,
+            "corpus": len(dc.host_entries), "rounds": dc.rounds}
+
+
+# algorithmic off-chip bytes per exec of each stage (SURVEY.md §8(d)): what the stage
+# must read and write given its inputs and outputs, not what the layout moves
+def _stage_bytes(dc):
+    from paper_2603_05725_b200.lowering import CHILD, VAL, VERDICT
+    seed = dc.host_entries[0][0]
+    payload = sum(len(v.data) for v in seed.args if hasattr(v, "data"))
+    scalars = 4 * sum(1 for v in seed.args if not hasattr(v, "data"))
+    E = dc.E
+    return {
+        "K1 sfg_plan + sfg_mutate (+ scans)": (2 * dc.n_args * VAL.itemsize + CHILD.itemsize,
+                                               "parent value descriptors read, child record + descriptors "
+                                               "written (the stage's own layout: 64-B descriptors)"),
+        "K2 sfg_apply": (2 * payload, "parent payload read + child work region written"),
+        "sfg_order (3 kernels)": (8 + dc.n_args * VAL.itemsize, "descriptors read, bucket + position written"),
+        "K3 bulk sfg_jit_execute": (payload + scalars + 64 + 4 * ((E + 31) // 32),
+                                    "child payload read once + 64-B verdict + hit bitmap (SURVEY.md §8(d))"),
+        "K3 tail sfg_apply + sfg_jit_tail": (payload + scalars + 64 + 4 * ((E + 31) // 32),
+                                             "as the bulk pass, for the deferred inputs; per round input"),
+        "K4 triage (stop/absorb/admit + scans)": (VERDICT.itemsize + 4 * E + 24,
+                                                  "verdict + edge-count row read, admission / alloc words written"),
+    }
+
+
+def stage_profile(dc, it, R, a, peaks, torch):
+    """Each stage's device time per round with nothing overlapping: ``a.profile_rounds``
+    rounds run one at a time (depth 1) after the timed region."""
+    pairs = [("submit", "mutated", "K1 sfg_plan + sfg_mutate (+ scans)"), ("mutated", "applied", "K2 sfg_apply"),
+             ("applied", "ordered", "sfg_order (3 kernels)"), ("ordered", "bulk", "K3 bulk sfg_jit_execute"),
+             ("bulk", "tail", "K3 tail sfg_apply + sfg_jit_tail"),
+             ("triage_start", "triaged", "K4 triage (stop/absorb/admit + scans)")]
+    dc.stage_marks = []
+    dc.run_rounds(it, it + a.profile_rounds * R, R, depth=1)
+    torch.cuda.synchronize()
+    marks = {}
+    for ri, name, ev in dc.stage_marks:
+        marks.setdefault(ri, {})[name] = ev          # last mark of a stage wins (re-runs)
+    dc.stage_marks = None
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    sizes = _stage_bytes(dc)
+    ncu = {}
+    nf = REPO / "profiles" / "r02_ncu_kernels.json"
+    if nf.exists():
+        ncu = json.loads(nf.read_text())
+    out = []
+    for s0, s1, label in pairs:
+        ms = [m[s0].elapsed_time(m[s1]) for m in marks.values() if s0 in m and s1 in m]
+        if not ms:
+            continue
+        t = statistics.mean(ms)
+        bpe, what = sizes[label]
+        gbs = bpe * R / (t / 1000.0) / 1e9 if t > 0 else 0.0
+        k = {"kernel": label, "ms_per_round": t, "bytes_per_exec": bpe, "bytes_note": what,
+             "achieved_gbs": gbs, "hbm_frac": gbs / hbm, "rounds": len(ms)}
+        n = ncu.get(label)
+        if n:
+            k.update(n)
+        out.append(k)
+    total = sum(k["ms_per_round"] for k in out)
+    for k in out:
+        k["share"] = k["ms_per_round"] / total if total else None
+    return out
+
+
+def run_e2e_cold(a, R, cache: bool):
+    """fuzz_loop in a fresh process (CUDA context, program build, allocation of the
+    round buffers all inside the measurement).  cache=False: an empty JIT cubin cache,
+    so the NVRTC compile of the specialized kernels is included as well."""
+    import tempfile
+    env = dict(os.environ)
+    tmp = None
+    if not cache:
+        tmp = tempfile.mkdtemp(prefix="sfg_jit_cold_")
+        env["SFG_JIT_CACHE"] = tmp
+    cmd = [sys.executable, str(REPO / "bench.py"), "--e2e-cold-child", "--round", str(R), "--depth", str(a.depth),
+           "--workload", a.workload, "--steps", str(a.steps)]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900)
+        line = [l for l in r.stdout.splitlines() if l.startswith("{")]
+        return json.loads(line[-1]) if line else {"error": r.stderr[-400:]}
+    except Exception as e:  # noqa: BLE001 - reported, not fatal to the bench line
+        return {"error": str(e)}
+
+
+def e2e_cold_child(a):
+    t_proc = time.perf_counter()
+    import torch
+    import paper_2603_05725_b200  # noqa: F401
+    from paper_2603_05725_b200 import _native
+    from paper_2603_05725_b200.campaign import CampaignConfig, fuzz_loop
+    from paper_2603_05725_b200.workloads import load
+    t0 = time.perf_counter()
+    torch.cuda.init()
+    torch.zeros(1, device="cuda")
+    t_ctx = time.perf_counter() - t0
+    steps = max(2 * a.steps, 48)
+    m = load(a.workload)
+    s = fuzz_loop(m, CampaignConfig(master_seed=11, iterations=steps * a.round, round_size=a.round,
+                                    pipeline_depth=a.depth))
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    print(json.dumps({"value": s.compute_runs / wall, "unit": UNIT, "wall_s": wall, "execs": s.compute_runs,
+                      "context_s": t_ctx, "setup_s": s.device_transfer.get("setup_s"),
+                      "import_s": t0 - t_proc, **_native.jit_stats(),
+                      "includes": "CUDA context, program build (NVRTC or on-disk cubin cache), INIT baseline, "
+                                  "round-buffer allocation, all rounds, result objects (python/torch import excluded)"}))
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -387,13 +615,23 @@ def main():
     p.add_argument("--depth", type=int, default=24, help="rounds in flight (speculative pipelining); at most "
                    "~30 so that every round's stream has its own hardware queue (CUDA_DEVICE_MAX_CONNECTIONS=32)")
     p.add_argument("--workload", default="matmul")
+    p.add_argument("--profile-rounds", type=int, default=4, help="rounds of the isolated per-kernel pass")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--cpu-seconds", type=float, default=15.0)
     p.add_argument("--ref-seconds", type=float, default=0.0,
                    help="seconds per process per reference step (default: 120 s / (steps + warmup), 1-10 s)")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--ref-port", action="store_true", help="reference arm / CPU baseline: the oracle port even "
+                   "when the reference is installed in baseline/_ref")
+    p.add_argument("--no-cold", action="store_true", help="skip the cold-process end-to-end runs")
+    p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                   help="weak: --round inputs per GPU per round; strong: --round inputs per round over all GPUs "
+                        "(the same campaign at every N)")
+    p.add_argument("--e2e-cold-child", action="store_true", help=argparse.SUPPRESS)
     a = p.parse_args()
-    if a.impl == "reference":
+    if a.e2e_cold_child:
+        e2e_cold_child(a)
+    elif a.impl == "reference":
         run_reference(a)
     else:
         run_ours(a)

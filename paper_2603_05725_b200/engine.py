@@ -272,6 +272,9 @@ class DeviceCampaign:
         self.ov_grows = 0                # copy-on-write overlay enlargements (rounds re-run)
         self.timing = False              # record CUDA events around each execute kernel
         self.exec_events: list = []
+        # stage profiling (bench.py per-kernel rooflines): when a list, every round
+        # appends (stage name, CUDA event) marks on its stream at stage boundaries
+        self.stage_marks = None
 
     # ---- INIT launches / TERM phase: one-input device programs ------------------------
     def _phase_program(self, script, baseline, *, term=False):
@@ -435,6 +438,7 @@ class DeviceCampaign:
             S.sub_ev = torch.cuda.Event(enable_timing=True)
             S.sub_ev.record(st)
             S.sub_host = time.perf_counter()
+        self._mark(S, "submit")
         self.launches += 2 + 3 * C
         _native.check(L.sfg_plan(hp, ctypes.byref(cd), it0, n, S.parent.data_ptr(), S.picks.data_ptr(),
                                  S.flags.data_ptr(), s), "plan")
@@ -467,9 +471,17 @@ class DeviceCampaign:
             if S.readouts is not None:
                 S.readouts.record_stream(st)
             S.readouts = None
+        self._mark(S, "mutated")
         _native.check(L.sfg_apply(hp, ctypes.byref(cd), n, S.children.data_ptr(), S.vals.data_ptr(),
                                   S.work_base.data_ptr(), S.work.data_ptr(), s), "apply")
+        self._mark(S, "applied")
         self._execute(S, n, self.soft_cap, cd)
+
+    def _mark(self, S: Slot, name: str):
+        if self.stage_marks is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(S.stream)
+            self.stage_marks.append((S.round_index, name, ev))
 
     def _submit_sequential(self, S: Slot, cd):
         """Children of the round from the worker stream, one after another (sfg_plan_seq),
@@ -521,12 +533,14 @@ class DeviceCampaign:
             _native.check(self.L.sfg_order(self.h, n, S.vals.data_ptr(), S.order.data_ptr(),
                                            S.order_scratch.data_ptr(), st.cuda_stream), "order")
             order = S.order.data_ptr()
+            self._mark(S, "ordered")
         _native.check(self.L.sfg_execute(
             self.h, n, S.children.data_ptr(), S.vals.data_ptr(), S.work_base.data_ptr(), S.work.data_ptr(),
             S.verdicts.data_ptr(), S.ecnt.data_ptr(), _ptr(S.readouts), S.ro_base.data_ptr(),
             S.counter.data_ptr(), soft, S.deferred.data_ptr() if tail else None, self.max_entry_work, order,
             st.cuda_stream), "execute")
         if tail:
+            self._mark(S, "bulk")
             if self.timing:
                 evb = torch.cuda.Event(enable_timing=True)
                 evb.record(st)
@@ -542,6 +556,7 @@ class DeviceCampaign:
                 self.max_entry_work, ts.cuda_stream), "execute_deferred")
             if ts is not st:
                 st.wait_stream(ts)
+            self._mark(S, "tail")
         if self.timing:
             ev[1].record(st)
             S.exec_ev = ev
@@ -557,6 +572,7 @@ class DeviceCampaign:
         s = st.cuda_stream
         n, ib = S.n, S.i_base
         self.launches += 7
+        self._mark(S, "triage_start")
         with torch.cuda.stream(st):
             S.mins.fill_(NONE)
             S.sums.zero_()
@@ -576,6 +592,7 @@ class DeviceCampaign:
                       "triage_admit")
         self._scan64(S, S.admit, n, 1, 0, S.pos, 2)
         self._scan64(S, S.allocs, n, 1, 0, S.allocs_prefix, 3)
+        self._mark(S, "triaged")
         with torch.cuda.stream(st):
             S.small.copy_(S.tot[2:4])
             gath = comm.all_gather(S.small, st)
