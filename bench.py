@@ -7,7 +7,7 @@ reference's ``compute_runs`` unit (campaign.py:648-652, 748).
 
 Workload: C2 of SURVEY.md §8(d) — the tiled matmul target with
 stride/size-argument OOB bugs (paper_2603_05725_b200/workloads/matmul.man),
-master_seed 11, batched rounds of R inputs.  One step = one round.
+master_seed 11, batched rounds of R = 2^20 inputs.  One step = one round.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--round R] [--impl ours|reference]
 
@@ -417,6 +417,8 @@ def run_ours(a):
     import gc
     gc.collect()
     e2e = run_e2e(a, m, torch, R, world)
+    if world == 1 and not a.no_sequential:
+        e2e["sequential_discipline"] = run_e2e_sequential(a, m, torch)
     if world == 1 and not a.no_cold:
         e2e["cold"] = run_e2e_cold(a, R, cache=True)
         e2e["cold_no_jit_cache"] = run_e2e_cold(a, R, cache=False)
@@ -562,6 +564,24 @@ def stage_profile(dc, it, R, a, peaks, torch):
     return out
 
 
+def run_e2e_sequential(a, m, torch):
+    """fuzz_loop with discipline="sequential": the reference fuzz_loop's own stream
+    discipline (one worker stream, live corpus), byte-identical output directories
+    (tests/test_gpu_parity.py), on the same workload; rounds of 2^16 generated in
+    order on the device and cut after each admission."""
+    from paper_2603_05725_b200.campaign import CampaignConfig, fuzz_loop
+    iters = a.sequential_execs
+    cfg = CampaignConfig(master_seed=11, iterations=iters, round_size=1 << 16, discipline="sequential")
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s = fuzz_loop(m, cfg)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    return {"value": s.compute_runs / wall, "unit": UNIT, "wall_s": wall, "execs": s.compute_runs,
+            "rounds": s.device_transfer["rounds"], "corpus_interesting": s.corpus.interesting,
+            "api": "campaign.fuzz_loop(manifest, CampaignConfig(discipline='sequential'))"}
+
+
 def run_e2e_cold(a, R, cache: bool):
     """fuzz_loop in a fresh process (CUDA context, program build, allocation of the
     round buffers all inside the measurement).  cache=False: an empty JIT cubin cache,
@@ -611,7 +631,10 @@ def main():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=96)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--round", type=int, default=262144)
+    # one round = 2^20 inputs (BASELINE.json configs[1]: 1M execs on 1 B200): a round's
+    # latency is its slowest input (~15 ms), so larger rounds amortize pipeline fill /
+    # drain over more work (R = 2^18 / 2^19 / 2^20: 90 / 103 / 110 M execs/s, 20 steps)
+    p.add_argument("--round", type=int, default=1 << 20)
     p.add_argument("--depth", type=int, default=24, help="rounds in flight (speculative pipelining); at most "
                    "~30 so that every round's stream has its own hardware queue (CUDA_DEVICE_MAX_CONNECTIONS=32)")
     p.add_argument("--workload", default="matmul")
@@ -624,6 +647,8 @@ def main():
     p.add_argument("--ref-port", action="store_true", help="reference arm / CPU baseline: the oracle port even "
                    "when the reference is installed in baseline/_ref")
     p.add_argument("--no-cold", action="store_true", help="skip the cold-process end-to-end runs")
+    p.add_argument("--no-sequential", action="store_true", help="skip the sequential-discipline e2e run")
+    p.add_argument("--sequential-execs", type=int, default=1 << 22)
     p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                    help="weak: --round inputs per GPU per round; strong: --round inputs per round over all GPUs "
                         "(the same campaign at every N)")

@@ -27,6 +27,7 @@ from .findings import BugClass, FindingsLog
 from .hooks import ExecHooks, TraceHooks, dispatch  # noqa: F401  (re-export)
 from .lowering import LoweringError
 from .manifest import HarnessManifest, load_harness  # noqa: F401  (re-export)
+from .interop import as_config, as_manifest, as_testcase
 from .testcase import argspec_digest, serialize_testcase
 
 
@@ -83,6 +84,16 @@ class CampaignConfig:
     # generated in order on the device and cut after each admission -- results
     # identical to the reference fuzz_loop, output directories byte for byte
     discipline: str = "batched"
+    # extensions for BASELINE.json configs 3-4 (not reference fields): the 16 MiB
+    # context-sensitive hashed coverage map (2^ctx_map_bits one-byte slots, a derived
+    # view; summary.context_map_slots), extra seed test cases added to the corpus
+    # after the manifest seed, and fixed fan-out (input it mutates round-corpus entry
+    # ((it - 1) // fanout) mod n instead of schedule_next); soft_cap: retired
+    # instructions before an input moves to the long-input pass (None = default)
+    ctx_map_bits: int = 0
+    extra_seeds: tuple = ()
+    fanout: int = 0
+    soft_cap: int | None = None
 
 
 @dataclass
@@ -108,6 +119,12 @@ class CampaignSummary:
     @property
     def execs_per_second(self) -> float:
         return self.compute_runs / self.wall_seconds if self.wall_seconds > 0 else 0.0
+
+    def to_reference(self, sf, reference_manifest):
+        """(FindingsLog, CoverageMap, Corpus) as the reference package's own types
+        (``sf`` = the imported ``simt_forge`` module; interop.summary_to_reference)."""
+        from .interop import summary_to_reference
+        return summary_to_reference(self, sf, reference_manifest.program)
 
     def to_rec(self) -> str:
         return "\n".join([
@@ -139,10 +156,14 @@ def _device_campaign(manifest, config: CampaignConfig, comm) -> DeviceCampaign:
                           diff_readback=config.diff_readback, stop_on_first_finding=config.stop_on_first_finding,
                           stop_bug_class=config.stop_bug_class, device=config.device,
                           ids_reset_per_input=config.mode == "reinit",
-                          sequential=config.discipline == "sequential")
+                          sequential=config.discipline == "sequential", ctx_map_bits=config.ctx_map_bits,
+                          extra_seeds=tuple(as_testcase(t) for t in config.extra_seeds), fanout=config.fanout,
+                          soft_cap=config.soft_cap)
 
 
 def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
+    # the reference's own objects are accepted as they are (interop.py)
+    manifest, config = as_manifest(manifest), as_config(config)
     if config.mode not in ("amortized", "reinit"):
         raise CampaignFatalError(f"unknown mode {config.mode!r}")
     if config.workers < 1 or config.iterations < 1:
@@ -269,6 +290,8 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
     # host<->device traffic of the campaign (not a reference field; bench e2e accounting)
     summary.device_transfer = {"h2d_bytes": dc.h2d_bytes, "d2h_bytes": dc.d2h_bytes, "rounds": dc.rounds,
                                "setup_s": t_setup}
+    if config.ctx_map_bits:
+        summary.context_map_slots = dc.ctx_map_slots()
     dc.close()
     return summary
 

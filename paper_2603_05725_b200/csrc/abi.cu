@@ -17,7 +17,7 @@ struct sfg_program {
   int jit_grid = 0;                   // resident CTAs (occupancy x SMs)
   int tail_grid = 0;                  // resident one-warp tail CTAs
   int sms = 0;
-  int tail_k = 4;                     // long inputs per tail warp (group-parallel pass)
+  int tail_k = 1;                     // long inputs per tail warp (group-parallel pass): 1 = lowest latency
   int tail_k_seq = 32;                // inputs per warp of the thread-sequential re-run pass
   int tail_ctas = 1024;               // one-warp CTAs of the long-input pass
   int bulk_persist = 1;               // bulk pass: persistent grid (1) or a CTA per batch (0)

@@ -260,7 +260,8 @@ class DeviceCampaign:
         self.cap = self.data_cap = self.n_corpus = self.corpus_bytes = 0
         self.max_entry_work = 0
         self.host_entries: list = []     # (TestCase, admitted_iteration, is_seed)
-        seeds = [self.seed_tc] + list(extra_seeds)
+        from .interop import as_testcase
+        seeds = [self.seed_tc] + [as_testcase(t) for t in extra_seeds]
         self._upload_seeds(seeds)
         self.n_seeds = len(seeds)
         self.slots: list[Slot] = []
@@ -1051,6 +1052,8 @@ class DeviceCampaign:
         ("mem", kernel, iid, ctaid, tid, space, addr, width, is_store) /
         ("cf", kernel, ctaid, tid, src_block, dst_block), executor.py:108-135),
         recorded on the device by the generic interpreter (sfg_execute_trace)."""
+        from .interop import as_testcase
+        tcs = [as_testcase(t) for t in tcs]
         n = len(tcs)
         S = self._aux_slot(n)
         self.drain()

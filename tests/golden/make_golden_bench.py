@@ -17,7 +17,7 @@ inputs) during absorption.
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden_bench.py [c2] [c5]
 
 Writes (gzip JSON, committed):
-  ref_bench_c2.json.gz  workloads/matmul.man, master_seed 11, R = 262,144:
+  ref_bench_c2.json.gz  workloads/matmul.man, master_seed 11, R = 2^20 (bench.py's default):
                         round 1 in full (per-1024-input block hashes of the
                         records, the first 20,000 records verbatim, findings /
                         coverage / corpus after the round) and the first 4,096
@@ -171,7 +171,7 @@ def campaign(name, *, master_seed, round_size, rounds, keep_prefix, procs):
     return out
 
 
-C2 = dict(name="matmul.man", master_seed=11, round_size=262144, rounds=[262144, 4096], keep_prefix=20000)
+C2 = dict(name="matmul.man", master_seed=11, round_size=1 << 20, rounds=[1 << 20, 4096], keep_prefix=20000)
 C5 = dict(names=("dot", "amax", "rotm"), master_seed=11, round_size=1 << 14, rounds=[1 << 14, 1 << 14],
           keep_prefix=2000)
 

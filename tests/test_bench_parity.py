@@ -1,7 +1,7 @@
 """Parity at the benchmarked configurations (tests/golden/make_golden_bench.py).
 
 C2: the bench's own setup -- workloads/matmul.man, master_seed 11, rounds of
-R = 262,144, 24 rounds in flight, the default soft cap (long inputs deferred to
+R = 2^20, 24 rounds in flight, the default soft cap (long inputs deferred to
 the tail pass), sfg_order on -- against the REAL reference's batched-round
 records: every input of round 1 (per-1024-input block hashes of the records,
 the first 20,000 records compared field by field), the campaign state after
@@ -90,7 +90,7 @@ def test_c2_bench_configuration_matches_reference(cuda_ok):
     from paper_2603_05725_b200.engine import DeviceCampaign
     ref = _gz("ref_bench_c2.json.gz")
     cfg = ref["config"]
-    assert cfg["round_size"] == 262144
+    assert cfg["round_size"] == 1 << 20      # bench.py's default --round
     dc = DeviceCampaign(workload_manifest("matmul"), master_seed=cfg["master_seed"])   # bench.py's defaults
     _check_rounds(dc, ref["rounds"], ref["block"], depth=24)
     dc.close()

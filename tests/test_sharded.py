@@ -117,7 +117,7 @@ def test_round_merge_gloo_world2():
 # ---------------------------------------------------------------- GPU: the product path, sharded
 
 
-def _campaign_worker(rank, world, port, out_path, which):
+def _campaign_worker(rank, world, port, out_path, which, backend="gloo"):
     import hashlib
     import json
     import sys
@@ -127,9 +127,10 @@ def _campaign_worker(rank, world, port, out_path, which):
     from paper_2603_05725_b200.engine import DeviceCampaign
     from paper_2603_05725_b200.shard import RoundComm
     from paper_2603_05725_b200.testcase import serialize_testcase
-    torch.cuda.set_device(0)
+    # gloo: every rank on cuda:0 (collectives staged through host memory); nccl: one GPU per rank
+    torch.cuda.set_device(rank if backend == "nccl" else 0)
     if world > 1:
-        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        dist.init_process_group(backend, init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     if which == "matmul":
         from conftest import workload_manifest
         m, R, iters = workload_manifest("matmul"), 100, 300
@@ -155,6 +156,27 @@ def test_sharded_campaign_equals_reference(cuda_ok, which):
     with tempfile.TemporaryDirectory() as d:
         out = os.path.join(d, "res.json")
         mp.start_processes(_campaign_worker, args=(2, _free_port(), out, which), nprocs=2, start_method="spawn")
+        got = json.load(open(out))
+    ref = golden("ref_workloads.json")["matmul"] if which == "matmul" else golden("ref_batched.json")["runs"][which]
+    assert got["findings"] == ref["findings"]
+    assert got["coverage"] == ref["coverage"]
+    assert got["corpus"] == ref["corpus"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("which", ["amax", "matmul"])
+def test_nccl_sharded_campaign_equals_reference(cuda_ok, which, world):
+    """The NCCL path itself (one process per GPU, NCCL all-reduce / all-gather of the
+    per-round partials): the sharded campaign equals the reference golden records
+    for every GPU count the box has (skipped on a one-GPU box)."""
+    import json
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "res.json")
+        mp.start_processes(_campaign_worker, args=(world, _free_port(), out, which, "nccl"), nprocs=world,
+                           start_method="spawn")
         got = json.load(open(out))
     ref = golden("ref_workloads.json")["matmul"] if which == "matmul" else golden("ref_batched.json")["runs"][which]
     assert got["findings"] == ref["findings"]
