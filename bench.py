@@ -234,6 +234,8 @@ class ClockSampler:
         # NVML is initialized here, before the timed region: nvmlInit takes driver
         # locks for tens of ms and stalled kernel launches when it ran inside it
         self._nv = self._h = self._mx = None
+        if os.environ.get("SFG_BENCH_NO_NVML"):    # diagnostics: no sampling at all
+            return
         try:
             import pynvml as nv
             nv.nvmlInit()
@@ -262,6 +264,13 @@ class ClockSampler:
     def __exit__(self, *exc):
         self._stop.set()
         self._t.join(timeout=6)
+        # NVML left initialized in the process was seen to stall later kernel launches
+        # (end-to-end runs after the timed region 20-35 % slower in 2 of 5 runs)
+        if self._nv is not None and not os.environ.get("SFG_BENCH_NVML_KEEP"):
+            try:
+                self._nv.nvmlShutdown()
+            except Exception:
+                pass
 
     def summary(self):
         if not self.rows:

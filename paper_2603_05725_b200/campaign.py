@@ -273,6 +273,8 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
         if dc is not None:    # release the round buffers now, not at garbage collection
             dc.close()
         raise
+    if dc.round_log is not None:
+        dc.round_log.append(("loop_end", -1, time.perf_counter()))
     wall = time.perf_counter() - t0
     corpus = Corpus([CorpusEntry(tc, adm, seed) for tc, adm, seed in dc.host_entries])
     cov = dc.coverage_map()
@@ -292,6 +294,9 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
                                "setup_s": t_setup}
     if config.ctx_map_bits:
         summary.context_map_slots = dc.ctx_map_slots()
+    if dc.round_log is not None:
+        dc.round_log.append(("summary", -1, time.perf_counter()))
+        summary.device_transfer["round_log"] = list(dc.round_log)
     dc.close()
     return summary
 

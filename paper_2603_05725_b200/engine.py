@@ -276,6 +276,8 @@ class DeviceCampaign:
         # stage profiling (bench.py per-kernel rooflines): when a list, every round
         # appends (stage name, CUDA event) marks on its stream at stage boundaries
         self.stage_marks = None
+        # diagnostics: host clock of every submission / finalization (SFG_ROUND_LOG=1)
+        self.round_log = [] if os.environ.get("SFG_ROUND_LOG") else None
 
     # ---- INIT launches / TERM phase: one-input device programs ------------------------
     def _phase_program(self, script, baseline, *, term=False):
@@ -875,11 +877,17 @@ class DeviceCampaign:
         # every slot this call will use exists before the first submission: allocating
         # device memory mid-pipeline can stall the device behind in-flight rounds
         if plan:
+            if self.round_log is not None:
+                self.round_log.append(("reserve", -1, time.perf_counter()))
             self.reserve(min(depth, len(plan)), max(n for _, n in plan))
+            if self.round_log is not None:
+                self.round_log.append(("reserved", -1, time.perf_counter()))
 
         def submit(k):
             it_k, n_k = plan[k]
             S = self._slot(k % depth, n_k)
+            if self.round_log is not None:
+                self.round_log.append(("submit", k, time.perf_counter()))
             self._submit(S, it_k, n_k, base_round + k)
             inflight.append((k, S))
 
@@ -899,7 +907,11 @@ class DeviceCampaign:
         fill()
         while inflight:
             k, S = inflight.popleft()
+            if self.round_log is not None:
+                self.round_log.append(("finalize", k, time.perf_counter()))
             res = self._finalize(S)
+            if self.round_log is not None:
+                self.round_log.append(("finalized", k, time.perf_counter()))
             results.append(res)
             if on_round is not None:
                 on_round(res)
