@@ -35,6 +35,13 @@ SFG_DEV uint32_t sfg_fop(int op, uint32_t a, uint32_t b) {
   return sfg_fop_nan(a, b);
 }
 
+// the same op where the result's NaN payload cannot be observed (jit.cu f_observers)
+SFG_DEV uint32_t sfg_fop_any(int op, uint32_t a, uint32_t b) {
+  if (op == SFG_FADD) return sfg_b(__fadd_rn(sfg_f(a), sfg_f(b)));
+  if (op == SFG_FSUB) return sfg_b(__fsub_rn(sfg_f(a), sfg_f(b)));
+  return sfg_b(__fmul_rn(sfg_f(a), sfg_f(b)));
+}
+
 SFG_DEV uint32_t sfg_quiet(uint32_t b) { return b | (sfg_isnan_bits(b) ? 0x00400000u : 0u); }
 
 // read-only views of the device corpus (entries at round start)

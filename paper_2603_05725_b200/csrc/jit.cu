@@ -592,13 +592,36 @@ struct Gen {
   // through a double) only then: fadd/fsub/fmul (sfg_fop quiets its first NaN
   // operand itself), float setp and cvt cannot tell a signaling NaN from its
   // quieted form.
-  std::vector<char> fbits;
-  void f_observers(const sfg_ins* I, int n, int regs) {
+  // A store observes its value's bits unless it is write-only into memory that is
+  // dead after the launch (the `wo` stores of emit_mem: a pointer parameter's record
+  // that no load of the kernel reaches, no untagged load, no later launch or
+  // readout) -- then fadd/fsub/fmul results headed only there need no x86 NaN
+  // payload fix-up either (sfg_fop_any: any NaN is as good as another to fadd /
+  // fmul / setp / cvt and to a store nobody reads).
+  // fexact[r]: the NaN payload of f register r matters -- r's bits are observable,
+  // or r is an operand of a payload-exact fadd/fsub/fmul (which propagates the
+  // payload of its first NaN operand); closed backwards over the arithmetic.
+  std::vector<char> fbits, fexact;
+  void f_observers(const sfg_ins* I, int n, int regs, const std::vector<std::vector<int>>& tags) {
     fbits.assign(regs > 0 ? regs : 1, 0);
     for (int i = 0; i < n; ++i) {
       const sfg_ins& x = I[i];
       if (x.op == SFG_MOV && x.mode == SFG_CLS_F && !(x.flags & SFG_F_S1_IMM)) fbits[x.s1] = 1;
-      if (x.op == SFG_ST && x.mode == SFG_MK_F32 && !(x.flags & SFG_F_S2_IMM)) fbits[x.s2] = 1;
+      if (x.op == SFG_ST && x.mode == SFG_MK_F32 && !(x.flags & SFG_F_S2_IMM)) {
+        const int tg = tags[i][x.s1];
+        const bool wo = tg > 0 && dead_now && !any_untagged_load && !loaded[tg - 1];
+        if (!wo) fbits[x.s2] = 1;
+      }
+    }
+    fexact = fbits;
+    for (bool changed = true; changed;) {
+      changed = false;
+      for (int i = 0; i < n; ++i) {
+        const sfg_ins& x = I[i];
+        if ((x.op != SFG_FADD && x.op != SFG_FSUB && x.op != SFG_FMUL) || !fexact[x.dst]) continue;
+        if (!(x.flags & SFG_F_S1_IMM) && !fexact[x.s1]) fexact[x.s1] = changed = true;
+        if (!(x.flags & SFG_F_S2_IMM) && !fexact[x.s2]) fexact[x.s2] = changed = true;
+      }
     }
   }
   std::string AT() const { return narrow ? "int64_t" : "i128"; }
@@ -682,7 +705,8 @@ struct Gen {
       case SFG_FADD:
       case SFG_FSUB:
       case SFG_FMUL:
-        o << "    " << f(x.dst) << " = sfg_fop(" << (int)x.op << ", " << src_f(x, 1) << ", " << src_f(x, 2) << ");\n";
+        o << "    " << f(x.dst) << " = " << (fexact[x.dst] ? "sfg_fop(" : "sfg_fop_any(") << (int)x.op << ", "
+          << src_f(x, 1) << ", " << src_f(x, 2) << ");\n";
         break;
       case SFG_SETP:
         if (x.flags & SFG_F_FLOAT)
@@ -724,7 +748,6 @@ struct Gen {
     cur_na = K.na;
     const sfg_ins* I = ins + K.base;
     narrow = narrow_ok(I, K.n);
-    f_observers(I, K.n, K.regs);
     const std::vector<int> starts = block_starts(I, K.n);
     std::vector<int> blk_of;
     const auto tags = tag_flow(I, K.n, K, starts, blk_of);
@@ -740,6 +763,7 @@ struct Gen {
       else if (tg != TAG_BOT) (st ? any_untagged_store : any_untagged_load) = true;  // BOT: unreachable
     }
     dead_now = (dead_kernels >> kidx) & 1u;
+    f_observers(I, K.n, K.regs, tags);
 
     o << "template <bool PAR>\nstatic __device__ __forceinline__ int sim_" << kidx
       << "(JitRunner& J, const sfg_prog& P, Lane& L, Mem& M, sfg_verdict& V, const Pre& pre, int ctaid, int tid, "
