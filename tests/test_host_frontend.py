@@ -200,8 +200,9 @@ def test_control_taint_mask():
 
 
 def test_bench_reference_arm_cpu():
-    """bench.py --impl reference: the CPU port of the reference loop on the bench
-    workload in clock-bounded windows; one JSON line with the contract's keys."""
+    """bench.py --impl reference: the unmodified reference fuzz_loop from
+    baseline/_ref when it is installed, else the CPU port of the reference loop, on
+    the bench workload in clock-bounded windows; one JSON line with the contract's keys."""
     import json
     import subprocess
     import sys
@@ -212,8 +213,12 @@ def test_bench_reference_arm_cpu():
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "execs/s"
-    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
-    assert line["e2e"]["h2d_bytes_per_step"] == 0 and 900 <= line["ms_per_step"] <= 1500
+    want = "reference" if (root / "baseline" / "_ref" / "simt_forge").is_dir() else "port"
+    assert line["cpu_baseline"]["kind"] == want and line["cpu_baseline"]["cores"] >= 1
+    # the port measures clock windows; the reference arm's step also holds the
+    # campaign processes' start-up (numpy import, manifest load, INIT)
+    hi = 1500 if want == "port" else 30000
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and 900 <= line["ms_per_step"] <= hi
 
 
 def test_jit_pointer_register_width():
