@@ -92,6 +92,24 @@ int sfg_stream_state_init(uint64_t seed, uint64_t stream_id, void* out_host);
 int sfg_plan_seq(const sfg_program* p, const sfg_corpus_dev* c, int64_t it0, int n, const void* state,
                  const uint64_t* counts_base, void* children, void* vals, uint32_t* int_flags, void* states,
                  void* stream);
+/* Sequential discipline in parallel (mutate.cu "seqgen"): the same outputs as
+ * sfg_plan_seq (children, vals, int_flags, states[n + 1]) computed without a
+ * one-thread walk: every candidate child boundary of the worker stream's next
+ * `words` words draws one child, pointer doubling finds the boundaries reachable
+ * from *state, and the children are generated in parallel from them.  Requires
+ * it0 >= 2, saturated rotation counts (every mutable column of counts_base >= 3),
+ * no fan-out and no corpus entry leaving the recent window inside the round.
+ * stats[0] = children whose start was found (the round must be cut after
+ * stats[0] - 1 when < n; states[stats[0]] is exact), stats[1] = words drawn by
+ * them.  scratch: sfg_seq_scratch_ints(n, words) int32 of device memory. */
+int64_t sfg_seq_scratch_ints(int n, int64_t words);
+int sfg_plan_seq_par(const sfg_program* p, const sfg_corpus_dev* c, int64_t it0, int n, const void* state,
+                     int64_t words, const uint64_t* counts_base, void* children, void* vals, uint32_t* int_flags,
+                     void* states, int32_t* scratch, int64_t scratch_ints, uint64_t* stats, void* stream);
+/* Children it0 .. it0+n-1 (batched contract).  Input i's rotation count of int
+ * column c is counts_base[c] + counts_prefix[i][c]; counts_prefix may be NULL when
+ * every mutable column of counts_base is >= 3 (the counts then no longer steer
+ * generation, mutation.py:378-386, and no plan pass / pick scans are needed). */
 int sfg_mutate(const sfg_program* p, const sfg_corpus_dev* c, int64_t it0, int n,
                const uint64_t* counts_prefix, const uint64_t* counts_base, void* children,
                void* vals, void* stream);

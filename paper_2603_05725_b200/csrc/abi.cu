@@ -265,7 +265,29 @@ int sfg_program_create(const void* prog, size_t prog_bytes, const void* ins, siz
       }
       dead &= ~alive;
     }
-    const int rc = sfg_jit_build(p->P, (const sfg_ins*)ins, events, dead, p->jit_source, p->jit_log, &p->jit_lib,
+    // the lane's allocator tables at this harness's static bounds (checked against the
+    // ceilings at load time, lowering.py): INIT records + one record per array
+    // argument (materialized once) and per COMPUTE alloc; the baseline quarantine /
+    // free list + one entry per COMPUTE free
+    sfgjit::LaneCaps caps;
+    {
+      int n_ptr = 0, n_alloc = 0, n_free_ops = 0;
+      for (int a = 0; a < p->P.n_args; ++a) n_ptr += p->P.arg_kind[a] == SFG_V_ARR;
+      for (size_t h = 0; h < n_hostops; ++h) {
+        n_alloc += H[h].kind == SFG_H_ALLOC;
+        n_free_ops += H[h].kind == SFG_H_FREE;
+      }
+      auto clampc = [](int v, int hi) { return v < 1 ? 1 : (v > hi ? hi : v); };
+      caps.recs = clampc(p->P.n_base_recs + n_ptr + n_alloc, SFG_MAX_LANE_RECS);
+      caps.q = clampc(p->P.n_quar + n_free_ops, 32);
+      caps.freel = clampc(p->P.n_free + p->P.n_quar + n_free_ops, 32);
+      caps.named = clampc(p->P.n_named, SFG_MAX_NAMED);
+      caps.args = clampc(p->P.n_args, SFG_MAX_ARGS);
+      int np = 1;
+      for (int k = 0; k < p->P.n_kernels; ++k) np = p->P.kernels[k].n_params > np ? p->P.kernels[k].n_params : np;
+      caps.params = clampc(np, SFG_MAX_ARGS);
+    }
+    const int rc = sfg_jit_build(p->P, (const sfg_ins*)ins, events, dead, caps, p->jit_source, p->jit_log, &p->jit_lib,
                                  &p->jit_kernel, &p->jit_tail);
     if (rc != 0) {
       g_err = "sfg_program_create: JIT build failed (" + std::to_string(rc) + "): " + p->jit_log.substr(0, 6000);
@@ -380,7 +402,7 @@ int sfg_jit_check(const void* prog, size_t prog_bytes, const void* ins, uint64_t
   memcpy(&P, prog, sizeof P);
   std::string src, log;
   std::vector<char> cubin;
-  const int rc = sfg_jit_compile(P, (const sfg_ins*)ins, max_edge_events, 0u, src, log, cubin);
+  const int rc = sfg_jit_compile(P, (const sfg_ins*)ins, max_edge_events, 0u, sfgjit::LaneCaps{}, src, log, cubin);
   const std::string text = rc ? log + "\n----\n" + src : src;
   if (out && cap) {
     const size_t n = text.size() < cap - 1 ? text.size() : cap - 1;
@@ -430,6 +452,51 @@ int sfg_plan_seq(const sfg_program* p, const sfg_corpus_dev* c, int64_t it0, int
   sfg_plan_seq_kernel<<<1, 32, 0, S(stream)>>>(p->P, CV(c), it0, n, (const SfgStream*)state, counts_base,
                                                 (sfg_child*)children, (sfg_val*)vals, int_flags, (SfgStream*)states);
   SFG_CHECK_LAUNCH("sfg_plan_seq");
+  return 0;
+}
+
+static int seq_levels(int n) {
+  int k = 1;
+  while ((1ll << k) <= (int64_t)n) ++k;
+  return k;
+}
+
+int64_t sfg_seq_scratch_ints(int n, int64_t words) {
+  if (n <= 0 || words <= 0) return 0;
+  return (int64_t)seq_levels(n) * 2 * words + (n + 1) + 4;
+}
+
+int sfg_plan_seq_par(const sfg_program* p, const sfg_corpus_dev* c, int64_t it0, int n, const void* state,
+                     int64_t words, const uint64_t* counts_base, void* children, void* vals, uint32_t* int_flags,
+                     void* states, int32_t* scratch, int64_t scratch_ints, uint64_t* stats, void* stream) {
+  if (n <= 0) return 0;
+  if (it0 < 2 || words <= 0 || 2 * words >= (int64_t)0x7FFFFFFF || scratch_ints < sfg_seq_scratch_ints(n, words)) {
+    g_err = "sfg_plan_seq_par: bad arguments (it0 >= 2, 0 < 2*words < 2^31, scratch of sfg_seq_scratch_ints)";
+    return 1;
+  }
+  const int K = seq_levels(n);
+  const int64_t M = 2 * words;
+  int32_t* J = scratch;                       // K levels of M successors
+  int32_t* path = scratch + (int64_t)K * M;   // n + 1
+  int32_t* q0 = path + n + 1;
+  cudaStream_t st = S(stream);
+  const SfgStream* start = (const SfgStream*)state;
+  unsigned long long* stt = (unsigned long long*)stats;
+  sfg_seq_root_kernel<<<1, 32, 0, st>>>(p->P, CV(c), it0, n, start, words, counts_base, (sfg_child*)children,
+                                        (sfg_val*)vals, int_flags, (SfgStream*)states, path, q0, stt);
+  sfg_seq_walk_kernel<<<blocks_for(M, 128), 128, 0, st>>>(p->P, CV(c), it0, start, words, J);
+  const int jb = (int)std::min<int64_t>(blocks_for(M, 256), (int64_t)(p->sms > 0 ? p->sms : 148) * 8);
+  for (int k = 0; k + 1 < K; ++k)
+    sfg_seq_jump_kernel<<<jb, 256, 0, st>>>(J + (int64_t)k * M, J + (int64_t)(k + 1) * M, M);
+  for (int k = K - 1; k >= 0; --k) {
+    const int64_t step = 1ll << k;
+    const int64_t threads = ((int64_t)n + 2 * step) / (2 * step);
+    sfg_seq_path_kernel<<<blocks_for(threads, 128), 128, 0, st>>>(J + (int64_t)k * M, path, q0, n, step);
+  }
+  sfg_seq_mutate_kernel<<<blocks_for(n, 128), 128, 0, st>>>(p->P, CV(c), it0, n, start, path, q0, counts_base,
+                                                            (sfg_child*)children, (sfg_val*)vals, int_flags,
+                                                            (SfgStream*)states, stt);
+  SFG_CHECK_LAUNCH("sfg_plan_seq_par");
   return 0;
 }
 

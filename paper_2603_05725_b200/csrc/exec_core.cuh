@@ -33,8 +33,31 @@
 namespace {
 
 constexpr uint8_t SH_RZ = 0xFA, SH_FREED = 0xFD, SH_UNALLOC = 0xFF;
-constexpr int kMaxQ = 32;
-constexpr int kMaxFree = 32;
+// Per-input table capacities.  The generic interpreter uses the ceilings; the
+// specialized kernels define them from the harness's static bounds (jit.cu
+// LaneCaps: INIT records + one record per array argument and COMPUTE alloc, the
+// baseline quarantine / free list + one entry per COMPUTE free), so a lane's
+// tables are a few hundred bytes and stay in L1 instead of spilling to DRAM.
+#ifndef SFG_LANE_RECS
+#define SFG_LANE_RECS SFG_MAX_LANE_RECS
+#endif
+#ifndef SFG_LANE_Q
+#define SFG_LANE_Q 32
+#endif
+#ifndef SFG_LANE_FREE
+#define SFG_LANE_FREE 32
+#endif
+#ifndef SFG_LANE_NAMED
+#define SFG_LANE_NAMED SFG_MAX_NAMED
+#endif
+#ifndef SFG_LANE_ARGS
+#define SFG_LANE_ARGS SFG_MAX_ARGS
+#endif
+#ifndef SFG_LANE_PARAMS   // kernel parameters of a launch (bound values by class)
+#define SFG_LANE_PARAMS SFG_MAX_ARGS
+#endif
+constexpr int kMaxQ = SFG_LANE_Q;
+constexpr int kMaxFree = SFG_LANE_FREE;
 
 enum : uint8_t { R_FREED = 1, R_RES = 2, R_BASE = 4 };
 
@@ -47,14 +70,14 @@ struct LRec {            // 48 bytes
 };
 
 struct Lane {
-  LRec rec[SFG_MAX_LANE_RECS];
+  LRec rec[SFG_LANE_RECS];
   int nrec, nalloc, nq, nfree, nov;
   int64_t cursor[3], qbytes[3];
   int16_t quar[kMaxQ];
   sfg_free fl[kMaxFree];
-  int64_t named_addr[SFG_MAX_NAMED];
-  int16_t named_rec[SFG_MAX_NAMED];
-  int16_t mat_rec[SFG_MAX_ARGS];
+  int64_t named_addr[SFG_LANE_NAMED];
+  int16_t named_rec[SFG_LANE_NAMED];
+  int16_t mat_rec[SFG_LANE_ARGS];
   uint64_t ro_cursor;
 };
 
@@ -232,7 +255,7 @@ SFG_DEV int lane_alloc(const sfg_prog& P, Lane& L, int sp, int64_t size, int lab
     off = L.cursor[sp];
     L.cursor[sp] += slot;
   }
-  if (L.nrec >= SFG_MAX_LANE_RECS) return -SFG_ST_LANE_RECS;
+  if (L.nrec >= SFG_LANE_RECS) return -SFG_ST_LANE_RECS;
   LRec& r = L.rec[L.nrec];
   r.slot_start = sbase(sp) + off;
   r.slot_end = r.slot_start + slot;
@@ -442,9 +465,9 @@ SFG_DEV void edge_hit(uint32_t* ecnt, int e, bool& overflow) {
 
 // bound launch arguments, per register class in parameter order (executor.py:167-188)
 struct Pre {
-  uint32_t r[SFG_MAX_ARGS], f[SFG_MAX_ARGS];
-  int64_t a[SFG_MAX_ARGS];
-  int32_t ap[SFG_MAX_ARGS];
+  uint32_t r[SFG_LANE_PARAMS], f[SFG_LANE_PARAMS];
+  int64_t a[SFG_LANE_PARAMS];
+  int32_t ap[SFG_LANE_PARAMS];
   int nr, nf, na;
 };
 

@@ -127,6 +127,13 @@ static std::vector<std::vector<int>> tag_flow(const sfg_ins* I, int n, const KIn
   return at;
 }
 
+// Static bounds of one input's allocator tables for this harness (sizes the
+// lane's Lane struct in the specialized kernels, exec_core.cuh SFG_LANE_*).
+struct LaneCaps {
+  int recs = SFG_MAX_LANE_RECS, q = 32, freel = 32, named = SFG_MAX_NAMED, args = SFG_MAX_ARGS,
+      params = SFG_MAX_ARGS;
+};
+
 struct Gen {
   const sfg_prog& P;
   const sfg_ins* ins;
@@ -649,6 +656,7 @@ struct Gen {
   // bit k: memory is dead after every launch of kernel k (no later launch in the
   // COMPUTE script, no readouts) -- its stores can only be observed by its own loads
   uint32_t dead_kernels = 0;
+  LaneCaps caps;
   bool dead_now = false;
 
   std::string src_r(const sfg_ins& x, int slot) {
@@ -910,11 +918,14 @@ struct Gen {
   bool loop_summaries = true;
   int n_summaries = 0;
   int tail_minb = 12;
-  int bulk_minb = 3;
+  int bulk_minb = 4;
 
   std::string run(int n_edges, uint64_t max_edge_events) {
     edge_ovf_checks = max_edge_events >= 0xFFFFFFFFull;
     const int NE = n_edges > 0 ? n_edges : 1;
+    o << "#define SFG_LANE_RECS " << caps.recs << "\n#define SFG_LANE_Q " << caps.q << "\n#define SFG_LANE_FREE "
+      << caps.freel << "\n#define SFG_LANE_NAMED " << caps.named << "\n#define SFG_LANE_ARGS " << caps.args
+      << "\n#define SFG_LANE_PARAMS " << caps.params << "\n";
     o << "#include \"exec_core.cuh\"\n\nnamespace {\n\n";
     o << "constexpr uint32_t kPoll = 4096u;\n";
     // loop-summary helpers (see analyse_cycle)
@@ -1123,13 +1134,14 @@ static void jit_cache_store(const std::string& key, const std::vector<char>& cub
 
 // Generate and compile; on success `cubin` holds the sm_100a image.  Returns 0 on success.
 static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_edge_events, uint32_t dead_kernels,
-                           std::string& source,
+                           const sfgjit::LaneCaps& caps, std::string& source,
                            std::string& log, std::vector<char>& cubin) {
   sfgjit::Gen g(P, ins);
   g.dead_kernels = dead_kernels;
+  g.caps = caps;
   if (const char* ls = getenv("SFG_LOOPSUM")) g.loop_summaries = atoi(ls) != 0;
   if (const char* tb = getenv("SFG_TAIL_MINB")) g.tail_minb = atoi(tb) >= 1 ? atoi(tb) : 12;
-  if (const char* bb = getenv("SFG_BULK_MINB")) g.bulk_minb = atoi(bb) >= 1 ? atoi(bb) : 3;
+  if (const char* bb = getenv("SFG_BULK_MINB")) g.bulk_minb = atoi(bb) >= 1 ? atoi(bb) : 4;
   source = g.run(P.n_edges, max_edge_events);
   // process-wide cache: identical programs (same generated source) compile once;
   // then the on-disk cache across processes
@@ -1189,10 +1201,10 @@ static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_e
 
 // Generate, compile and load the specialized execute kernels (bulk + tail).  Returns 0 on success.
 static int sfg_jit_build(const sfg_prog& P, const sfg_ins* ins, uint64_t max_edge_events, uint32_t dead_kernels,
-                         std::string& source,
+                         const sfgjit::LaneCaps& caps, std::string& source,
                          std::string& log, cudaLibrary_t* lib_out, cudaKernel_t* kern_out, cudaKernel_t* tail_out) {
   std::vector<char> cubin;
-  const int rc = sfg_jit_compile(P, ins, max_edge_events, dead_kernels, source, log, cubin);
+  const int rc = sfg_jit_compile(P, ins, max_edge_events, dead_kernels, caps, source, log, cubin);
   if (rc) return rc;
   cudaError_t e = cudaLibraryLoadData(lib_out, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
   if (e != cudaSuccess) {

@@ -43,6 +43,8 @@ from .testcase import MutationError, TestCase
 NONE = 0x7FFFFFFF   # "no index" in the triage MIN buffers (sfg.h)
 STATUS = {0: "ok", 1: "finding", 2: "budget"}
 DEFAULT_SOFT_CAP = 1 << 15   # retired instructions before an input moves to the tail pass
+SEQ_PAR_MIN = 64      # sequential discipline: smaller rounds walk the stream on one thread
+SEQ_ROUND0 = 4096     # sequential discipline: first round size (doubles while rounds run to their end)
 
 
 class CorpusDev(ctypes.Structure):
@@ -130,6 +132,9 @@ class Slot:
         self.order = i32(cap)            # bulk-pass schedule (sfg_order)
         # sequential discipline: worker stream state before every input and after the last
         self.states = u8((cap + 1) * dc.state_bytes) if dc.sequential else None
+        self.seq_par, self.seq_scratch, self.seq_words = False, None, 0
+        self.seq_stats = i64(2)          # seqgen: [children found, words they drew]
+        self.pin_seq = torch.zeros(2, dtype=torch.int64, pin_memory=True)
         self.order_scratch = i32(int(dc.L.sfg_order_scratch_ints(cap)))
         # triage partials (merged across ranks between the phases, sfg.h):
         # MIN: [stop, fatal, first_hit[E], key_first[K]]; SUM: [edge_delta[E], key_count[K], entered[16]]
@@ -140,6 +145,10 @@ class Slot:
         self.edelta, self.kcount, self.ent = self.sums[:E0], self.sums[E0:E0 + K0], self.sums[E0 + K0:]
         self.small = i64(2)              # [admitted, allocs] of this rank, all-gathered
         self.counts_base = torch.zeros(C, dtype=torch.int64, device=dev)
+        self.counts_after = torch.zeros(max(C, 1), dtype=torch.int64, device=dev)
+        self.pin_ca = torch.zeros(max(C, 1), dtype=torch.int64, pin_memory=True)
+        self.counts_after_valid = False
+        self.sat_base = False
         self.pin_tot = torch.empty(8 + 16, dtype=torch.int64, pin_memory=True)
         self.pin_sc = torch.empty(2, dtype=torch.int32, pin_memory=True)
         self.pin_gath = torch.empty((dc.comm.world, 2), dtype=torch.int64, pin_memory=True)
@@ -187,6 +196,9 @@ class DeviceCampaign:
         # sequential: the reference fuzz_loop's own stream discipline (one worker stream,
         # rounds cut after each admission) instead of the batched-round contract
         self.sequential = bool(sequential)
+        self.seq_single = os.environ.get("SFG_SEQ_SINGLE", "0") == "1"   # force the one-thread walk (tests / A-B)
+        self._seq_mu = 12.0            # words per child (seqgen candidate range), refined per round
+        self.seq_truncations = 0
         self.state_bytes = int(self.L.sfg_stream_state_bytes())
         if self.sequential and (self.comm.world > 1 or fanout):
             raise LoweringError("the sequential discipline runs on one device without fan-out")
@@ -244,6 +256,14 @@ class DeviceCampaign:
         self.ghit = torch.zeros(max(self.E, 1), dtype=torch.uint8, device=self.dev)
         self.entered = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.counts_run = torch.zeros(max(self.C, 1), dtype=torch.int64, device=self.dev)
+        # MutationSchedule rotation counts only steer generation while below 3
+        # (mutation.py:378-386): once every mutable int column has reached 3 they are
+        # saturated for the rest of the worker, and a round needs neither the plan
+        # pass nor the per-column pick scans (sfg_mutate with a NULL prefix)
+        P0 = self.low.prog
+        self._sat_cols = [int(P0["int_slot"][a]) for a in range(int(P0["n_args"]))
+                          if int(P0["int_slot"][a]) >= 0 and not int(P0["arg_fixed"][a])]
+        self._counts_sat = not self._sat_cols
         self.seq_state = torch.zeros(self.state_bytes, dtype=torch.uint8, device=self.dev)
         self._set_worker_stream(0)
         # context-sensitive hashed coverage map (derived view, csrc/ctxmap.cu)
@@ -413,6 +433,7 @@ class DeviceCampaign:
         self.drain()
         self.counts_run.zero_()
         self._last_counts = None
+        self._counts_sat = not self._sat_cols
         self.next_alloc_id = self.base.next_id
         if self.sequential:
             self._set_worker_stream(w)
@@ -442,25 +463,42 @@ class DeviceCampaign:
             S.sub_ev.record(st)
             S.sub_host = time.perf_counter()
         self._mark(S, "submit")
-        self.launches += 2 + 3 * C
-        _native.check(L.sfg_plan(hp, ctypes.byref(cd), it0, n, S.parent.data_ptr(), S.picks.data_ptr(),
-                                 S.flags.data_ptr(), s), "plan")
-        for c in range(C):
-            _native.check(L.sfg_scan_u32(S.flags.data_ptr(), n, C, c, S.prefix.data_ptr(), C, c, S.tmp.data_ptr(),
-                                         S.tot.data_ptr() + 8 * (8 + c), s), "scan flags")
-        with torch.cuda.stream(st):
-            if not resubmit:                   # a re-submitted round keeps its rotation base
-                if self._last_counts is not None:
-                    st.wait_event(self._last_counts)
-                S.counts_base.copy_(self.counts_run)
-                if C:
-                    # rotation counts: picks of earlier slices of the round come first
-                    g = comm.all_gather(S.tot[8:8 + C], st)
-                    S.counts_base[:C] += g[:comm.rank].sum(0)
-                    self.counts_run[:C] += g.sum(0)
-                S.ev_counts.record(st)
-                self._last_counts = S.ev_counts
-        _native.check(L.sfg_mutate(hp, ctypes.byref(cd), it0, n, S.prefix.data_ptr(), S.counts_base.data_ptr(),
+        if self._counts_sat:
+            # saturated rotation counts: no plan pass, no pick scans; counts_run is
+            # frozen (every mutable column >= 3) and serves as every round's base
+            self.launches += 1
+            prefix = None
+            S.counts_after_valid = False
+            if not getattr(S, "sat_base", False):
+                with torch.cuda.stream(st):
+                    if self._last_counts is not None:
+                        st.wait_event(self._last_counts)
+                    S.counts_base.copy_(self.counts_run)
+                S.sat_base = True
+        else:
+            self.launches += 2 + 3 * C
+            S.sat_base = False
+            prefix = S.prefix.data_ptr()
+            _native.check(L.sfg_plan(hp, ctypes.byref(cd), it0, n, S.parent.data_ptr(), S.picks.data_ptr(),
+                                     S.flags.data_ptr(), s), "plan")
+            for c in range(C):
+                _native.check(L.sfg_scan_u32(S.flags.data_ptr(), n, C, c, S.prefix.data_ptr(), C, c,
+                                             S.tmp.data_ptr(), S.tot.data_ptr() + 8 * (8 + c), s), "scan flags")
+            with torch.cuda.stream(st):
+                if not resubmit:                   # a re-submitted round keeps its rotation base
+                    if self._last_counts is not None:
+                        st.wait_event(self._last_counts)
+                    S.counts_base.copy_(self.counts_run)
+                    if C:
+                        # rotation counts: picks of earlier slices of the round come first
+                        g = comm.all_gather(S.tot[8:8 + C], st)
+                        S.counts_base[:C] += g[:comm.rank].sum(0)
+                        self.counts_run[:C] += g.sum(0)
+                    S.counts_after.copy_(self.counts_run)   # read at finalize: saturated yet?
+                    S.counts_after_valid = True
+                    S.ev_counts.record(st)
+                    self._last_counts = S.ev_counts
+        _native.check(L.sfg_mutate(hp, ctypes.byref(cd), it0, n, prefix, S.counts_base.data_ptr(),
                                    S.children.data_ptr(), S.vals.data_ptr(), s), "mutate")
         cw = CHILD.itemsize // 8
         self._scan64(S, S.children.view(torch.int64), n, cw, CHILD.fields["work_bytes"][1] // 8, S.work_base, 0)
@@ -498,10 +536,29 @@ class DeviceCampaign:
             if self._last_done is not None:     # the previous round's cut fixes our start
                 st.wait_event(self._last_done)
             S.counts_base.copy_(self.counts_run)
-        self.launches += 1
-        _native.check(L.sfg_plan_seq(hp, ctypes.byref(cd), it0, n, self.seq_state.data_ptr(),
-                                     S.counts_base.data_ptr(), S.children.data_ptr(), S.vals.data_ptr(),
-                                     S.flags.data_ptr(), S.states.data_ptr(), s), "plan_seq")
+        # children in parallel (seqgen, sfg_plan_seq_par) when the round's children
+        # depend on nothing but the stream: it0 >= 2, saturated rotation counts, no
+        # corpus entry leaving the recent window inside the round (the round
+        # planner cuts there); otherwise one thread walks the stream
+        S.seq_par = it0 >= 2 and self._counts_sat and n >= SEQ_PAR_MIN and not self.seq_single
+        if S.seq_par:
+            words = int(self._seq_mu * n * 1.25) + 256
+            need = int(L.sfg_seq_scratch_ints(n, words))
+            if S.seq_scratch is None or S.seq_scratch.numel() < need:
+                if S.seq_scratch is not None:
+                    S.seq_scratch.record_stream(st)
+                S.seq_scratch = torch.empty(need, dtype=torch.int32, device=self.dev)
+            self.launches += 4 + 2 * max(1, n.bit_length())
+            _native.check(L.sfg_plan_seq_par(hp, ctypes.byref(cd), it0, n, self.seq_state.data_ptr(), words,
+                                             S.counts_base.data_ptr(), S.children.data_ptr(), S.vals.data_ptr(),
+                                             S.flags.data_ptr(), S.states.data_ptr(), S.seq_scratch.data_ptr(),
+                                             S.seq_scratch.numel(), S.seq_stats.data_ptr(), s), "plan_seq_par")
+            S.seq_words = words
+        else:
+            self.launches += 1
+            _native.check(L.sfg_plan_seq(hp, ctypes.byref(cd), it0, n, self.seq_state.data_ptr(),
+                                         S.counts_base.data_ptr(), S.children.data_ptr(), S.vals.data_ptr(),
+                                         S.flags.data_ptr(), S.states.data_ptr(), s), "plan_seq")
         cw = CHILD.itemsize // 8
         self._scan64(S, S.children.view(torch.int64), n, cw, CHILD.fields["work_bytes"][1] // 8, S.work_base, 0)
         S.ensure_work(n * self.max_entry_work + 64, self.dev)
@@ -604,11 +661,18 @@ class DeviceCampaign:
             S.pin_gath.copy_(gath, non_blocking=True)
             if self.K:
                 S.pin_kc[:self.K].copy_(S.kcount, non_blocking=True)
+            if S.counts_after_valid and not self._counts_sat:
+                S.pin_ca.copy_(S.counts_after, non_blocking=True)
+            if self.sequential and S.seq_par:
+                S.pin_seq.copy_(S.seq_stats, non_blocking=True)
             self.d2h_bytes += S.pin_sc.nbytes + S.pin_tot.nbytes + S.pin_gath.nbytes + 8 * self.K
             ev = torch.cuda.Event()
             ev.record(st)
         ev.synchronize()
         stop, fatal = (int(x) for x in S.pin_sc.numpy())
+        if S.counts_after_valid and not self._counts_sat:
+            ca = S.pin_ca.numpy()
+            self._counts_sat = all(int(ca[c]) >= 3 for c in self._sat_cols)
         return stop, fatal, S.pin_gath.numpy().copy()
 
     def _finalize(self, S: Slot) -> RoundResult:
@@ -631,11 +695,23 @@ class DeviceCampaign:
             stop, fatal, gathered = self._triage_pass(S)
         N = S.round_n
         cut = None
+        if self.sequential and S.seq_par:
+            found, used = (int(x) for x in S.pin_seq.numpy())
+            if found > 0:   # words per child, for the next round's candidate range
+                self._seq_mu = max(2.0, 0.5 * self._seq_mu + 0.5 * used / found)
+            if found < N:
+                # the seqgen path ran out of candidates at `found`: the round ends
+                # there (states[found] is exact) and the next resumes from it
+                if used >= 0.8 * S.seq_words or found == 0:
+                    self._seq_mu *= 1.5
+                self.seq_truncations += 1
+                cut = max(found, 1) - 1
+                stop, fatal, gathered = self._triage_pass(S, cut=cut)
         if self.sequential and int(gathered[:, 0].sum()):
             executed0 = N if stop == NONE else stop + 1
             adm = _np(S.admit[:S.n], np.int64)
             first = int(np.argmax(adm != 0))
-            if first < executed0 - 1:
+            if first < executed0 - 1 and (cut is None or first < cut):
                 cut = first
                 stop, fatal, gathered = self._triage_pass(S, cut=cut)
         if fatal != NONE and fatal <= stop:
@@ -666,6 +742,10 @@ class DeviceCampaign:
                 self.seq_state.copy_(S.states[k * self.state_bytes:(k + 1) * self.state_bytes])
                 if self.C and k:
                     self.counts_run[:self.C] += S.flags[:k * self.C].view(k, self.C).sum(0).to(torch.int64)
+            if not self._counts_sat and self._sat_cols:
+                with torch.cuda.stream(st):
+                    ca = self.counts_run.cpu().numpy()
+                self._counts_sat = all(int(ca[c]) >= 3 for c in self._sat_cols)
         S.ev_done.record(st)
         self._last_done = S.ev_done
         self.rounds += 1
@@ -826,8 +906,15 @@ class DeviceCampaign:
         results = []
         it = it0
         self.reserve(1, min(round_size, max(it_stop - it0, 1)))
+        size = min(round_size, SEQ_ROUND0)
+        window = int(self.low.prog["window"])
         while it < it_stop and (should_continue is None or should_continue()):
-            n = min(round_size, it_stop - it)
+            n = min(size, it_stop - it)
+            # a round never spans a corpus entry leaving the recent window
+            # (schedule_next's weights change there, campaign.py:593-603)
+            flips = [adm + window + 1 for _, adm, seed in self.host_entries if not seed and adm + window + 1 > it]
+            if flips:
+                n = max(1, min(n, min(flips) - it))
             S = self._slot(0, n)
             self._submit(S, it, n, self.rounds)
             res = self._finalize(S)
@@ -837,7 +924,40 @@ class DeviceCampaign:
             if res.stop is not None:
                 break
             it += res.executed
+            # rounds grow while they run to their end and shrink when cut (an
+            # admission): a cut round's later children are generated for nothing
+            size = min(round_size, 2 * size) if res.executed >= n else max(SEQ_ROUND0, size // 2)
         return results
+
+    def seq_generate(self, it0: int, n: int, parallel: bool, words: int | None = None):
+        """Sequential discipline, generation only (tests / diagnostics): children
+        it0 .. it0+n-1 from the current worker state, by the one-thread walk or
+        by seqgen.  Returns host copies (children, vals, int flags, states[n + 1],
+        stats or None); the worker state is not advanced."""
+        S = Slot(self, max(n, 1024), 99)
+        cd = self.corpus_dev()
+        s = S.stream.cuda_stream
+        L, hp = self.L, self.h
+        with torch.cuda.stream(S.stream):
+            S.stream.wait_stream(torch.cuda.current_stream())
+            S.counts_base.copy_(self.counts_run)
+        stats = None
+        if parallel:
+            words = words or int(self._seq_mu * n * 1.25) + 256
+            scratch = torch.empty(int(L.sfg_seq_scratch_ints(n, words)), dtype=torch.int32, device=self.dev)
+            _native.check(L.sfg_plan_seq_par(hp, ctypes.byref(cd), it0, n, self.seq_state.data_ptr(), words,
+                                             S.counts_base.data_ptr(), S.children.data_ptr(), S.vals.data_ptr(),
+                                             S.flags.data_ptr(), S.states.data_ptr(), scratch.data_ptr(),
+                                             scratch.numel(), S.seq_stats.data_ptr(), s), "plan_seq_par")
+        else:
+            _native.check(L.sfg_plan_seq(hp, ctypes.byref(cd), it0, n, self.seq_state.data_ptr(),
+                                         S.counts_base.data_ptr(), S.children.data_ptr(), S.vals.data_ptr(),
+                                         S.flags.data_ptr(), S.states.data_ptr(), s), "plan_seq")
+        S.stream.synchronize()
+        out = (S.children[:n * CHILD.itemsize].cpu().numpy(), S.vals[:n * self.n_args * VAL.itemsize].cpu().numpy(),
+               S.flags[:n * self.C].cpu().numpy(), S.states[:(n + 1) * self.state_bytes].cpu().numpy(),
+               S.seq_stats.cpu().numpy() if parallel else None)
+        return out
 
     def reserve(self, depth: int, round_size: int) -> None:
         """Allocate the device buffers of ``depth`` rounds of ``round_size`` inputs

@@ -439,3 +439,54 @@ def test_wide_pointer_registers_match_oracle(engine_cls):
     # wild addresses past 2^63 and below 0, out-of-bounds and space mismatches
     assert len(kinds) >= 5 and any(k[2] for k in kinds) and any(k[3] for k in kinds)
     dc.close()
+
+
+@pytest.mark.parametrize("name", ["matmul", "vadd", "structcfg", "dot", "amax", "rotm", "axpy"])
+def test_seqgen_equals_one_thread_walk(engine_cls, name):
+    """The sequential discipline's parallel generator (seqgen: every candidate child
+    boundary of the worker stream draws one child, pointer doubling finds the
+    boundaries reachable from the worker state, children generated in parallel)
+    gives the one-thread walk's children, values, int picks and stream states bit
+    for bit over 20,000 children -- the walk is the path pinned to the reference
+    fuzz_loop (test_sequential_fuzz_loop_matches_reference_output_dir)."""
+    from conftest import workload_manifest
+    from paper_2603_05725_b200.engine import CHILD
+    m = bench_manifest(name) if name in bench_names() else workload_manifest(name)
+    dc = engine_cls(m, master_seed=11, sequential=True)
+    dc.new_worker(0)
+    dc.run_rounds(1, 1 + 512, 512)            # one-thread rounds until the rotation counts saturate
+    assert dc._counts_sat
+    # no corpus entry may leave the recent window inside the generated range
+    window = int(dc.low.prog["window"])
+    it0 = max([513] + [adm + window + 1 for _, adm, seed in dc.host_entries if not seed])
+    n = 20000
+    a = dc.seq_generate(it0, n, parallel=False)
+    b = dc.seq_generate(it0, n, parallel=True)
+    found = int(b[4][0])
+    assert found == n, (found, dc.seq_truncations)
+    assert (a[0] == b[0]).all()
+    assert (a[1] == b[1]).all()
+    assert (a[2] == b[2]).all()
+    assert (_stream_states(a[3]) == _stream_states(b[3])).all()
+    # a candidate range too short for the round truncates it exactly: the children
+    # found are the walk's, and the resume state after them is exact
+    c = dc.seq_generate(it0, n, parallel=True, words=3000)
+    k = int(c[4][0])
+    assert 0 < k < n
+    cw, sb = CHILD.itemsize, dc.state_bytes
+    assert (c[0][:k * cw] == a[0][:k * cw]).all()
+    assert (_stream_states(c[3][:(k + 1) * sb]) == _stream_states(a[3][:(k + 1) * sb])).all()
+    dc.close()
+
+
+def _stream_states(raw):
+    """SfgStream records (philox.cuh) with the bytes that carry no state cleared: the
+    32-bit cache word when no half-word is cached, and the padding."""
+    import numpy as np
+    st = np.frombuffer(raw.tobytes(), dtype=np.dtype([("ctr", "<u8", (4,)), ("key", "<u8", (2,)), ("buf", "<u8", (4,)),
+                                                      ("pos", "<u4"), ("has32", "<u4"), ("cache32", "<u4"),
+                                                      ("pad", "<u4")])).copy()
+    assert st.dtype.itemsize == 96
+    st["cache32"][st["has32"] == 0] = 0
+    st["pad"] = 0
+    return st
