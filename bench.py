@@ -476,21 +476,27 @@ def run_e2e(a, m, torch, R, world):
     steps = max(2 * a.steps, 48)
     cfg = CampaignConfig(master_seed=11, iterations=steps * R, round_size=R, pipeline_depth=a.depth,
                          distributed=world > 1)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    s = fuzz_loop(m, cfg)
-    torch.cuda.synchronize()
-    wall = time.perf_counter() - t0
-    t = torch.tensor([wall], dtype=torch.float64,
-                     device="cuda" if os.environ.get("SFG_DIST_BACKEND", "nccl") == "nccl" else "cpu")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    wall = float(t.item())
+    # three whole campaigns, the median reported (a ~0.4 s campaign sees sporadic
+    # host-side stalls: one run in several is up to 2x slower); all three listed
+    runs = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        s = fuzz_loop(m, cfg)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        t = torch.tensor([wall], dtype=torch.float64,
+                         device="cuda" if os.environ.get("SFG_DIST_BACKEND", "nccl") == "nccl" else "cpu")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        runs.append((float(t.item()), s))
+    wall, s = sorted(runs, key=lambda r: r[0])[1]
     tr = s.device_transfer
     return {"value": s.compute_runs / wall, "unit": UNIT, "h2d_bytes_per_step": tr["h2d_bytes"] / steps,
             "d2h_bytes_per_step": tr["d2h_bytes"] / steps, "wall_s": wall, "execs": s.compute_runs, "rounds": steps,
+            "campaigns": [r[1].compute_runs / r[0] for r in runs], "reported": "median of the 3 campaigns",
             "api": "campaign.fuzz_loop(manifest, CampaignConfig) -> CampaignSummary",
             "includes": "program build (JIT cache hit), INIT baseline, corpus upload, all rounds, result objects",
             "findings_unique": len(s.findings), "stop": s.stop_reason, "setup_s": tr.get("setup_s")}
@@ -576,11 +582,12 @@ def stage_profile(dc, it, R, a, peaks, torch):
 def run_e2e_sequential(a, m, torch):
     """fuzz_loop with discipline="sequential": the reference fuzz_loop's own stream
     discipline (one worker stream, live corpus), byte-identical output directories
-    (tests/test_gpu_parity.py), on the same workload; rounds of 2^16 generated in
-    order on the device and cut after each admission."""
+    (tests/test_gpu_parity.py), on the same workload and round size: children
+    generated in parallel from the worker stream (seqgen), rounds chained
+    speculatively on the device and cut after each admission."""
     from paper_2603_05725_b200.campaign import CampaignConfig, fuzz_loop
     iters = a.sequential_execs
-    cfg = CampaignConfig(master_seed=11, iterations=iters, round_size=1 << 16, discipline="sequential")
+    cfg = CampaignConfig(master_seed=11, iterations=iters, round_size=a.round, discipline="sequential")
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     s = fuzz_loop(m, cfg)
@@ -657,7 +664,7 @@ def main():
                    "when the reference is installed in baseline/_ref")
     p.add_argument("--no-cold", action="store_true", help="skip the cold-process end-to-end runs")
     p.add_argument("--no-sequential", action="store_true", help="skip the sequential-discipline e2e run")
-    p.add_argument("--sequential-execs", type=int, default=1 << 22)
+    p.add_argument("--sequential-execs", type=int, default=1 << 25)
     p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                    help="weak: --round inputs per GPU per round; strong: --round inputs per round over all GPUs "
                         "(the same campaign at every N)")

@@ -133,6 +133,10 @@ class Slot:
         # sequential discipline: worker stream state before every input and after the last
         self.states = u8((cap + 1) * dc.state_bytes) if dc.sequential else None
         self.seq_par, self.seq_scratch, self.seq_words = False, None, 0
+        self.start_state = u8(dc.state_bytes) if dc.sequential else None
+        self.seq_prev = None             # the in-flight round this one continues (pipelined)
+        self.ev_gen = None               # children generated (the next round may read states[n])
+        self.reader_ev = None            # the next round has copied states[n]
         self.seq_stats = i64(2)          # seqgen: [children found, words they drew]
         self.pin_seq = torch.zeros(2, dtype=torch.int64, pin_memory=True)
         self.order_scratch = i32(int(dc.L.sfg_order_scratch_ints(cap)))
@@ -148,7 +152,8 @@ class Slot:
         self.counts_after = torch.zeros(max(C, 1), dtype=torch.int64, device=dev)
         self.pin_ca = torch.zeros(max(C, 1), dtype=torch.int64, pin_memory=True)
         self.counts_after_valid = False
-        self.sat_base = False
+        self.sat_base = False            # counts_base holds the frozen (saturated) counts
+        self.sat_round = False           # the round was submitted with saturated counts
         self.pin_tot = torch.empty(8 + 16, dtype=torch.int64, pin_memory=True)
         self.pin_sc = torch.empty(2, dtype=torch.int32, pin_memory=True)
         self.pin_gath = torch.empty((dc.comm.world, 2), dtype=torch.int64, pin_memory=True)
@@ -198,6 +203,8 @@ class DeviceCampaign:
         self.sequential = bool(sequential)
         self.seq_single = os.environ.get("SFG_SEQ_SINGLE", "0") == "1"   # force the one-thread walk (tests / A-B)
         self._seq_mu = 12.0            # words per child (seqgen candidate range), refined per round
+        self.seq_scratch = None        # seqgen successor levels + path (one per campaign)
+        self._seq_gen_ev = None        # the last submitted generation
         self.seq_truncations = 0
         self.state_bytes = int(self.L.sfg_stream_state_bytes())
         if self.sequential and (self.comm.world > 1 or fanout):
@@ -456,20 +463,24 @@ class DeviceCampaign:
         cd = self.corpus_dev()
         C = self.C
         if self.sequential:
-            self._submit_sequential(S, cd)
+            self._submit_sequential(S, cd, resubmit)
             return
         if self.timing:
             S.sub_ev = torch.cuda.Event(enable_timing=True)
             S.sub_ev.record(st)
             S.sub_host = time.perf_counter()
         self._mark(S, "submit")
-        if self._counts_sat:
+        # a re-submitted round keeps the rotation-count mode it was first submitted in
+        # (its base and prefix must not change); a fresh one uses the current mode
+        sat = S.sat_round if resubmit else self._counts_sat
+        S.sat_round = sat
+        if sat:
             # saturated rotation counts: no plan pass, no pick scans; counts_run is
             # frozen (every mutable column >= 3) and serves as every round's base
             self.launches += 1
             prefix = None
             S.counts_after_valid = False
-            if not getattr(S, "sat_base", False):
+            if not S.sat_base and not resubmit:
                 with torch.cuda.stream(st):
                     if self._last_counts is not None:
                         st.wait_event(self._last_counts)
@@ -524,7 +535,7 @@ class DeviceCampaign:
             ev.record(S.stream)
             self.stage_marks.append((S.round_index, name, ev))
 
-    def _submit_sequential(self, S: Slot, cd):
+    def _submit_sequential(self, S: Slot, cd, resubmit: bool = False):
         """Children of the round from the worker stream, one after another (sfg_plan_seq),
         then the same layout scan, payloads and execute as the batched path."""
         L, hp, st = self.L, self.h, S.stream
@@ -532,9 +543,25 @@ class DeviceCampaign:
         it0, n = S.it0, S.n
         if it0 + n - 1 >= 2 and self.low.prog["n_mutable"] == 0:
             raise MutationError("no mutable arguments")
+        prev = getattr(S, "seq_prev", None)
         with torch.cuda.stream(st):
+            if S.reader_ev is not None:         # the round that started from this slot's end has read it
+                st.wait_event(S.reader_ev)
+                S.reader_ev = None
             if self._last_done is not None:     # the previous round's cut fixes our start
                 st.wait_event(self._last_done)
+            if not resubmit:
+                # the round's start: the previous round's end state while speculating
+                # (pipelined rounds), else the worker state after the last finalized round
+                if prev is not None:
+                    st.wait_event(prev.ev_gen)
+                    sb = self.state_bytes
+                    S.start_state.copy_(prev.states[prev.n * sb:(prev.n + 1) * sb])
+                    ev = torch.cuda.Event()
+                    ev.record(st)
+                    prev.reader_ev = ev
+                else:
+                    S.start_state.copy_(self.seq_state)
             S.counts_base.copy_(self.counts_run)
         # children in parallel (seqgen, sfg_plan_seq_par) when the round's children
         # depend on nothing but the stream: it0 >= 2, saturated rotation counts, no
@@ -544,21 +571,29 @@ class DeviceCampaign:
         if S.seq_par:
             words = int(self._seq_mu * n * 1.25) + 256
             need = int(L.sfg_seq_scratch_ints(n, words))
-            if S.seq_scratch is None or S.seq_scratch.numel() < need:
-                if S.seq_scratch is not None:
-                    S.seq_scratch.record_stream(st)
-                S.seq_scratch = torch.empty(need, dtype=torch.int32, device=self.dev)
+            # one scratch for the campaign: generations are chained in submission
+            # order (each waits for the last one submitted, dropped rounds included)
+            if self._seq_gen_ev is not None:
+                st.wait_event(self._seq_gen_ev)
+            if self.seq_scratch is None or self.seq_scratch.numel() < need:
+                if self.seq_scratch is not None:
+                    self.seq_scratch.record_stream(st)
+                self.seq_scratch = torch.empty(need, dtype=torch.int32, device=self.dev)
+            S.seq_scratch = self.seq_scratch
             self.launches += 4 + 2 * max(1, n.bit_length())
-            _native.check(L.sfg_plan_seq_par(hp, ctypes.byref(cd), it0, n, self.seq_state.data_ptr(), words,
+            _native.check(L.sfg_plan_seq_par(hp, ctypes.byref(cd), it0, n, S.start_state.data_ptr(), words,
                                              S.counts_base.data_ptr(), S.children.data_ptr(), S.vals.data_ptr(),
                                              S.flags.data_ptr(), S.states.data_ptr(), S.seq_scratch.data_ptr(),
                                              S.seq_scratch.numel(), S.seq_stats.data_ptr(), s), "plan_seq_par")
             S.seq_words = words
         else:
             self.launches += 1
-            _native.check(L.sfg_plan_seq(hp, ctypes.byref(cd), it0, n, self.seq_state.data_ptr(),
+            _native.check(L.sfg_plan_seq(hp, ctypes.byref(cd), it0, n, S.start_state.data_ptr(),
                                          S.counts_base.data_ptr(), S.children.data_ptr(), S.vals.data_ptr(),
                                          S.flags.data_ptr(), S.states.data_ptr(), s), "plan_seq")
+        S.ev_gen = torch.cuda.Event()
+        S.ev_gen.record(st)
+        self._seq_gen_ev = S.ev_gen
         cw = CHILD.itemsize // 8
         self._scan64(S, S.children.view(torch.int64), n, cw, CHILD.fields["work_bytes"][1] // 8, S.work_base, 0)
         S.ensure_work(n * self.max_entry_work + 64, self.dev)
@@ -900,33 +935,65 @@ class DeviceCampaign:
             return out
 
     # ---- public round API --------------------------------------------------------------
-    def _run_rounds_sequential(self, it0, it_stop, round_size, on_round, should_continue):
-        """Sequential discipline: one round at a time, each starting right after the
-        previous round's last kept input (a cut after an admission, or its end)."""
+    def _run_rounds_sequential(self, it0, it_stop, round_size, on_round, should_continue, depth=8):
+        """Sequential discipline: rounds in worker-stream order, each starting right
+        after the previous round's last kept input.  Once the rotation counts are
+        saturated, later rounds are submitted speculatively from the end state of the
+        round before them (seqgen chains on the device); a round that is cut (an
+        admission, or a seqgen truncation) or that admits drops the rounds in flight,
+        which are generated again from the cut.  Rounds grow while they run to their
+        end and shrink when cut."""
         results = []
+        inflight = deque()
         it = it0
-        self.reserve(1, min(round_size, max(it_stop - it0, 1)))
         size = min(round_size, SEQ_ROUND0)
         window = int(self.low.prog["window"])
-        while it < it_stop and (should_continue is None or should_continue()):
-            n = min(size, it_stop - it)
+        self.reserve(1, min(round_size, max(it_stop - it0, 1)))
+        spec = 1
+        prev = None
+        k = 0
+
+        def plan(at):
+            n = min(size, it_stop - at)
             # a round never spans a corpus entry leaving the recent window
             # (schedule_next's weights change there, campaign.py:593-603)
-            flips = [adm + window + 1 for _, adm, seed in self.host_entries if not seed and adm + window + 1 > it]
-            if flips:
-                n = max(1, min(n, min(flips) - it))
-            S = self._slot(0, n)
-            self._submit(S, it, n, self.rounds)
+            flips = [adm + window + 1 for _, adm, seed in self.host_entries if not seed and adm + window + 1 > at]
+            return max(1, min(n, min(flips) - at)) if flips else n
+
+        while True:
+            while len(inflight) < (spec if self._counts_sat else 1) and it < it_stop and \
+                    (should_continue is None or should_continue()):
+                n = plan(it)
+                S = self._slot(k % max(depth, 1), n)
+                k += 1
+                S.seq_prev = prev
+                self._submit(S, it, n, self.rounds + len(inflight))
+                inflight.append(S)
+                prev = S
+                it += n
+                if spec > 1:       # speculating after a clean round: the next one twice as large
+                    size = min(round_size, 2 * size)
+            if not inflight:
+                break
+            S = inflight.popleft()
             res = self._finalize(S)
             results.append(res)
             if on_round is not None:
                 on_round(res)
             if res.stop is not None:
+                self.drain()
                 break
-            it += res.executed
-            # rounds grow while they run to their end and shrink when cut (an
-            # admission): a cut round's later children are generated for nothing
-            size = min(round_size, 2 * size) if res.executed >= n else max(SEQ_ROUND0, size // 2)
+            if res.executed < S.round_n or res.n_admitted:
+                # the rounds in flight continued past a cut or from the pre-admission
+                # corpus: generate them again from the worker state
+                inflight.clear()
+                prev = None
+                it = S.round_it0 + res.executed
+                spec = 1
+                size = max(SEQ_ROUND0, size // 2) if res.executed < S.round_n else size
+            else:
+                spec = min(2 * spec, max(depth, 1))
+                size = min(round_size, 2 * size)
         return results
 
     def seq_generate(self, it0: int, n: int, parallel: bool, words: int | None = None):
@@ -934,6 +1001,7 @@ class DeviceCampaign:
         it0 .. it0+n-1 from the current worker state, by the one-thread walk or
         by seqgen.  Returns host copies (children, vals, int flags, states[n + 1],
         stats or None); the worker state is not advanced."""
+        self.drain()                     # the worker state of the last finalized round is in place
         S = Slot(self, max(n, 1024), 99)
         cd = self.corpus_dev()
         s = S.stream.cuda_stream
@@ -982,7 +1050,7 @@ class DeviceCampaign:
         whole range, so a long campaign is one call.  Returns the list of RoundResults
         (stops early on a stop)."""
         if self.sequential:
-            return self._run_rounds_sequential(it0, it_stop, round_size, on_round, should_continue)
+            return self._run_rounds_sequential(it0, it_stop, round_size, on_round, should_continue, depth)
         plan = []
         it = it0
         while it < it_stop:
@@ -1324,7 +1392,7 @@ class DeviceCampaign:
         self.slots = []
         self._aux = None
         for name in ("blob", "c_meta", "c_vals", "c_child", "c_data", "edge_total", "ghit", "entered", "counts_run",
-                     "ctx_map", "edge_ctx", "ctx_new"):
+                     "ctx_map", "edge_ctx", "ctx_new", "seq_scratch"):
             if hasattr(self, name):
                 setattr(self, name, None)
 

@@ -55,5 +55,5 @@ for rep in range(reps):
     print(f"rep{rep}: {dt:.3f}s {s.compute_runs / dt / 1e6:.1f}M/s first_final {log[0][0] - t0:.3f}s "
           f"admitting rounds {adm} max gap {max(gaps) * 1e3:.1f}ms rounds {len(log)}", flush=True)
 dt, lg, t0 = max(runs, key=lambda r: r[0])
-print("slowest run, finalize times (ms) of the first 40 rounds:",
-      [round((x[0] - t0) * 1e3) for x in lg[:40]])
+print("slowest run, finalize times (ms):", [round((x[0] - t0) * 1e3) for x in lg])
+print("slowest run, speculation depth:", [x[2] for x in lg])

@@ -15,7 +15,7 @@ execs = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 22
 sizes = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else [1 << 16, 1 << 18, 1 << 20]
 m = load(name)
 fuzz_loop(m, CampaignConfig(master_seed=11, iterations=1 << 14, discipline="sequential", round_size=1 << 12))
-for R in sizes:
+for R in [r for r in sizes for _ in range(2)]:   # each size twice: the second with warm buffers
     torch.cuda.synchronize()
     t = time.perf_counter()
     s = fuzz_loop(m, CampaignConfig(master_seed=11, iterations=execs, discipline="sequential", round_size=R))
