@@ -532,6 +532,10 @@ def _stage_bytes(dc):
         "sfg_order (3 kernels)": (8 + dc.n_args * VAL.itemsize, "descriptors read, bucket + position written"),
         "K3 bulk sfg_jit_execute": (payload + scalars + 64 + 4 * ((E + 31) // 32),
                                     "child payload read once + 64-B verdict + hit bitmap (SURVEY.md §8(d))"),
+        "K2+K3 bulk sfg_jit_execute (payload build fused)": (
+            payload + scalars + 64 + 4 * ((E + 31) // 32),
+            "parent payload read once (the child's is built in the pass) + 64-B verdict + hit bitmap "
+            "(SURVEY.md §8(d))"),
         "K3 tail sfg_apply + sfg_jit_tail": (payload + scalars + 64 + 4 * ((E + 31) // 32),
                                              "as the bulk pass, for the deferred inputs; per round input"),
         "K4 triage (stop/absorb/admit + scans)": (VERDICT.itemsize + 4 * E + 24,
@@ -542,8 +546,10 @@ def _stage_bytes(dc):
 def stage_profile(dc, it, R, a, peaks, torch):
     """Each stage's device time per round with nothing overlapping: ``a.profile_rounds``
     rounds run one at a time (depth 1) after the timed region."""
-    pairs = [("submit", "mutated", "K1 sfg_plan + sfg_mutate (+ scans)"), ("mutated", "applied", "K2 sfg_apply"),
-             ("applied", "ordered", "sfg_order (3 kernels)"), ("ordered", "bulk", "K3 bulk sfg_jit_execute"),
+    bulk = "K2+K3 bulk sfg_jit_execute (payload build fused)" if dc.fuse_apply else "K3 bulk sfg_jit_execute"
+    pairs = [("submit", "mutated", "K1 sfg_plan + sfg_mutate (+ scans)")] + \
+        ([] if dc.fuse_apply else [("mutated", "applied", "K2 sfg_apply")]) + \
+        [("applied", "ordered", "sfg_order (3 kernels)"), ("ordered", "bulk", bulk),
              ("bulk", "tail", "K3 tail sfg_apply + sfg_jit_tail"),
              ("triage_start", "triaged", "K4 triage (stop/absorb/admit + scans)")]
     dc.stage_marks = []

@@ -137,8 +137,12 @@ int sfg_regen(const sfg_program* p, const sfg_corpus_dev* c, int n_sel, const in
  * re-materializes the listed inputs' payloads and runs them from scratch with
  * the real budget (soft-cap list group-parallel, spread one input per warp;
  * then the sequential list).  Results are identical to soft_cap 0 and to
- * sequential execution (executor.py:405-424). */
-int sfg_execute(const sfg_program* p, int n, const void* children, const void* vals,
+ * sequential execution (executor.py:405-424).
+ * c != NULL (the campaign's corpus as of the round start): the kernel builds every
+ * input's arrays in its work region itself, from its parent's payload, before its
+ * COMPUTE phase (sfg_apply fused into the execute pass); c == NULL: the work
+ * regions were built by sfg_apply (or by the host, execute_testcases). */
+int sfg_execute(const sfg_program* p, const sfg_corpus_dev* c, int n, const void* children, const void* vals,
                 const uint64_t* work_base, uint8_t* work, void* verdicts, uint32_t* edge_counts,
                 uint8_t* readouts, const uint64_t* readout_base, int* work_counter,
                 uint64_t soft_cap, int32_t* deferred, int64_t max_work_bytes, const int32_t* order,

@@ -565,8 +565,8 @@ int sfg_order(const sfg_program* p, int n, const void* vals, int32_t* order, int
 }
 
 
-int sfg_execute(const sfg_program* p, int n, const void* children, const void* vals, const uint64_t* work_base,
-                uint8_t* work, void* verdicts, uint32_t* edge_counts, uint8_t* readouts,
+int sfg_execute(const sfg_program* p, const sfg_corpus_dev* c, int n, const void* children, const void* vals,
+                const uint64_t* work_base, uint8_t* work, void* verdicts, uint32_t* edge_counts, uint8_t* readouts,
                 const uint64_t* readout_base, int* work_counter, uint64_t soft_cap,
                 int32_t* deferred, int64_t max_work_bytes, const int32_t* order, void* stream) {
   if (n <= 0) {
@@ -578,7 +578,7 @@ int sfg_execute(const sfg_program* p, int n, const void* children, const void* v
              (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, n,
              0ull, deferred, work_counter ? work_counter + 1 : nullptr,
              deferred ? deferred + n : nullptr, work_counter ? work_counter + 3 : nullptr, 1, 0, order,
-             nullptr, 0, nullptr};
+             nullptr, 0, nullptr, c ? (const sfg_val*)c->vals : nullptr, c ? (const uint8_t*)c->data : nullptr};
   if (p->jit_kernel) {
     if (work_counter == nullptr || (deferred == nullptr && soft_cap != 0)) {
       g_err = "sfg_execute: the specialized kernel needs a per-launch work counter (and deferred lists for soft_cap)";
@@ -634,7 +634,7 @@ int sfg_execute_trace(const sfg_program* p, int n, const void* children, const v
   ExecView E{p->ins, p->hostops, p->binds, p->recs, p->base_blob, p->const_blob,
              (const sfg_child*)children, (const sfg_val*)vals, work_base, work,
              (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, n,
-             0ull, nullptr, nullptr, nullptr, nullptr, 1, 0, nullptr, trace, trace_cap, trace_count};
+             0ull, nullptr, nullptr, nullptr, nullptr, 1, 0, nullptr, trace, trace_cap, trace_count, nullptr, nullptr};
   if (!p->gen_ok) {
     g_err = "the program's registers / edges exceed the generic interpreter's shared memory";
     return 1;
@@ -653,7 +653,7 @@ int sfg_execute_deferred(const sfg_program* p, const sfg_corpus_dev* c, int n, c
              (const sfg_child*)children, (const sfg_val*)vals, work_base, work,
              (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, n,
              0ull, deferred, work_counter + 1, deferred + n, work_counter + 3, p->group, 0, nullptr,
-             nullptr, 0, nullptr};
+             nullptr, 0, nullptr, nullptr, nullptr};
   for (int pass = 0; pass < 2; ++pass) {
     // pristine payloads again (the earlier attempt's stores landed in the work regions)
     int32_t* list = pass == 0 ? deferred : deferred + n;

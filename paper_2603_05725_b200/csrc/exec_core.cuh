@@ -123,6 +123,11 @@ struct ExecView {
   uint64_t* trace;
   uint32_t trace_cap;
   uint32_t* trace_count;
+  // in-kernel materialization (the bulk pass, sfg_execute with a corpus): each input's
+  // arrays are built from its parent's payload right before its COMPUTE phase, by the
+  // rule of sfg_apply (campaign.py:440-450); null: the work regions are already built
+  const sfg_val* mat_vals;
+  const uint8_t* mat_data;
 };
 
 namespace {
@@ -716,6 +721,22 @@ SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R, c
   int defer_kind = 0;  // 1: soft cap reached (deferred), 2: re-run thread-sequentially (deferred_seq)
   int seq_reruns = 0;  // group-parallel chunks undone and re-run sequentially (diagnostics)
   if (GRP && ntags > g.tag_cap) defer_kind = 2;
+  if (E.mat_data != nullptr && defer_kind == 0) {
+    const sfg_val* pv = E.mat_vals + (size_t)(ch.parent < 0 ? 0 : ch.parent) * P.n_args;
+    const int gl = GRP ? g.gl : 0, gn = GRP ? g.G : 1;
+    for (int a = 0; a < P.n_args; ++a) {
+      if (cv[a].kind != SFG_V_ARR) continue;
+      const sfg_op* op = nullptr;
+      for (int k = 0; k < ch.n_ops; ++k)
+        if (ch.ops[k].arg == a) op = &ch.ops[k];
+      emit_child(wk + cv[a].data_off, sfg_mat_size(cv[a]), E.mat_data + pv[a].data_off, pv[a].nbytes, cv[a], op, gl,
+                 gn);
+      if ((P.copy_src_mask >> a) & 1u)   // the test case's own bytes for copy_in (campaign.py:404-409)
+        emit_child(wk + sfg_pristine_off(&P, cv, ch.work_bytes, a, nullptr), cv[a].nbytes,
+                   E.mat_data + pv[a].data_off, pv[a].nbytes, cv[a], op, gl, gn);
+    }
+    if constexpr (GRP) __syncwarp(g.mask);
+  }
 
   bool stop = defer_kind != 0;
   for (int h = 0; h < P.n_hostops && !stop; ++h) {

@@ -213,26 +213,6 @@ __device__ void gen_array_op(Strm& s, const sfg_prog& P, const sfg_val& v, sfg_o
   op.inner = in.kind; op.isub = in.sub; op.ibyte = in.byte; op.imask = in.mask; op.delta = in.delta;
 }
 
-__device__ uint32_t int_bits_op(uint32_t v, uint8_t kind, uint8_t sub, uint8_t byte, uint32_t mask,
-                                int64_t delta) {
-  if (kind == SFG_M_INT_BOUNDARY) return sub == 0 ? 0u : (sub == 1 ? 0x7FFFFFFFu : 0x80000000u);
-  if (sub == 0) return v ^ ((mask & 0xFFu) << (8 * byte));      // flip
-  return (uint32_t)((int64_t)(int32_t)v + delta);                // add, wraps mod 2^32
-}
-
-__device__ uint32_t float_bits_op(uint32_t b, uint8_t kind, uint8_t sub, uint8_t byte, uint32_t mask) {
-  switch (kind) {                                                // mutation.py:281-306
-    case SFG_M_FLOAT_SIGN: return b ^ 0x80000000u;
-    case SFG_M_FLOAT_EXPONENT:
-      if (sub == 0) return b | 0x7F800000u;
-      if (sub == 1) return b & 0x807FFFFFu;
-      return b ^ (1u << (23 + byte));
-    case SFG_M_FLOAT_MANTISSA: return b ^ (mask & 0x007FFFFFu);
-    case SFG_M_FLOAT_BYTE: return b ^ ((mask & 0xFFu) << (8 * byte));
-    default: return sfg_fop(SFG_FADD, b, mask);                  // float_arith
-  }
-}
-
 // descriptor-level apply_op (mutation.py:258-357); payload bytes are done by emit_child
 __device__ void apply_desc(const sfg_prog& P, sfg_val& v, const sfg_op& op) {
   switch (op.kind) {
@@ -256,59 +236,6 @@ __device__ void apply_desc(const sfg_prog& P, sfg_val& v, const sfg_op& op) {
       break;
     }
     default: break;  // ARRAY_ELEM: payload only
-  }
-}
-
-// byte p of the child's payload (p < child nbytes), given the parent's payload
-__device__ __forceinline__ uint8_t child_byte(const uint8_t* src, uint32_t src_n, const sfg_op* op,
-                                              uint8_t elem, uint64_t p) {
-  if (op != nullptr) {
-    if (op->kind == SFG_M_ARRAY_EXTREME) {
-      const uint32_t pat = elem == 1 ? (op->sub == 0 ? 0u : op->sub == 1 ? 0x7F7FFFFFu : 0xFF7FFFFFu)
-                                     : (op->sub == 0 ? 0u : op->sub == 1 ? 0x7FFFFFFFu : 0x80000000u);
-      return (uint8_t)(pat >> (8 * (p & 3)));
-    }
-    if (op->kind == SFG_M_ARRAY_ELEM && (p >> 2) == op->index) {
-      const uint64_t w0 = p & ~3ull;
-      uint32_t w = 0;
-      for (int k = 0; k < 4; ++k) w |= (uint32_t)(w0 + k < src_n ? src[w0 + k] : 0) << (8 * k);
-      if (elem == 1) w = float_bits_op(w, op->inner, op->isub, op->ibyte, op->imask);
-      else w = int_bits_op(w, op->inner, op->isub, op->ibyte, op->imask, op->delta);
-      return (uint8_t)(w >> (8 * (p & 3)));
-    }
-  }
-  return p < src_n ? src[p] : 0;
-}
-
-// Write bytes [0, limit) of a child array: payload bytes where p < child nbytes,
-// zeros beyond.  Lanes of a warp stride over 16-byte chunks; dst is 16-aligned.
-__device__ void emit_child(uint8_t* dst, uint64_t limit, const uint8_t* src, uint32_t src_n,
-                           const sfg_val& child, const sfg_op* op, int lane, int lanes) {
-  const bool extreme = op != nullptr && op->kind == SFG_M_ARRAY_EXTREME;
-  const uint64_t elem_chunk =
-      (op != nullptr && op->kind == SFG_M_ARRAY_ELEM) ? ((uint64_t)op->index * 4) >> 4 : ~0ull;
-  const uint64_t payload = child.nbytes;
-  const uint64_t copy_lim = payload < src_n ? payload : src_n;
-  const bool src_al = (((uintptr_t)src) & 15) == 0;
-  const uint64_t nchunks = (limit + 15) >> 4;
-  for (uint64_t c = lane; c < nchunks; c += lanes) {
-    const uint64_t p0 = c << 4;
-    if (!extreme && c != elem_chunk && src_al && p0 + 16 <= copy_lim && p0 + 16 <= limit) {
-      *reinterpret_cast<uint4*>(dst + p0) = __ldg(reinterpret_cast<const uint4*>(src + p0));
-      continue;
-    }
-    if (extreme && p0 + 16 <= payload && p0 + 16 <= limit) {
-      const uint32_t pat = child.elem == 1 ? (op->sub == 0 ? 0u : op->sub == 1 ? 0x7F7FFFFFu : 0xFF7FFFFFu)
-                                           : (op->sub == 0 ? 0u : op->sub == 1 ? 0x7FFFFFFFu : 0x80000000u);
-      *reinterpret_cast<uint4*>(dst + p0) = make_uint4(pat, pat, pat, pat);
-      continue;
-    }
-    if (p0 >= payload && p0 + 16 <= limit) {
-      *reinterpret_cast<uint4*>(dst + p0) = make_uint4(0, 0, 0, 0);
-      continue;
-    }
-    const uint64_t pe = p0 + 16 < limit ? p0 + 16 : limit;
-    for (uint64_t p = p0; p < pe; ++p) dst[p] = p < payload ? child_byte(src, src_n, op, child.elem, p) : 0;
   }
 }
 

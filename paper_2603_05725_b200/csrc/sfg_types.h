@@ -18,7 +18,7 @@ typedef unsigned long uintptr_t;
 #include <stdint.h>
 #endif
 
-#define SFG_ABI_VERSION 4
+#define SFG_ABI_VERSION 5
 
 #define SFG_MAX_ARGS 16      // argspecs per harness
 #define SFG_MAX_OPS 3        // MutationConfig.max_ops ceiling (reference default 3)

@@ -135,6 +135,7 @@ class Slot:
         self.seq_par, self.seq_scratch, self.seq_words = False, None, 0
         self.start_state = u8(dc.state_bytes) if dc.sequential else None
         self.seq_prev = None             # the in-flight round this one continues (pipelined)
+        self.fused = False               # the execute pass builds the work regions itself
         self.ev_gen = None               # children generated (the next round may read states[n])
         self.reader_ev = None            # the next round has copied states[n]
         self.seq_stats = i64(2)          # seqgen: [children found, words they drew]
@@ -206,6 +207,9 @@ class DeviceCampaign:
         self.seq_scratch = None        # seqgen successor levels + path (one per campaign)
         self._seq_gen_ev = None        # the last submitted generation
         self.seq_truncations = 0
+        # K2 fused into the bulk pass (sfg_execute with the corpus); SFG_FUSE_APPLY=0:
+        # a separate sfg_apply pass (A/B, tests)
+        self.fuse_apply = os.environ.get("SFG_FUSE_APPLY", "1") != "0"
         self.state_bytes = int(self.L.sfg_stream_state_bytes())
         if self.sequential and (self.comm.world > 1 or fanout):
             raise LoweringError("the sequential discipline runs on one device without fan-out")
@@ -524,8 +528,10 @@ class DeviceCampaign:
                 S.readouts.record_stream(st)
             S.readouts = None
         self._mark(S, "mutated")
-        _native.check(L.sfg_apply(hp, ctypes.byref(cd), n, S.children.data_ptr(), S.vals.data_ptr(),
-                                  S.work_base.data_ptr(), S.work.data_ptr(), s), "apply")
+        S.fused = self.fuse_apply
+        if not S.fused:
+            _native.check(L.sfg_apply(hp, ctypes.byref(cd), n, S.children.data_ptr(), S.vals.data_ptr(),
+                                      S.work_base.data_ptr(), S.work.data_ptr(), s), "apply")
         self._mark(S, "applied")
         self._execute(S, n, self.soft_cap, cd)
 
@@ -606,8 +612,10 @@ class DeviceCampaign:
             if S.readouts is not None:
                 S.readouts.record_stream(st)
             S.readouts = None
-        _native.check(L.sfg_apply(hp, ctypes.byref(cd), n, S.children.data_ptr(), S.vals.data_ptr(),
-                                  S.work_base.data_ptr(), S.work.data_ptr(), s), "apply")
+        S.fused = self.fuse_apply
+        if not S.fused:
+            _native.check(L.sfg_apply(hp, ctypes.byref(cd), n, S.children.data_ptr(), S.vals.data_ptr(),
+                                      S.work_base.data_ptr(), S.work.data_ptr(), s), "apply")
         self._execute(S, n, self.soft_cap, cd)
 
     def _execute(self, S: Slot, n: int, soft_cap: int = 0, cd=None):
@@ -629,8 +637,11 @@ class DeviceCampaign:
                                            S.order_scratch.data_ptr(), st.cuda_stream), "order")
             order = S.order.data_ptr()
             self._mark(S, "ordered")
+        # the bulk pass builds each input's arrays from its parent itself (sfg_apply
+        # fused) when the round has a corpus and nothing was materialized before
+        fuse = cd if (cd is not None and S.fused) else None
         _native.check(self.L.sfg_execute(
-            self.h, n, S.children.data_ptr(), S.vals.data_ptr(), S.work_base.data_ptr(), S.work.data_ptr(),
+            self.h, ctypes.byref(fuse) if fuse is not None else None, n, S.children.data_ptr(), S.vals.data_ptr(), S.work_base.data_ptr(), S.work.data_ptr(),
             S.verdicts.data_ptr(), S.ecnt.data_ptr(), _ptr(S.readouts), S.ro_base.data_ptr(),
             S.counter.data_ptr(), soft, S.deferred.data_ptr() if tail else None, self.max_entry_work, order,
             st.cuda_stream), "execute")

@@ -52,7 +52,7 @@ def test_library_exports_and_layouts():
     assert declared == set(_native.EXPORTS), declared ^ set(_native.EXPORTS)
     for sym in declared:
         assert hasattr(lib, sym), sym
-    assert lib.sfg_abi_version() == 4
+    assert lib.sfg_abi_version() == 5
     sizes = [lib.sfg_layout_probe(i) for i in range(14)]
     want = [lw.INS.itemsize, lw.KERNEL.itemsize, lw.HOSTOP.itemsize, lw.BINDING.itemsize, lw.REC.itemsize,
             lw.VAL.itemsize, lw.OP.itemsize, lw.CHILD.itemsize, lw.ENTRY.itemsize, lw.VERDICT.itemsize,
