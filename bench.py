@@ -471,9 +471,10 @@ def run_e2e(a, m, torch, R, world):
     dedupe-key counts and new findings / admissions down."""
     from paper_2603_05725_b200.campaign import CampaignConfig, fuzz_loop
     import torch.distributed as dist
-    # a campaign long enough that pipeline fill/drain (one slowest-round latency,
-    # ~0.15 s on C2) does not dominate: twice the timed steps, at least 48 rounds
-    steps = max(2 * a.steps, 48)
+    # a campaign long enough that pipeline fill/drain (the first rounds run at a low
+    # speculation depth, one slowest-round latency at either end, ~0.2 s on C2) does
+    # not dominate: four times the timed steps, at least 96 rounds
+    steps = max(4 * a.steps, 96)
     cfg = CampaignConfig(master_seed=11, iterations=steps * R, round_size=R, pipeline_depth=a.depth,
                          distributed=world > 1)
     # three whole campaigns, the median reported (a ~0.4 s campaign sees sporadic

@@ -119,6 +119,9 @@ class Slot:
         # the long-input pass runs on a high-priority stream: its CTAs are dispatched
         # ahead of other rounds' bulk CTAs whenever SM slots free up
         self.tail_stream = torch.cuda.Stream(device=dev, priority=-1) if dc.tail_priority else self.stream
+        # triage / commit of a finalized round: high priority, so the host's wait for the
+        # round's verdict scalars does not queue behind later rounds' bulk CTAs
+        self.fin = torch.cuda.Stream(device=dev, priority=-1)
         self.parent, self.picks, self.flags, self.prefix = i32(cap), u8(cap * 3), i32(cap * C), i64(cap * C)
         self.children, self.vals = u8(cap * CHILD.itemsize), u8(cap * A * VAL.itemsize)
         self.work_base, self.ro_base = i64(cap), i64(cap)
@@ -426,10 +429,11 @@ class DeviceCampaign:
             self.slots[k] = s
         return s
 
-    def _scan64(self, S: Slot, src, n, stride, col, out, total_slot):
+    def _scan64(self, S: Slot, src, n, stride, col, out, total_slot, stream=None):
         self.launches += 3
         _native.check(self.L.sfg_scan_u64(src.data_ptr(), n, stride, col, out.data_ptr(), 1, 0, S.tmp.data_ptr(),
-                                          S.tot.data_ptr() + 8 * total_slot, S.stream.cuda_stream), "scan")
+                                          S.tot.data_ptr() + 8 * total_slot, (stream or S.stream).cuda_stream),
+                      "scan")
 
     def _set_worker_stream(self, w: int):
         """Worker w's stream Stream(master_seed, 1000 + w) (campaign.py:714)."""
@@ -535,10 +539,10 @@ class DeviceCampaign:
         self._mark(S, "applied")
         self._execute(S, n, self.soft_cap, cd)
 
-    def _mark(self, S: Slot, name: str):
+    def _mark(self, S: Slot, name: str, stream=None):
         if self.stage_marks is not None:
             ev = torch.cuda.Event(enable_timing=True)
-            ev.record(S.stream)
+            ev.record(stream or S.stream)
             self.stage_marks.append((S.round_index, name, ev))
 
     def _submit_sequential(self, S: Slot, cd, resubmit: bool = False):
@@ -674,11 +678,12 @@ class DeviceCampaign:
         """stop -> [MIN] -> absorb -> [MIN, SUM] -> admit -> scans -> [gather], read
         back to the host.  cut: round index after which inputs are discarded (the
         sequential discipline's cut after an admission), applied as a stop."""
-        L, hp, st, comm = self.L, self.h, S.stream, self.comm
+        L, hp, st, comm = self.L, self.h, S.fin, self.comm
         s = st.cuda_stream
+        st.wait_stream(S.stream)      # the round's execute (and tail) passes
         n, ib = S.n, S.i_base
         self.launches += 7
-        self._mark(S, "triage_start")
+        self._mark(S, "triage_start", st)
         with torch.cuda.stream(st):
             S.mins.fill_(NONE)
             S.sums.zero_()
@@ -696,9 +701,9 @@ class DeviceCampaign:
         _native.check(L.sfg_triage_admit(hp, n, ib, vp, ep, S.children.data_ptr(), S.scalars.data_ptr(),
                                          S.first.data_ptr(), self.ghit.data_ptr(), S.admit.data_ptr(), s),
                       "triage_admit")
-        self._scan64(S, S.admit, n, 1, 0, S.pos, 2)
-        self._scan64(S, S.allocs, n, 1, 0, S.allocs_prefix, 3)
-        self._mark(S, "triaged")
+        self._scan64(S, S.admit, n, 1, 0, S.pos, 2, st)
+        self._scan64(S, S.allocs, n, 1, 0, S.allocs_prefix, 3, st)
+        self._mark(S, "triaged", st)
         with torch.cuda.stream(st):
             S.small.copy_(S.tot[2:4])
             gath = comm.all_gather(S.small, st)
@@ -726,7 +731,7 @@ class DeviceCampaign:
         findings.  Sequential discipline: a round whose first admission is not its
         last executed input is triaged again, cut right after that admission (the
         later inputs were generated from the pre-admission corpus)."""
-        L, hp, st, comm = self.L, self.h, S.stream, self.comm
+        L, hp, st, comm = self.L, self.h, S.fin, self.comm
         s = st.cuda_stream
         ib = S.i_base
         with torch.cuda.stream(st):
@@ -737,6 +742,7 @@ class DeviceCampaign:
         # the round again (deterministic, so the results are those of a large overlay)
         while fatal != NONE and fatal <= stop and self._fatal_status(S, fatal)[0] == ST_OVERLAY:
             self._grow_overlay()
+            S.stream.wait_stream(S.fin)
             self._submit(S, S.round_it0, S.round_n, S.round_index, resubmit=True)
             stop, fatal, gathered = self._triage_pass(S)
         N = S.round_n
@@ -794,6 +800,7 @@ class DeviceCampaign:
                 self._counts_sat = all(int(ca[c]) >= 3 for c in self._sat_cols)
         S.ev_done.record(st)
         self._last_done = S.ev_done
+        S.stream.wait_stream(st)      # the slot's next round starts after its finalize work
         self.rounds += 1
         return RoundResult(S.round_it0, N, None if stop == NONE else stop, executed, n_adm, new_keys, S)
 
@@ -835,7 +842,7 @@ class DeviceCampaign:
         """Append the round's admitted children (all ranks, in id order) to the
         corpus: each rank stages its own rows, the rows are all-gathered, and
         every rank regenerates the payloads from (parent, ops) on its device."""
-        L, hp, st, comm = self.L, self.h, S.stream, self.comm
+        L, hp, st, comm = self.L, self.h, S.fin, self.comm
         s = st.cuda_stream
         A = self.n_args
         CB, VB = CHILD.itemsize, A * VAL.itemsize
@@ -847,7 +854,7 @@ class DeviceCampaign:
             return self._admit_on_stream(S, per_rank, A, CB, VB, mine, T, mx)
 
     def _admit_on_stream(self, S, per_rank, A, CB, VB, mine, T, mx):
-        L, hp, st, comm = self.L, self.h, S.stream, self.comm
+        L, hp, st, comm = self.L, self.h, S.fin, self.comm
         s = st.cuda_stream
         stage = self._u8(max(mx, 1) * (CB + VB))
         _native.check(L.sfg_select(hp, S.children.data_ptr(), S.vals.data_ptr(), S.admit.data_ptr(),
@@ -866,7 +873,7 @@ class DeviceCampaign:
         boff = torch.empty(max(T, 1), dtype=torch.int64, device=self.dev)
         self.launches += 1
         _native.check(L.sfg_child_bytes(hp, gva.data_ptr(), None, T, nb.data_ptr(), s), "child_bytes")
-        self._scan64(S, nb.view(torch.int64), T, 1, 0, boff, 4)
+        self._scan64(S, nb.view(torch.int64), T, 1, 0, boff, 4, st)
         with torch.cuda.stream(st):
             nbytes = int(S.tot[4].item())
         self._grow_corpus(max(self.cap, (self.n_corpus + T) * 2),
@@ -911,7 +918,7 @@ class DeviceCampaign:
         """FindingsLog updates of a round: hit counts of known keys; new keys are
         decoded by the rank owning their first input and shared with all ranks."""
         comm = self.comm
-        with torch.cuda.stream(S.stream):
+        with torch.cuda.stream(S.fin):
             kc = S.pin_kc.numpy()[:self.K]   # copied with the round's scalars (_finalize)
             hot = np.nonzero(kc)[0]
             if not len(hot):
