@@ -296,8 +296,10 @@ def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:
         summary.context_map_slots = dc.ctx_map_slots()
     if dc.round_log is not None:
         dc.round_log.append(("summary", -1, time.perf_counter()))
-        summary.device_transfer["round_log"] = list(dc.round_log)
+        summary.device_transfer["round_log"] = dc.round_log
     dc.close()
+    if dc.round_log is not None:
+        dc.round_log.append(("closed", -1, time.perf_counter()))
     return summary
 
 

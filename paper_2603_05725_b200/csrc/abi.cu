@@ -32,6 +32,7 @@ struct sfg_program {
   sfg_binding* binds;
   sfg_rec* recs;
   uint8_t* const_blob;
+  size_t tab_bytes[5] = {0, 0, 0, 0, 0};   // bytes of the five tables above (table_free)
   const uint8_t* base_blob;  // caller-owned device buffer
   size_t smem;
   int gen_warps = 4;                  // warps per block of the generic interpreter
@@ -157,11 +158,41 @@ static inline CorpusView CV(const sfg_corpus_dev* c) {
   return CorpusView{(const sfg_entry*)c->meta, (const sfg_val*)c->vals, (const uint8_t*)c->data, c->n, c->n_seeds};
 }
 
+// Program tables (a few KB each) come from a process-wide free list rather than
+// cudaMalloc / cudaFree per program: cudaFree synchronizes the device and, next to a
+// caching allocator holding tens of GB, took 0.1-0.4 s at random when a campaign's
+// program was destroyed (measured around fuzz_loop calls).
+static std::mutex g_tab_mu;
+static std::multimap<std::pair<int, size_t>, void*> g_tab_free;   // (device, bytes) -> block
+
+static cudaError_t table_alloc(void** dst, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(g_tab_mu);
+    auto it = g_tab_free.find({dev, bytes});
+    if (it != g_tab_free.end()) {
+      *dst = it->second;
+      g_tab_free.erase(it);
+      return cudaSuccess;
+    }
+  }
+  return cudaMalloc(dst, bytes);
+}
+
+static void table_free(void* ptr, size_t bytes) {
+  if (!ptr) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  g_tab_free.insert({{dev, bytes}, ptr});
+}
+
 template <typename T>
 static cudaError_t dupe(T** dst, const void* src, size_t count) {
   *dst = nullptr;
   if (count == 0) return cudaSuccess;
-  cudaError_t e = cudaMalloc((void**)dst, count * sizeof(T));
+  cudaError_t e = table_alloc((void**)dst, count * sizeof(T));
   if (e != cudaSuccess) return e;
   return cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice);
 }
@@ -228,6 +259,12 @@ int sfg_program_create(const void* prog, size_t prog_bytes, const void* ins, siz
   sfg_program* p = new sfg_program();
   memcpy(&p->P, prog, sizeof(sfg_prog));
   cudaError_t e;
+  p->ins = nullptr; p->hostops = nullptr; p->binds = nullptr; p->recs = nullptr; p->const_blob = nullptr;
+  p->tab_bytes[0] = n_ins * sizeof(sfg_ins);
+  p->tab_bytes[1] = n_hostops * sizeof(sfg_hostop);
+  p->tab_bytes[2] = n_binds * sizeof(sfg_binding);
+  p->tab_bytes[3] = n_recs * sizeof(sfg_rec);
+  p->tab_bytes[4] = const_bytes;
   if ((e = dupe(&p->ins, ins, n_ins)) != cudaSuccess ||
       (e = dupe(&p->hostops, hostops, n_hostops)) != cudaSuccess ||
       (e = dupe(&p->binds, binds, n_binds)) != cudaSuccess ||
@@ -376,12 +413,13 @@ int sfg_program_update(sfg_program* p, const void* prog, size_t prog_bytes) {
 
 void sfg_program_destroy(sfg_program* p) {
   if (!p) return;
-  if (p->jit_lib) cudaLibraryUnload(p->jit_lib);
-  cudaFree(p->ins);
-  cudaFree(p->hostops);
-  cudaFree(p->binds);
-  cudaFree(p->recs);
-  cudaFree(p->const_blob);
+  // p->jit_lib stays loaded: it is shared by every program with the same generated
+  // source in this process (jit.cu sfg_jit_build)
+  table_free(p->ins, p->tab_bytes[0]);
+  table_free(p->hostops, p->tab_bytes[1]);
+  table_free(p->binds, p->tab_bytes[2]);
+  table_free(p->recs, p->tab_bytes[3]);
+  table_free(p->const_blob, p->tab_bytes[4]);
   delete p;
 }
 

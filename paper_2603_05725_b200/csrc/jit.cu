@@ -1206,6 +1206,25 @@ static int sfg_jit_build(const sfg_prog& P, const sfg_ins* ins, uint64_t max_edg
   std::vector<char> cubin;
   const int rc = sfg_jit_compile(P, ins, max_edge_events, dead_kernels, caps, source, log, cubin);
   if (rc) return rc;
+  // Loaded libraries stay loaded for the process, one per distinct program on each
+  // device: unloading a module whose kernels use a large local-memory frame makes the
+  // driver shrink and later regrow the context's local-memory pool, which stalled the
+  // next campaign's first launches for 0.1-0.4 s (measured around fuzz_loop calls).
+  struct Loaded { cudaLibrary_t lib; cudaKernel_t kern, tail; };
+  static std::mutex lmu;
+  static std::map<std::pair<int, std::string>, Loaded> loaded;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(lmu);
+    auto it = loaded.find({dev, source});
+    if (it != loaded.end()) {
+      *lib_out = it->second.lib;
+      *kern_out = it->second.kern;
+      *tail_out = it->second.tail;
+      return 0;
+    }
+  }
   cudaError_t e = cudaLibraryLoadData(lib_out, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
   if (e != cudaSuccess) {
     log += std::string("\ncudaLibraryLoadData: ") + cudaGetErrorString(e);
@@ -1217,5 +1236,7 @@ static int sfg_jit_build(const sfg_prog& P, const sfg_ins* ins, uint64_t max_edg
     log += std::string("\ncudaLibraryGetKernel: ") + cudaGetErrorString(e);
     return 4;
   }
+  std::lock_guard<std::mutex> lk(lmu);
+  loaded[{dev, source}] = Loaded{*lib_out, *kern_out, *tail_out};
   return 0;
 }

@@ -1400,15 +1400,22 @@ class DeviceCampaign:
         """Release the program and every device buffer now (not at garbage
         collection): a following campaign then reuses the memory instead of
         allocating -- cudaMalloc mid-run costs tenths of a second."""
+        rl = getattr(self, "round_log", None)
         if getattr(self, "h", None):
             try:
                 self.drain()
             except Exception:
                 pass
+            if rl is not None:
+                rl.append(("close_drained", -1, time.perf_counter()))
             self.L.sfg_program_destroy(self.h)
             self.h = None
+            if rl is not None:
+                rl.append(("close_destroyed", -1, time.perf_counter()))
         self.slots = []
         self._aux = None
+        if rl is not None:
+            rl.append(("close_slots", -1, time.perf_counter()))
         for name in ("blob", "c_meta", "c_vals", "c_child", "c_data", "edge_total", "ghit", "entered", "counts_run",
                      "ctx_map", "edge_ctx", "ctx_new", "seq_scratch"):
             if hasattr(self, name):

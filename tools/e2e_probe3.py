@@ -50,9 +50,16 @@ for rep in range(reps):
     gaps = [b[0] - a[0] for a, b in zip(log, log[1:])]
     adm = [k for k, x in enumerate(log) if x[1]]
     runs.append((dt, list(log), t0))
+    rl = s.device_transfer.get("round_log")
+    if rl:
+        marks = {n: t for n, k, t in rl if k == -1}
+        tail = {n: round((t - t0) * 1e3) for n, t in marks.items()}
+        print("   phases (ms from call):", tail, "last finalize", round((log[-1][0] - t0) * 1e3),
+              "end", round(dt * 1e3))
     a1 = torch.cuda.memory_stats().get("num_device_alloc", 0)
     print(f"cudaMallocs {a1 - a0} reserved {torch.cuda.memory_reserved() / 1e9:.1f} GB", end=" ")
-    print(f"rep{rep}: {dt:.3f}s {s.compute_runs / dt / 1e6:.1f}M/s first_final {log[0][0] - t0:.3f}s "
+    print(f"rep{rep}: {dt:.3f}s {s.compute_runs / dt / 1e6:.1f}M/s setup {s.device_transfer.get('setup_s', 0):.3f}s "
+          f"first_final {log[0][0] - t0:.3f}s "
           f"admitting rounds {adm} max gap {max(gaps) * 1e3:.1f}ms rounds {len(log)}", flush=True)
 dt, lg, t0 = max(runs, key=lambda r: r[0])
 print("slowest run, finalize times (ms):", [round((x[0] - t0) * 1e3) for x in lg])

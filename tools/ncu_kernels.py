@@ -57,21 +57,28 @@ def figures(m):
 
 
 launches = [dict(zip(hdr, r)) for r in rows[2:] if len(r) == len(hdr)]
+fused = "unfused" not in sys.argv[4:]    # K2 built inside the bulk pass (the default engine)
+BULK = "K2+K3 bulk sfg_jit_execute (payload build fused)" if fused else "K3 bulk sfg_jit_execute"
+K4 = "K4 triage (stop/absorb/admit + scans)"
 stages = {}
 seen_apply = False
 for m in launches:
     name = m.get("Kernel Name", "").split("(")[0]
-    if name.startswith("sfg_plan") or name.startswith("sfg_mutate"):
+    if name.startswith("sfg_plan_kernel") or name.startswith("sfg_mutate"):
         label = "K1 sfg_plan + sfg_mutate (+ scans)"
     elif name.startswith("sfg_apply"):
-        label = "K2 sfg_apply" if not seen_apply else None
+        label = "K2 sfg_apply" if not (seen_apply or fused) else None   # later launches: the tail's re-materialize
         seen_apply = True
     elif name == "sfg_jit_execute":
-        label = "K3 bulk sfg_jit_execute"
+        label = BULK
     elif name == "sfg_jit_tail":
         label = "K3 tail sfg_apply + sfg_jit_tail"
-    elif name.startswith("sfg_triage"):
-        label = "K4 triage (stop/absorb/admit + scans)"
+    elif name in ("sfg_stop_kernel", "sfg_absorb_kernel", "sfg_admit_kernel"):
+        label = K4
+    elif name.startswith("sfg_seq_walk"):
+        label = "seqgen walk (candidate successors)"
+    elif name.startswith("sfg_seq_mutate"):
+        label = "seqgen mutate (children from their start positions)"
     else:
         label = None
     if label is None:
@@ -81,8 +88,10 @@ for m in launches:
     prev = stages.get(label)
     if prev is None:
         stages[label] = f
-    elif label.startswith("K1") and prev["ncu_kernel"] != name:   # plan + mutate: sum the two kernels
-        for k in ("duration_ns", "dram_bytes_read", "dram_bytes_write", "traffic"):
+    elif (label.startswith("K1") or label == K4) and name not in prev["ncu_kernel"].split(" + "):
+        # plan + mutate, stop + absorb + admit: sum the kernels of the stage
+        for k in ("duration_ns", "dram_bytes_read", "dram_bytes_write", "traffic", "l2_atom_sectors",
+                  "l2_red_sectors"):
             if prev.get(k) is not None and f.get(k) is not None:
                 prev[k] += f[k]
         prev["ncu_kernel"] += " + " + name
