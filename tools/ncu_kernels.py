@@ -48,7 +48,10 @@ def figures(m):
          "thread_inst_executed": num(m, "sass__thread_inst_executed_true_per_opcode"),
          "achieved_warps_per_sm": num(m, "sm__warps_active.avg.per_cycle_active"),
          "dram_throughput_pct": num(m, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
-         "l2_atom_sectors": num(m, "lts__t_sectors_op_atom.sum"), "l2_red_sectors": num(m, "lts__t_sectors_op_red.sum")}
+         "l2_atom_sectors": num(m, "lts__t_sectors_srcunit_tex_op_atom.sum"),
+         "l2_red_sectors": num(m, "lts__t_sectors_srcunit_tex_op_red.sum"),
+         "l2_atom_requests": num(m, "lts__t_requests_srcunit_tex_op_atom_dot_alu.sum"),
+         "l2_red_requests": num(m, "lts__t_requests_srcunit_tex_op_red.sum")}
     if f["inst_executed"] and f["thread_inst_executed"]:
         f["active_threads_per_warp"] = f["thread_inst_executed"] / f["inst_executed"]
     if f["dram_bytes_read"] is not None and f["dram_bytes_write"] is not None:
