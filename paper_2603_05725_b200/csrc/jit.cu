@@ -24,6 +24,7 @@
 #include <filesystem>
 #include <fstream>
 #include <functional>
+#include <set>
 #include <map>
 #include <mutex>
 #include <sstream>
@@ -536,6 +537,464 @@ struct Gen {
     return out;
   }
 
+  // ---------------------------------------------------------------------------
+  // Nest summaries.  A loop at check block h whose body (the blocks on a cycle
+  // through h, inner loops included) repeats exactly from one trip to the next up
+  // to basic induction registers: the only registers carried from trip to trip are
+  // r = r +/- X (X an immediate or a register the body never writes, the def in a
+  // block every trip passes once); every other value the body uses is a function
+  // of registers the body never writes, of values loaded from records the body
+  // never stores to, and of the induction registers through i32 arithmetic whose
+  // per-trip change is 0 mod 2^32 (a run-time guard, e.g. row * ldc with
+  // ldc = -2^31 and a row step of 8); every exit tests a trip-invariant predicate
+  // or, at h, an induction register against an invariant.  Then every trip runs
+  // the same instructions on the same addresses and values: the first complete
+  // trip after arming is measured (retired instructions, edge counts) and the
+  // next k trips are skipped at once -- k below the first trip whose exit test at
+  // h holds (closed form, inside the i32 no-wrap horizon) and below the budget --
+  // induction registers advanced k steps, edges and retired counted k times;
+  // memory is as after one trip.  The remaining trips run instruction by
+  // instruction (exits and budget exhaustion exact, executor.py:411-415).
+  struct NV { int k = 0; std::string e; };   // 0 read-before-def, 1 invariant (e: expr or ""), 2 per-trip delta e, 3 hard
+  struct Nest {
+    int h = -1;
+    std::vector<int> blocks;
+    std::vector<std::pair<int, std::string>> r_iv;   // induction register, per-trip step (u32 expr)
+    bool has_x = false;                      // exit at h: iv <x_cmp> rhs (oriented: exits when it holds)
+    int x_cmp = 0, x_iv = -1;
+    std::string x_rhs;                       // int64 expression
+    // u32 expressions that must be 0, each needed only if its block ran in the measured
+    // trip (an access / compare the trip does not reach constrains nothing)
+    std::vector<std::pair<std::string, int>> guards;
+    std::vector<std::pair<std::string, std::pair<int, int>>> distinct;   // ptA != ptB if both blocks ran
+    std::vector<int> edges;                  // edges between body blocks (snapshotted per trip)
+    std::vector<std::vector<int>> in_edges;  // per body block (index into blocks): its in-edges' snapshot slots, -1: always runs
+  };
+
+  static int swap_cmp(int c) {
+    static const int m[] = {SFG_CMP_EQ, SFG_CMP_NE, SFG_CMP_GT, SFG_CMP_GE, SFG_CMP_LT, SFG_CMP_LE};
+    return m[c];
+  }
+
+  bool analyse_nest(const sfg_ins* I, int n, const std::vector<int>& starts, const std::vector<int>& blk_of, int regs,
+                    int h, const std::vector<std::vector<int>>& tags, Nest& N) {
+    const int nb = (int)starts.size();
+    const int R = regs > 0 ? regs : 1;
+    auto bend = [&](int b) { return b + 1 < nb ? starts[b + 1] : n; };
+    std::vector<std::vector<Succ>> sc(nb);
+    std::vector<std::vector<int>> pred(nb);
+    for (int b = 0; b < nb; ++b) {
+      sc[b] = succs(I, n, starts, blk_of, b);
+      for (const Succ& x : sc[b]) pred[x.blk].push_back(b);
+    }
+    std::vector<char> fw(nb, 0), bw(nb, 0), in(nb, 0);
+    std::vector<int> st{h};
+    fw[h] = 1;
+    while (!st.empty()) {
+      const int b = st.back(); st.pop_back();
+      for (const Succ& x : sc[b]) if (!fw[x.blk]) { fw[x.blk] = 1; st.push_back(x.blk); }
+    }
+    st = {h};
+    bw[h] = 1;
+    while (!st.empty()) {
+      const int b = st.back(); st.pop_back();
+      for (int q : pred[b]) if (!bw[q]) { bw[q] = 1; st.push_back(q); }
+    }
+    bool back = false;
+    for (int b = 0; b < nb; ++b) in[b] = fw[b] && bw[b];
+    for (int q : pred[h]) back |= in[q] != 0;
+    if (!back) return false;
+    N = Nest();
+    N.h = h;
+    for (int b = 0; b < nb; ++b) if (in[b]) N.blocks.push_back(b);
+    if (N.blocks.size() > 64) return false;
+    // register defs in the body
+    auto def_cls = [&](const sfg_ins& x, int& c) -> bool {
+      switch (x.op) {
+        case SFG_MOV: c = x.mode; return true;
+        case SFG_ADD: case SFG_SUB: case SFG_MUL: c = x.mode == SFG_CLS_A ? SFG_CLS_A : SFG_CLS_R; return true;
+        case SFG_FADD: case SFG_FSUB: case SFG_FMUL: c = SFG_CLS_F; return true;
+        case SFG_SETP: c = SFG_CLS_P; return true;
+        case SFG_CVT: c = x.mode == SFG_CVT_F_FROM_I ? SFG_CLS_F : SFG_CLS_R; return true;
+        case SFG_SREG: c = SFG_CLS_R; return true;
+        case SFG_LD: c = x.mode == SFG_MK_F32 ? SFG_CLS_F : x.mode == SFG_MK_B64 ? SFG_CLS_A : SFG_CLS_R; return true;
+        default: return false;
+      }
+    };
+    std::vector<int> ndef(4 * R, 0), def_at(4 * R, -1);
+    for (int b : N.blocks)
+      for (int i = starts[b]; i < bend(b); ++i) {
+        int c;
+        if (I[i].op == SFG_EXIT) return false;
+        if (def_cls(I[i], c)) { ++ndef[c * R + I[i].dst]; def_at[c * R + I[i].dst] = i; }
+      }
+    // a block every trip passes exactly once
+    auto once = [&](int D) -> bool {
+      if (D == h) return true;
+      std::vector<char> seen(nb, 0);
+      std::vector<int> s2;
+      for (const Succ& x : sc[D]) if (in[x.blk] && x.blk != h && !seen[x.blk]) { seen[x.blk] = 1; s2.push_back(x.blk); }
+      while (!s2.empty()) {
+        const int b = s2.back(); s2.pop_back();
+        if (b == D) return false;
+        for (const Succ& x : sc[b]) if (in[x.blk] && x.blk != h && !seen[x.blk]) { seen[x.blk] = 1; s2.push_back(x.blk); }
+      }
+      std::fill(seen.begin(), seen.end(), 0);
+      for (const Succ& x : sc[h]) {
+        if (x.blk == h) return false;
+        if (in[x.blk] && x.blk != D && !seen[x.blk]) { seen[x.blk] = 1; s2.push_back(x.blk); }
+      }
+      while (!s2.empty()) {
+        const int b = s2.back(); s2.pop_back();
+        for (const Succ& x : sc[b]) {
+          if (x.blk == h) return false;
+          if (in[x.blk] && x.blk != D && !seen[x.blk]) { seen[x.blk] = 1; s2.push_back(x.blk); }
+        }
+      }
+      return true;
+    };
+    std::vector<NV> entry(4 * R);
+    for (int c = 0; c < 4; ++c)
+      for (int q = 0; q < R; ++q) {
+        NV& v = entry[c * R + q];
+        if (ndef[c * R + q] == 0) {
+          v.k = 1;
+          v.e = c == SFG_CLS_R ? r(q) : "";
+          continue;
+        }
+        v.k = 0;
+        if (c != SFG_CLS_R || ndef[c * R + q] != 1) continue;
+        const sfg_ins& x = I[def_at[c * R + q]];
+        if (!(x.op == SFG_ADD || x.op == SFG_SUB) || x.mode != SFG_CLS_R) continue;
+        const bool i1 = x.flags & SFG_F_S1_IMM, i2 = x.flags & SFG_F_S2_IMM;
+        auto inv = [&](bool imm, int64_t iv, int reg) -> std::string {
+          if (imm) return u32lit(iv);
+          return ndef[SFG_CLS_R * R + reg] == 0 ? r(reg) : std::string();
+        };
+        std::string step;
+        if (!i1 && x.s1 == q) step = inv(i2, x.imm2, x.s2);
+        else if (x.op == SFG_ADD && !i2 && x.s2 == q) step = inv(i1, x.imm1, x.s1);
+        if (step.empty() || !once(blk_of[def_at[c * R + q]])) continue;
+        v.k = 2;
+        v.e = x.op == SFG_SUB ? "(uint32_t)(0u - " + step + ")" : step;
+        N.r_iv.push_back({q, v.e});
+      }
+    // the exit test at h: `setp p, iv, rhs` (or rhs, iv) then `bra p` leaving the body
+    int x_setp = -1;
+    {
+      const int e = bend(h);
+      const sfg_ins& last = I[e - 1];
+      if (last.op == SFG_BRA && (last.flags & SFG_F_PRED)) {
+        int stay = -1, outs = 0;
+        for (const Succ& x : sc[h]) {
+          if (in[x.blk]) stay = x.taken ? 1 : 0;
+          else ++outs;
+        }
+        int sdef = -1;
+        for (int i = starts[h]; i < e - 1; ++i)
+          if (I[i].op == SFG_SETP && I[i].dst == last.s1) sdef = i;
+          else { int c; if (def_cls(I[i], c) && c == SFG_CLS_P && I[i].dst == last.s1) sdef = -2; }
+        if (outs == 1 && stay >= 0 && sdef >= 0 && !(I[sdef].flags & SFG_F_FLOAT)) {
+          const sfg_ins& x = I[sdef];
+          const bool exit_p = (stay == 1) == ((last.flags & SFG_F_PNEG) != 0);
+          auto is_iv = [&](int slot) -> int {
+            const bool imm = slot == 1 ? (x.flags & SFG_F_S1_IMM) : (x.flags & SFG_F_S2_IMM);
+            if (imm) return -1;
+            const int q = slot == 1 ? x.s1 : x.s2;
+            for (auto& iv : N.r_iv) if (iv.first == q) {
+              for (int i = starts[h]; i < sdef; ++i) { int c; if (def_cls(I[i], c) && c == SFG_CLS_R && I[i].dst == q) return -1; }
+              return q;
+            }
+            return -1;
+          };
+          auto rhs = [&](int slot) -> std::string {
+            const bool imm = slot == 1 ? (x.flags & SFG_F_S1_IMM) : (x.flags & SFG_F_S2_IMM);
+            if (imm) {
+              int64_t m = slot == 1 ? x.imm1 : x.imm2;
+              const int64_t cl = 1ll << 40;
+              return i64lit(m > cl ? cl : m < -cl ? -cl : m);
+            }
+            const int q = slot == 1 ? x.s1 : x.s2;
+            return ndef[SFG_CLS_R * R + q] == 0 ? "(int64_t)(int32_t)" + r(q) : std::string();
+          };
+          const int l = is_iv(1), rr = is_iv(2);
+          int cmpv = -1;
+          std::string rh;
+          if (l >= 0 && rr < 0) { rh = rhs(2); cmpv = x.mode; N.x_iv = l; }
+          else if (rr >= 0 && l < 0) { rh = rhs(1); cmpv = swap_cmp(x.mode); N.x_iv = rr; }
+          if (cmpv >= 0 && !rh.empty()) {
+            N.has_x = true;
+            N.x_cmp = exit_p ? cmpv : neg_cmp(cmpv);
+            N.x_rhs = rh;
+            x_setp = sdef;
+          }
+        }
+      }
+    }
+    // abstract values through a trip, to a fixed point over the body (the back edges
+    // into h are cut: h starts every trip with `entry`)
+    bool ok = true;
+    bool check = false;
+    int cur_b = -1;
+    std::set<std::pair<std::string, int>> G;
+    std::set<std::pair<int, int>> ldt, stt;   // (tag, block)
+    auto need_inv = [&](const NV& v) {
+      if (v.k == 0 || v.k == 3) ok = false;
+      else if (v.k == 2 && check) G.insert({v.e, cur_b});
+    };
+    auto join = [&](NV& a, const NV& b) -> bool {
+      NV old = a;
+      if (a.k == 0 || b.k == 0) { a.k = 0; a.e.clear(); }
+      else if (a.k == 3 || b.k == 3) { a.k = 3; a.e.clear(); }
+      else if (a.k != b.k) { a.k = 3; a.e.clear(); }
+      else if (a.e != b.e) { if (a.k == 1) a.e.clear(); else { a.k = 3; a.e.clear(); } }
+      return a.k != old.k || a.e != old.e;
+    };
+    auto transfer = [&](std::vector<NV>& v, int i) {
+      const sfg_ins& x = I[i];
+      const bool i1 = x.flags & SFG_F_S1_IMM, i2 = x.flags & SFG_F_S2_IMM;
+      auto V = [&](int c, int q) -> NV& { return v[c * R + q]; };
+      auto rop = [&](int slot) -> NV {
+        const bool imm = slot == 1 ? i1 : i2;
+        if (imm) { NV t; t.k = 1; t.e = u32lit(slot == 1 ? x.imm1 : x.imm2); return t; }
+        const NV t = V(SFG_CLS_R, slot == 1 ? x.s1 : x.s2);
+        if (t.k == 0) ok = false;
+        return t;
+      };
+      auto cls_op = [&](int c, int slot) -> NV {   // f / a / p operand
+        const bool imm = slot == 1 ? i1 : i2;
+        if (imm) { NV t; t.k = 1; return t; }
+        const NV t = V(c, slot == 1 ? x.s1 : x.s2);
+        if (t.k == 0) ok = false;
+        return t;
+      };
+      NV res;
+      res.k = 1;
+      switch (x.op) {
+        case SFG_MOV:
+          if (x.mode == SFG_CLS_R) V(SFG_CLS_R, x.dst) = rop(1);
+          else V(x.mode, x.dst) = cls_op(x.mode, 1);
+          break;
+        case SFG_ADD: case SFG_SUB: case SFG_MUL: {
+          if (x.mode == SFG_CLS_A) {
+            // a pointer that varies from trip to trip is summarized by the i32 deltas
+            // that entered it: invariant iff they are all 0 (checked where it is used)
+            if (x.op == SFG_MUL) { ok = false; break; }
+            const NV sp = cls_op(SFG_CLS_A, 1);
+            const NV ro = i2 ? NV{1, ""} : rop(2);
+            NV t;
+            if (sp.k == 0 || ro.k == 0) { ok = false; break; }
+            if (sp.k == 3 || ro.k == 3) t.k = 3;
+            else if (sp.k == 1 && ro.k == 1) t.k = 1;
+            else {
+              t.k = 2;
+              t.e = sp.k == 2 && ro.k == 2 ? "(uint32_t)(" + sp.e + " | " + ro.e + ")" : (sp.k == 2 ? sp.e : ro.e);
+            }
+            V(SFG_CLS_A, x.dst) = t;
+            break;
+          }
+          const NV a1 = rop(1), a2 = rop(2);
+          if (a1.k == 0 || a2.k == 0) { ok = false; break; }
+          if (a1.k == 3 || a2.k == 3) { res.k = 3; }
+          else if (a1.k == 1 && a2.k == 1) {
+            res.k = 1;
+            const char* opc = x.op == SFG_ADD ? "+" : x.op == SFG_SUB ? "-" : "*";
+            res.e = (a1.e.empty() || a2.e.empty()) ? "" : "(uint32_t)(" + a1.e + " " + opc + " " + a2.e + ")";
+          } else if (x.op == SFG_MUL) {
+            if (a1.k == 2 && a2.k == 2) { need_inv(a1); need_inv(a2); res.k = 1; }
+            else {
+              const NV& vv = a1.k == 2 ? a1 : a2;
+              const NV& ii = a1.k == 2 ? a2 : a1;
+              if (ii.e.empty()) { need_inv(vv); res.k = 1; }
+              else { res.k = 2; res.e = "(uint32_t)(" + vv.e + " * " + ii.e + ")"; }
+            }
+          } else {
+            res.k = 2;
+            const char* opc = x.op == SFG_ADD ? "+" : "-";
+            const std::string d1 = a1.k == 2 ? a1.e : "0u", d2 = a2.k == 2 ? a2.e : "0u";
+            res.e = "(uint32_t)(" + d1 + " " + opc + " " + d2 + ")";
+          }
+          V(SFG_CLS_R, x.dst) = res;
+          break;
+        }
+        case SFG_FADD: case SFG_FSUB: case SFG_FMUL: {
+          const NV a1 = cls_op(SFG_CLS_F, 1), a2 = cls_op(SFG_CLS_F, 2);
+          res.k = (a1.k == 3 || a2.k == 3) ? 3 : 1;
+          V(SFG_CLS_F, x.dst) = res;
+          break;
+        }
+        case SFG_SETP:
+          if (x.flags & SFG_F_FLOAT) {
+            const NV a1 = cls_op(SFG_CLS_F, 1), a2 = cls_op(SFG_CLS_F, 2);
+            res.k = (a1.k == 3 || a2.k == 3) ? 3 : 1;
+          } else if (i != x_setp) {
+            need_inv(rop(1));
+            need_inv(rop(2));
+          } else {
+            res.k = 3;   // the exit test at h: only its branch may use it (closed form)
+          }
+          V(SFG_CLS_P, x.dst) = res;
+          break;
+        case SFG_CVT:
+          if (x.mode == SFG_CVT_F_FROM_I) { if (!i1) need_inv(rop(1)); V(SFG_CLS_F, x.dst) = res; }
+          else { const NV a1 = cls_op(SFG_CLS_F, 1); res.k = a1.k == 3 ? 3 : 1; V(SFG_CLS_R, x.dst) = res; }
+          break;
+        case SFG_SREG: {
+          static const char* names[] = {"tid", "block", "ctaid", "grid"};
+          res.e = std::string("(uint32_t)") + names[x.mode];
+          V(SFG_CLS_R, x.dst) = res;
+          break;
+        }
+        case SFG_LD: case SFG_ST: {
+          need_inv(cls_op(SFG_CLS_A, 1));
+          const int tg = tags[i][x.s1];
+          if (tg <= 0) ok = false;
+          if (x.op == SFG_LD) {
+            ldt.insert({tg, cur_b});
+            int c; def_cls(x, c);
+            V(c, x.dst) = res;
+          } else {
+            stt.insert({tg, cur_b});
+            if (x.mode == SFG_MK_F32) { if (!i2) { const NV t = cls_op(SFG_CLS_F, 2); if (t.k != 1) ok = false; } }
+            else if (x.mode == SFG_MK_B64) need_inv(cls_op(SFG_CLS_A, 2));
+            else if (!i2) need_inv(rop(2));
+          }
+          break;
+        }
+        case SFG_BRA:
+          if ((x.flags & SFG_F_PRED) && check) {
+            const NV pv = V(SFG_CLS_P, x.s1);
+            const bool is_x = blk_of[i] == h && i == bend(h) - 1 && x_setp >= 0;
+            if (!is_x && pv.k != 1) ok = false;
+          }
+          break;
+        default:
+          ok = false;
+      }
+    };
+    std::vector<std::vector<NV>> bin(nb);
+    std::vector<char> has(nb, 0);
+    bin[h] = entry;
+    has[h] = 1;
+    std::vector<int> work{h};
+    int steps = 0;
+    while (!work.empty() && ok) {
+      if (++steps > 4096) return false;
+      const int b = work.back(); work.pop_back();
+      std::vector<NV> v = bin[b];
+      cur_b = b;
+      for (int i = starts[b]; i < bend(b) && ok; ++i) transfer(v, i);
+      for (const Succ& x : sc[b]) {
+        if (!in[x.blk] || x.blk == h) continue;
+        if (!has[x.blk]) { bin[x.blk] = v; has[x.blk] = 1; work.push_back(x.blk); continue; }
+        bool ch = false;
+        for (int k = 0; k < 4 * R; ++k) ch |= join(bin[x.blk][k], v[k]);
+        if (ch) work.push_back(x.blk);
+      }
+    }
+    if (!ok) return false;
+    // the check pass over the fixed point: sinks need trip-invariant values
+    check = true;
+    for (int b : N.blocks) {
+      if (!has[b]) return false;
+      std::vector<NV> v = bin[b];
+      cur_b = b;
+      for (int i = starts[b]; i < bend(b) && ok; ++i) transfer(v, i);
+      // exits other than h's test need trip-invariant predicates (checked at BRA)
+      for (const Succ& x : sc[b]) if (!in[x.blk] && !(I[bend(b) - 1].op == SFG_BRA && (I[bend(b) - 1].flags & SFG_F_PRED)))
+        ok = false;   // an unconditional way out of the body cannot be on a cycle
+    }
+    if (!ok) return false;
+    for (auto& lt : ldt)
+      for (auto& s2 : stt) {
+        if (lt.first == s2.first) return false;   // a record the body both loads and stores
+        N.distinct.push_back({"pt" + std::to_string(lt.first - 1) + " != pt" + std::to_string(s2.first - 1),
+                              {lt.second, s2.second}});
+      }
+    for (auto& g : G) N.guards.push_back({"(uint32_t)(" + g.first + ") == 0u", g.second});
+    std::set<int> es;
+    for (int b : N.blocks) for (const Succ& x : sc[b]) if (x.edge >= 0 && in[x.blk]) es.insert(x.edge);
+    N.edges.assign(es.begin(), es.end());
+    // a body block ran in a trip iff one of its in-edges from the body was taken (h always)
+    N.in_edges.assign(N.blocks.size(), {});
+    for (size_t bi = 0; bi < N.blocks.size(); ++bi) {
+      const int b = N.blocks[bi];
+      if (b == h) { N.in_edges[bi] = {-1}; continue; }
+      for (int q : pred[b]) {
+        if (!in[q]) continue;
+        for (const Succ& x : sc[q]) {
+          if (x.blk != b) continue;
+          if (x.edge < 0) { N.in_edges[bi] = {-1}; break; }
+          N.in_edges[bi].push_back((int)(std::lower_bound(N.edges.begin(), N.edges.end(), x.edge) - N.edges.begin()));
+        }
+        if (!N.in_edges[bi].empty() && N.in_edges[bi][0] == -1) break;
+      }
+      if (N.in_edges[bi].empty()) N.in_edges[bi] = {-1};
+    }
+    return true;
+  }
+
+  // arming at the fast entry of h once the thread has run kNestArm instructions
+  // since the last attempt: snapshot of the retired count and the body's edges
+  std::string nest_arm_code(const Nest& N) {
+    std::ostringstream s;
+    const std::string H = std::to_string(N.h);
+    s << "  else if (ret >= nsn" << H << ") { ns" << H << " = true; nsr" << H << " = ret; nsn" << H
+      << " = ret + kNestArm;";
+    for (size_t k = 0; k < N.edges.size(); ++k)
+      s << " nse" << H << "[" << k << " ^ J.J_dyn] = J.ec[" << N.edges[k] << "];";
+    s << " }\n";
+    return s.str();
+  }
+
+  // at the fast entry of h, one complete trip after arming: skip k trips
+  std::string nest_skip_code(const Nest& N, const char* RT) {
+    std::ostringstream s;
+    const std::string H = std::to_string(N.h);
+    s << "  if (ns" << H << " && ret != nsr" << H << ") { // nest summary: blocks";
+    for (int b : N.blocks) s << " " << b;
+    s << "\n    ns" << H << " = false;\n";
+    auto ran = [&](int b) -> std::string {   // block b ran in the measured trip
+      const size_t bi = std::find(N.blocks.begin(), N.blocks.end(), b) - N.blocks.begin();
+      const std::vector<int>& ie = N.in_edges[bi];
+      if (ie.empty() || ie[0] < 0) return "true";
+      std::string c = "(";
+      for (size_t k = 0; k < ie.size(); ++k)
+        c += (k ? " || " : "") + std::string("J.ec[") + std::to_string(N.edges[ie[k]]) + "] != nse" + H + "[" +
+             std::to_string(ie[k]) + " ^ J.J_dyn]";
+      return c + ")";
+    };
+    s << "    bool g_ = true;\n";
+    for (auto& g : N.guards) s << "    g_ = g_ && (!" << ran(g.second) << " || " << g.first << ");\n";
+    for (auto& d : N.distinct)
+      s << "    g_ = g_ && (!(" << ran(d.second.first) << " && " << ran(d.second.second) << ") || " << d.first << ");\n";
+    s << "    const uint64_t len_ = (uint64_t)(ret - nsr" << H << ");\n"
+      << "    int64_t H_ = g_ && HARD > ret ? (int64_t)((uint64_t)(HARD - 1u - ret) / len_) : -1;\n";
+    for (auto& iv : N.r_iv) s << "    const uint32_t dn" << iv.first << "_ = " << iv.second << ";\n";
+    if (N.has_x) {
+      const std::string q = std::to_string(N.x_iv);
+      s << "    const int64_t x0_ = (int64_t)(int32_t)" << r(N.x_iv) << ", xd_ = (int64_t)(int32_t)dn" << q << "_;\n"
+        << "    H_ = sfg_min64(H_, sfg_wrap_h(x0_, xd_));\n"
+        << "    const int64_t T_ = sfg_first_t(" << N.x_cmp << ", x0_ - (" << N.x_rhs << "), xd_, H_);\n"
+        << "    const int64_t k_ = T_ < H_ ? T_ : H_;\n";
+    } else {
+      s << "    const int64_t k_ = H_;\n";
+    }
+    s << "    if (k_ >= 1) {\n";
+    for (auto& iv : N.r_iv)
+      s << "      " << r(iv.first) << " = (uint32_t)(" << r(iv.first) << " + (uint32_t)k_ * dn" << iv.first << "_);\n";
+    for (size_t k = 0; k < N.edges.size(); ++k)
+      s << "      { const uint64_t o_ = (uint64_t)J.ec[" << N.edges[k] << "] + (uint64_t)k_ * (uint64_t)(uint32_t)(J.ec["
+        << N.edges[k] << "] - nse" << H << "[" << k << " ^ J.J_dyn]); if (o_ > 0xFFFFFFFFull) J.ovf = true; J.ec["
+        << N.edges[k] << "] = (uint32_t)o_; }\n";
+    s << "      const " << RT << " sk_ = (" << RT << ")((uint64_t)k_ * len_);\n"
+      << "      ret += sk_;\n"
+      << "      if (SFT) { HARD = (" << RT << ")(BUD - HARD > sk_ ? HARD + sk_ : BUD); if (HARD == BUD) SFT = false; }\n"
+      << "    }\n  }\n";
+    s << nest_arm_code(N);
+    return s.str();
+  }
+
   // C++ of the summaries at a window check of block h
   std::string summary_code(const std::vector<Cycle>& cs, const char* RT) {
     std::ostringstream s;
@@ -839,8 +1298,8 @@ struct Gen {
     const char* RT = narrow ? "uint32_t" : "uint64_t";
     o << "  " << RT << " ret = 0; int rc = RUN_EXIT; const " << RT << " BUD = (" << RT << ")P.budget;\n";
     // fast-path limit: the budget, or the remaining soft cap of the input (deferral)
-    o << "  const uint64_t SOFT = J.soft_cap; const bool SFT = SOFT != 0ull && (SOFT <= total || SOFT - total < (uint64_t)BUD);\n";
-    o << "  const " << RT << " HARD = SFT ? (" << RT << ")(SOFT > total ? SOFT - total : 0ull) : BUD;\n";
+    o << "  const uint64_t SOFT = J.soft_cap; bool SFT = SOFT != 0ull && (SOFT <= total || SOFT - total < (uint64_t)BUD);\n";
+    o << "  " << RT << " HARD = SFT ? (" << RT << ")(SOFT > total ? SOFT - total : 0ull) : BUD;\n";
     // group-parallel mode: stop at poll points every kPoll retired instructions to see
     // whether this thread can still matter (run_launch_group)
     // bulk pass (soft cap on): poll every kStrag retired instructions whether the rest of
@@ -856,6 +1315,25 @@ struct Gen {
           has_sum |= !sums[b].empty();
         }
     for (auto& v : sums) n_summaries += (int)v.size();
+    // nest summaries (analyse_nest): loops with memory accesses and inner loops
+    std::vector<Nest> nests(nb);
+    std::vector<char> has_nest(nb, 0);
+    if (loop_summaries && nest_summaries)
+      for (int b = 0; b < nb; ++b)
+        if (chk[b] && span[b] > 0 && analyse_nest(I, K.n, starts, blk_of, K.regs, b, tags, nests[b])) {
+          has_nest[b] = 1;
+          has_sum = true;
+          ++n_nests;
+          if (getenv("SFG_LOOPSUM_DEBUG")) {
+            fprintf(stderr, "nest at %d:", b);
+            for (int x : nests[b].blocks) fprintf(stderr, " %d", x);
+            fprintf(stderr, " ivs %zu exit %d guards %zu distinct %zu edges %zu\n", nests[b].r_iv.size(),
+                    (int)nests[b].has_x, nests[b].guards.size(), nests[b].distinct.size(), nests[b].edges.size());
+          }
+          const std::string H = std::to_string(b);
+          o << "  bool ns" << H << " = false; " << RT << " nsr" << H << " = 0, nsn" << H << " = (" << RT
+            << ")kNestArm; uint32_t nse" << H << "[" << (nests[b].edges.empty() ? 1 : nests[b].edges.size()) << "];\n";
+        }
     o << "  " << RT << " LIM = PAR ? ((HARD > (" << RT << ")kPoll) ? (" << RT << ")kPoll : HARD)\n"
          "            : (((J.done != nullptr || " << (has_sum ? "true" : "false") << ") && HARD > (" << RT << ")kStrag) ? ("
       << RT << ")kStrag : HARD);\n";
@@ -867,15 +1345,20 @@ struct Gen {
       for (int pass = 0; pass < 2; ++pass) {
         const bool slow = pass == 1;
         o << (slow ? "S" : "B") << b << ":\n";
-        if (!slow && chk[b] && span[b] > 0)
+        if (slow && has_nest[b]) o << "  ns" << b << " = false;\n";   // a trip measured across the slow path is void
+        if (!slow && chk[b] && span[b] > 0) {
+          // a cycle summary at h moves the thread between arrivals: a pending nest measurement is void
+          const std::string arm = has_nest[b] ? "      ns" + std::to_string(b) + " = false;\n" : std::string();
           o << "  if (ret + " << sp << " >= LIM) {\n"
             << "    if constexpr (PAR) { if (LIM < HARD) { if (J.poll()) { rc = RUN_ABORT; goto done; }\n"
-            << summary_code(sums[b], RT)
+            << summary_code(sums[b], RT) << arm
             << "      LIM = (HARD - ret > " << sp << " + kPoll) ? ret + " << sp << " + kPoll : HARD; goto B" << b << "; } }\n"
             << "    else { if (LIM < HARD) { if (J.done != nullptr && J.straggler(total + ret)) { rc = RUN_DEFER; goto done; }\n"
-            << summary_code(sums[b], RT)
+            << summary_code(sums[b], RT) << arm
             << "      LIM = (HARD - ret > " << sp << " + kStrag) ? ret + " << sp << " + kStrag : HARD; goto B" << b << "; } }\n"
             << "    if (SFT) { rc = RUN_DEFER; goto done; } goto S" << b << "; }\n";
+          if (has_nest[b]) o << nest_skip_code(nests[b], RT);
+        }
         for (int i = s0; i < e; ++i) {
           const sfg_ins& x = I[i];
           const int j = i - s0;
@@ -916,7 +1399,8 @@ struct Gen {
   }
 
   bool loop_summaries = true;
-  int n_summaries = 0;
+  bool nest_summaries = true;
+  int n_summaries = 0, n_nests = 0;
   int tail_minb = 12;
   int bulk_minb = 4;
 
@@ -928,6 +1412,7 @@ struct Gen {
       << "\n#define SFG_LANE_PARAMS " << caps.params << "\n";
     o << "#include \"exec_core.cuh\"\n\nnamespace {\n\n";
     o << "constexpr uint32_t kPoll = 4096u;\n";
+    o << "constexpr uint32_t kNestArm = 4096u;   // retired instructions between nest-summary attempts\n";
     // loop-summary helpers (see analyse_cycle)
     o << "#define SFG_I64MAX 0x7FFFFFFFFFFFFFFFll\n";
     o << "SFG_DEV int64_t sfg_min64(int64_t a, int64_t b) { return a < b ? a : b; }\n"
@@ -1140,6 +1625,7 @@ static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_e
   g.dead_kernels = dead_kernels;
   g.caps = caps;
   if (const char* ls = getenv("SFG_LOOPSUM")) g.loop_summaries = atoi(ls) != 0;
+  if (const char* ns = getenv("SFG_NESTSUM")) g.nest_summaries = atoi(ns) != 0;
   if (const char* tb = getenv("SFG_TAIL_MINB")) g.tail_minb = atoi(tb) >= 1 ? atoi(tb) : 12;
   if (const char* bb = getenv("SFG_BULK_MINB")) g.bulk_minb = atoi(bb) >= 1 ? atoi(bb) : 4;
   source = g.run(P.n_edges, max_edge_events);

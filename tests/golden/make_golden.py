@@ -19,6 +19,8 @@ Writes (all small, committed):
                       workloads (paper_2603_05725_b200/workloads)
   ref_errors.json     the exception class the reference fuzz_loop raises for
                       failing harnesses (INIT failure, out of space)
+  ref_nests.json      matmul loop nests with loads/stores to the budget, to the
+                      row exit, and with failing nest guards (records per budget)
   ref_traces.json     ExecHooks event streams (TraceHooks "EV mem" / "EV cf"
                       lines): per sampled input of every benchmark, and for a
                       traced batched campaign (dot, amax)
@@ -432,6 +434,50 @@ def loops():
     return out
 
 
+# Loop nests with loads and stores (the JIT's nest summaries, csrc/jit.cu
+# analyse_nest) on the C2 matmul kernel: row loops whose cols / inner loops touch
+# the same addresses every row (a zero or wrapping leading dimension: i*lda*4 and
+# i*ldc*4 are 0 mod 2^32 for every row step of 8), to the budget at every position
+# of a row trip (budgets 10^6 + k) or to the row exit; and nests whose guards fail
+# (a stride that moves the accesses every row), ending at the budget or in an
+# out-of-bounds store.  (m, n, k, lda, ldb, ldc)
+M31N = 1 << 31
+NEST_INPUTS = [
+    ((1 << 31) - 1, 8, 0, 8, 8, -M31N),        # stores only, wrapping ldc: summarized to the budget
+    (16515080, 8, 8, 0, 8, 0),                 # loads + stores, zero lda / ldc
+    (15925256, 8, 8, -M31N, 8, -M31N),         # loads + stores, wrapping lda / ldc
+    (40000, 8, 0, 8, 8, 0),                    # exits at the row test before the budget
+    (4000, 8, 8, 0, 8, 0),                     # exits, loads + stores
+    (8000, 8, -5, 8, 8, -M31N),                # exits, inner loop never entered
+    ((1 << 31) - 1, 8, 8, 8, 8, 0),            # guard fails (lda moves the A row): plain execution
+    ((1 << 31) - 1, 8, 0, 8, 8, 1),            # guard fails (ldc = 1): out-of-bounds store
+]
+NEST_BUDGETS = [10 ** 6 + k for k in range(0, 700, 97)] + [200003]
+
+
+def nests():
+    mm = rc.load_harness(REPO / "paper_2603_05725_b200" / "workloads" / "matmul.man")
+    out = {"inputs": NEST_INPUTS, "budgets": NEST_BUDGETS, "records": []}
+    for budget in NEST_BUDGETS:
+        for vals in NEST_INPUTS:
+            s = mm.seed(1)
+            args = list(s.args)
+            for j, v in enumerate(vals):
+                args[3 + j] = IntValue(v)
+            tc = TestCase(tuple(args), s.rng_seed)
+            image = DeviceMemoryImage()
+            runner = rc.PhaseRunner(mm, image, instruction_budget=budget, diff_readback=True)
+            runner.run_phase(rc.INIT, mm.seed(1), iteration=0)
+            runner.mark_baseline()
+            cov = CoverageMap.for_program(mm.program)
+            res = runner.run_phase(rc.COMPUTE, tc, coverage=cov, iteration=1)
+            out["records"].append({
+                "budget": budget, "testcase": serialize_testcase(tc, with_id=False), "status": res.status,
+                "retired": res.retired, "report": res.report.to_line() if res.report else None,
+                "readouts": {k: v.hex() for k, v in res.readouts.items()}, "edges": edges_json(cov)})
+    return out
+
+
 # Phase features beyond the bundled harnesses (campaign.py:483-561, 723-762):
 # kernels storing >= 4 KB per exec into an INIT (`buf:`) buffer, an INIT-phase
 # launch (with an array argument materialized in INIT), a TERM-phase launch that
@@ -598,7 +644,7 @@ def _dump(obj) -> str:
 def main():
     import tempfile
     which = sys.argv[1:] or ["assets", "variants", "sampled", "batched", "fuzzloop", "workloads", "traces",
-                             "errors", "loops", "features"]
+                             "errors", "loops", "features", "nests"]
     if "assets" in which:
         (HERE / "bench_assets.json").write_text(_dump(assets()))
     if "variants" in which:
@@ -619,6 +665,8 @@ def main():
         (HERE / "ref_features.json").write_text(_dump(features()))
     if "loops" in which:
         (HERE / "ref_loops.json").write_text(_dump(loops()))
+    if "nests" in which:
+        (HERE / "ref_nests.json").write_text(_dump(nests()))
     if "errors" in which:
         with tempfile.TemporaryDirectory() as tmp:
             (HERE / "ref_errors.json").write_text(_dump(errors(tmp)))

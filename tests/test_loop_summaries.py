@@ -109,3 +109,41 @@ def test_loop_campaigns_match_reference(cuda_ok, kern, mode, monkeypatch):
         dc.L.sfg_program_jit_source(dc.h, buf, nb + 1)
         assert "// loop summary:" in buf.value.decode()
     dc.close()
+
+
+def test_nest_summary_generated_for_matmul_rows():
+    """matmul's row loop with its cols / inner loops, loads of A and B and stores of
+    C is a nest summary (csrc/jit.cu analyse_nest): one induction register (the
+    row), the row test as closed-form exit, the A / C address guards and the
+    load-vs-store record guards, all conditional on the block having run."""
+    src = _source(workload_manifest("matmul"))
+    assert src.count("// nest summary: blocks 1 2 3 4 5 6 7 8") == 1
+    assert "(uint32_t)(r14 * r5)" in src and "(uint32_t)(r14 * r3)" in src
+    assert "pt0 != pt2" in src and "pt1 != pt2" in src
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["default", "nonest"])
+def test_nest_inputs_match_reference(cuda_ok, mode, monkeypatch):
+    """matmul row loops with loads and stores (zero / wrapping leading dimensions)
+    to the budget at every position of a row trip (budgets 10^6 + 97 k), to the
+    row exit, and with failing guards, equal the REAL reference's records
+    (tests/golden/ref_nests.json): status, retired, report, edges, readouts."""
+    from paper_2603_05725_b200.engine import DeviceCampaign
+    if mode == "nonest":
+        monkeypatch.setenv("SFG_NESTSUM", "0")
+    d = golden("ref_nests.json")
+    m = workload_manifest("matmul")
+    for budget in d["budgets"]:
+        rs = [r for r in d["records"] if r["budget"] == budget]
+        dc = DeviceCampaign(m, master_seed=1, budget=budget, diff_readback=True)
+        # each input alone at iteration 1, as the reference ran it (reports carry the iteration)
+        outs = [dc.execute_testcases([parse_testcase(r["testcase"])[0]], iteration0=1)[0] for r in rs]
+        for i, (out, r) in enumerate(zip(outs, rs)):
+            where = (budget, i, d["inputs"][i])
+            assert out["status"] == r["status"], where
+            assert out["retired"] == r["retired"], where
+            assert (out["report"].to_line() if out["report"] else None) == r["report"], where
+            assert out["edges"] == r["edges"], where
+            assert {k: v.hex() for k, v in out["readouts"].items()} == r["readouts"], where
+        dc.close()
