@@ -324,7 +324,8 @@ int sfg_program_create(const void* prog, size_t prog_bytes, const void* ins, siz
       for (int k = 0; k < p->P.n_kernels; ++k) np = p->P.kernels[k].n_params > np ? p->P.kernels[k].n_params : np;
       caps.params = clampc(np, SFG_MAX_ARGS);
     }
-    const int rc = sfg_jit_build(p->P, (const sfg_ins*)ins, events, dead, caps, p->jit_source, p->jit_log, &p->jit_lib,
+    const int rc = sfg_jit_build(p->P, (const sfg_ins*)ins, events, dead, caps, H, n_hostops,
+                                 (const sfg_binding*)binds, p->jit_source, p->jit_log, &p->jit_lib,
                                  &p->jit_kernel, &p->jit_tail);
     if (rc != 0) {
       g_err = "sfg_program_create: JIT build failed (" + std::to_string(rc) + "): " + p->jit_log.substr(0, 6000);
@@ -440,7 +441,8 @@ int sfg_jit_check(const void* prog, size_t prog_bytes, const void* ins, uint64_t
   memcpy(&P, prog, sizeof P);
   std::string src, log;
   std::vector<char> cubin;
-  const int rc = sfg_jit_compile(P, (const sfg_ins*)ins, max_edge_events, 0u, sfgjit::LaneCaps{}, src, log, cubin);
+  const int rc = sfg_jit_compile(P, (const sfg_ins*)ins, max_edge_events, 0u, sfgjit::LaneCaps{}, nullptr, 0, nullptr,
+                                 src, log, cubin);
   const std::string text = rc ? log + "\n----\n" + src : src;
   if (out && cap) {
     const size_t n = text.size() < cap - 1 ? text.size() : cap - 1;

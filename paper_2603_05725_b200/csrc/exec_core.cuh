@@ -56,6 +56,15 @@ constexpr uint8_t SH_RZ = 0xFA, SH_FREED = 0xFD, SH_UNALLOC = 0xFF;
 #ifndef SFG_LANE_PARAMS   // kernel parameters of a launch (bound values by class)
 #define SFG_LANE_PARAMS SFG_MAX_ARGS
 #endif
+// Array arguments no launch stores through / loads through (jit.cu array_masks;
+// 0 for the generic interpreter): the bulk pass reads an unmutated read-only array
+// straight from the parent's corpus payload and does not build a write-only one.
+#ifndef SFG_RO_ARGS
+#define SFG_RO_ARGS 0u
+#endif
+#ifndef SFG_WO_ARGS
+#define SFG_WO_ARGS 0u
+#endif
 constexpr int kMaxQ = SFG_LANE_Q;
 constexpr int kMaxFree = SFG_LANE_FREE;
 
@@ -721,19 +730,33 @@ SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R, c
   int defer_kind = 0;  // 1: soft cap reached (deferred), 2: re-run thread-sequentially (deferred_seq)
   int seq_reruns = 0;  // group-parallel chunks undone and re-run sequentially (diagnostics)
   if (GRP && ntags > g.tag_cap) defer_kind = 2;
+  uint32_t alias = 0;               // arrays whose record reads the parent's payload in place
+  const sfg_val* mpv = nullptr;     // the parent's values (in-kernel materialization)
   if (E.mat_data != nullptr && defer_kind == 0) {
-    const sfg_val* pv = E.mat_vals + (size_t)(ch.parent < 0 ? 0 : ch.parent) * P.n_args;
+    mpv = E.mat_vals + (size_t)(ch.parent < 0 ? 0 : ch.parent) * P.n_args;
     const int gl = GRP ? g.gl : 0, gn = GRP ? g.G : 1;
     for (int a = 0; a < P.n_args; ++a) {
       if (cv[a].kind != SFG_V_ARR) continue;
       const sfg_op* op = nullptr;
       for (int k = 0; k < ch.n_ops; ++k)
         if (ch.ops[k].arg == a) op = &ch.ops[k];
-      emit_child(wk + cv[a].data_off, sfg_mat_size(cv[a]), E.mat_data + pv[a].data_off, pv[a].nbytes, cv[a], op, gl,
-                 gn);
       if ((P.copy_src_mask >> a) & 1u)   // the test case's own bytes for copy_in (campaign.py:404-409)
         emit_child(wk + sfg_pristine_off(&P, cv, ch.work_bytes, a, nullptr), cv[a].nbytes,
-                   E.mat_data + pv[a].data_off, pv[a].nbytes, cv[a], op, gl, gn);
+                   E.mat_data + mpv[a].data_off, mpv[a].nbytes, cv[a], op, gl, gn);
+      const uint64_t msz = sfg_mat_size(cv[a]);
+      if (!GRP) {
+        // never loaded (and no readback of it): its bytes are never read
+        if (((SFG_WO_ARGS >> a) & 1u) && !P.diff_readback) continue;
+        // never stored, data unchanged by the child's op, within the parent's bytes:
+        // the materialized contents ARE the parent's payload prefix (emit_child)
+        const uint64_t lim = cv[a].nbytes < mpv[a].nbytes ? cv[a].nbytes : mpv[a].nbytes;
+        if (((SFG_RO_ARGS >> a) & 1u) && msz <= lim &&
+            (op == nullptr || (op->kind != SFG_M_ARRAY_EXTREME && op->kind != SFG_M_ARRAY_ELEM))) {
+          alias |= 1u << a;
+          continue;
+        }
+      }
+      emit_child(wk + cv[a].data_off, msz, E.mat_data + mpv[a].data_off, mpv[a].nbytes, cv[a], op, gl, gn);
     }
     if constexpr (GRP) __syncwarp(g.mask);
   }
@@ -832,7 +855,11 @@ SFG_DEV void run_input(const sfg_prog& P, const ExecView& E, int i, Runner& R, c
       if (v.kind == SFG_V_F32) { pre.f[pre.nf++] = sfg_quiet(v.bits); continue; }
       if (L.mat_rec[B.idx] < 0) {
         const int64_t size = (int64_t)sfg_mat_size(v);
-        const int k = lane_alloc(P, L, v.space, size, P.label_arg_base + B.idx, (int64_t)v.data_off);
+        // an aliased array's record addresses the parent's payload (phys relative to the work region)
+        const int64_t phys = ((alias >> B.idx) & 1u)
+                                 ? (int64_t)((uintptr_t)(E.mat_data + mpv[B.idx].data_off) - (uintptr_t)wk)
+                                 : (int64_t)v.data_off;
+        const int k = lane_alloc(P, L, v.space, size, P.label_arg_base + B.idx, phys);
         if (k < 0) { V.status = -k; oos_detail(P, L, V, v.space, size); stop = true; break; }
         L.mat_rec[B.idx] = (int16_t)k;
       }

@@ -1116,6 +1116,63 @@ struct Gen {
   // COMPUTE script, no readouts) -- its stores can only be observed by its own loads
   uint32_t dead_kernels = 0;
   LaneCaps caps;
+  const sfg_hostop* hostops = nullptr;   // the COMPUTE script (array-argument access masks)
+  size_t n_hostops = 0;
+  const sfg_binding* binds = nullptr;
+
+  // Array arguments of the COMPUTE script that no launch ever stores through (ro) or
+  // loads through (wo), from the kernels' pointer-tag flow: a store / load with no
+  // static tag could reach any record and clears every bit.  The bulk pass reads
+  // an ro array of an unmutated child straight from its parent's corpus payload
+  // and leaves a wo array unbuilt (its bytes are never read), exec_core.cuh.
+  void array_masks(uint32_t& ro, uint32_t& wo) {
+    ro = wo = 0;
+    for (int a = 0; a < P.n_args; ++a)
+      if (P.arg_kind[a] == SFG_V_ARR) { ro |= 1u << a; wo |= 1u << a; }
+    if (!hostops || !binds) { ro = wo = 0; return; }
+    std::vector<std::vector<char>> kw(P.n_kernels), kl(P.n_kernels);
+    std::vector<char> kuw(P.n_kernels, 0), kul(P.n_kernels, 0);
+    for (int k = 0; k < P.n_kernels; ++k) {
+      const sfg_kernel& KD = P.kernels[k];
+      KInfo K{KD.ins_base, KD.n_ins, KD.regs, 0, 0, 0};
+      for (int q = 0; q < KD.n_params; ++q) {
+        if (KD.ptype[q] == 0) ++K.nr;
+        else if (KD.ptype[q] == 1) ++K.nf;
+        else ++K.na;
+      }
+      const sfg_ins* I = ins + K.base;
+      const std::vector<int> starts = block_starts(I, K.n);
+      std::vector<int> blk_of;
+      const auto tags = tag_flow(I, K.n, K, starts, blk_of);
+      kw[k].assign(K.na > 0 ? K.na : 1, 0);
+      kl[k].assign(K.na > 0 ? K.na : 1, 0);
+      for (int i = 0; i < K.n; ++i) {
+        if (I[i].op != SFG_ST && I[i].op != SFG_LD) continue;
+        const int tg = tags[i][I[i].s1];
+        const bool st = I[i].op == SFG_ST;
+        if (tg > 0) (st ? kw[k] : kl[k])[tg - 1] = 1;
+        else if (tg != TAG_BOT) (st ? kuw[k] : kul[k]) = 1;
+      }
+    }
+    for (size_t h = 0; h < n_hostops; ++h) {
+      const sfg_hostop& op = hostops[h];
+      if (op.kind != SFG_H_LAUNCH) continue;
+      const sfg_kernel& KD = P.kernels[op.kernel];
+      if (kuw[op.kernel]) ro = 0;
+      if (kul[op.kernel]) wo = 0;
+      int q = 0;   // pointer-parameter index of binding b
+      for (int b = 0; b < op.n_bind && b < KD.n_params; ++b) {
+        if (KD.ptype[b] != 2) continue;
+        const sfg_binding& B = binds[op.bind_base + b];
+        if (B.form == SFG_B_ARG && B.idx >= 0 && B.idx < 32) {
+          if (kw[op.kernel][q]) ro &= ~(1u << B.idx);
+          if (kl[op.kernel][q]) wo &= ~(1u << B.idx);
+        }
+        ++q;
+      }
+    }
+  }
+
   bool dead_now = false;
 
   std::string src_r(const sfg_ins& x, int slot) {
@@ -1407,6 +1464,10 @@ struct Gen {
   std::string run(int n_edges, uint64_t max_edge_events) {
     edge_ovf_checks = max_edge_events >= 0xFFFFFFFFull;
     const int NE = n_edges > 0 ? n_edges : 1;
+    uint32_t ro_mask = 0, wo_mask = 0;
+    array_masks(ro_mask, wo_mask);
+    if (const char* am = getenv("SFG_ARRAY_ALIAS")) if (atoi(am) == 0) ro_mask = wo_mask = 0;
+    o << "#define SFG_RO_ARGS " << ro_mask << "u\n#define SFG_WO_ARGS " << wo_mask << "u\n";
     o << "#define SFG_LANE_RECS " << caps.recs << "\n#define SFG_LANE_Q " << caps.q << "\n#define SFG_LANE_FREE "
       << caps.freel << "\n#define SFG_LANE_NAMED " << caps.named << "\n#define SFG_LANE_ARGS " << caps.args
       << "\n#define SFG_LANE_PARAMS " << caps.params << "\n";
@@ -1619,11 +1680,15 @@ static void jit_cache_store(const std::string& key, const std::vector<char>& cub
 
 // Generate and compile; on success `cubin` holds the sm_100a image.  Returns 0 on success.
 static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_edge_events, uint32_t dead_kernels,
-                           const sfgjit::LaneCaps& caps, std::string& source,
+                           const sfgjit::LaneCaps& caps, const sfg_hostop* hostops, size_t n_hostops,
+                           const sfg_binding* binds, std::string& source,
                            std::string& log, std::vector<char>& cubin) {
   sfgjit::Gen g(P, ins);
   g.dead_kernels = dead_kernels;
   g.caps = caps;
+  g.hostops = hostops;
+  g.n_hostops = n_hostops;
+  g.binds = binds;
   if (const char* ls = getenv("SFG_LOOPSUM")) g.loop_summaries = atoi(ls) != 0;
   if (const char* ns = getenv("SFG_NESTSUM")) g.nest_summaries = atoi(ns) != 0;
   if (const char* tb = getenv("SFG_TAIL_MINB")) g.tail_minb = atoi(tb) >= 1 ? atoi(tb) : 12;
@@ -1687,10 +1752,12 @@ static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_e
 
 // Generate, compile and load the specialized execute kernels (bulk + tail).  Returns 0 on success.
 static int sfg_jit_build(const sfg_prog& P, const sfg_ins* ins, uint64_t max_edge_events, uint32_t dead_kernels,
-                         const sfgjit::LaneCaps& caps, std::string& source,
+                         const sfgjit::LaneCaps& caps, const sfg_hostop* hostops, size_t n_hostops,
+                         const sfg_binding* binds, std::string& source,
                          std::string& log, cudaLibrary_t* lib_out, cudaKernel_t* kern_out, cudaKernel_t* tail_out) {
   std::vector<char> cubin;
-  const int rc = sfg_jit_compile(P, ins, max_edge_events, dead_kernels, caps, source, log, cubin);
+  const int rc = sfg_jit_compile(P, ins, max_edge_events, dead_kernels, caps, hostops, n_hostops, binds, source, log,
+                                 cubin);
   if (rc) return rc;
   // Loaded libraries stay loaded for the process, one per distinct program on each
   // device: unloading a module whose kernels use a large local-memory frame makes the

@@ -147,3 +147,17 @@ def test_nest_inputs_match_reference(cuda_ok, mode, monkeypatch):
             assert out["edges"] == r["edges"], where
             assert {k: v.hex() for k, v in out["readouts"].items()} == r["readouts"], where
         dc.close()
+
+
+@pytest.mark.gpu
+def test_array_alias_masks_for_matmul(cuda_ok):
+    """jit.cu array_masks on C2 matmul: A and B are never stored (read from the
+    parent's payload in place when unmutated), C is never loaded (not built)."""
+    from paper_2603_05725_b200.engine import DeviceCampaign
+    dc = DeviceCampaign(workload_manifest("matmul"), master_seed=1)
+    nb = dc.L.sfg_program_jit_source(dc.h, None, 0)
+    buf = ctypes.create_string_buffer(nb + 1)
+    dc.L.sfg_program_jit_source(dc.h, buf, nb + 1)
+    src = buf.value.decode()
+    assert "#define SFG_RO_ARGS 3u" in src and "#define SFG_WO_ARGS 4u" in src
+    dc.close()
