@@ -199,6 +199,9 @@ struct Gen {
       const std::string trk = (ro || wo) ? std::string() :
           "if (PAR && par_track(J.tags, J.ntags, pw" + Q + " + (lo_ - pb" + Q + "), " + W_s + ", " +
           (st ? "true" : "false") + ", J.me, J.waw)) { " + radj(slow, j) + "rc = RUN_CONFLICT; goto done; } ";
+      // a write-only store into memory dead after the launch is never read back
+      // unless diff readback copies the record out: only the sanitizer check matters
+      if (st && wo) return "if (P.diff_readback) *" + ptr + " = (" + T + ")sv_;";
       if (st) return trk + "*" + ptr + " = (" + T + ")sv_;";
       return trk + "v_ = *" + ptr + ";";
     };
