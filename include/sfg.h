@@ -138,6 +138,7 @@ int sfg_regen(const sfg_program* p, const sfg_corpus_dev* c, int n_sel, const in
  * the real budget (soft-cap list group-parallel, spread one input per warp;
  * then the sequential list).  Results are identical to soft_cap 0 and to
  * sequential execution (executor.py:405-424).
+ * n_live (with order): the schedule holds *n_live inputs (sfg_dedupe representatives).
  * c != NULL (the campaign's corpus as of the round start): the kernel builds every
  * input's arrays in its work region itself, from its parent's payload, before its
  * COMPUTE phase (sfg_apply fused into the execute pass); c == NULL: the work
@@ -146,7 +147,7 @@ int sfg_execute(const sfg_program* p, const sfg_corpus_dev* c, int n, const void
                 const uint64_t* work_base, uint8_t* work, void* verdicts, uint32_t* edge_counts,
                 uint8_t* readouts, const uint64_t* readout_base, int* work_counter,
                 uint64_t soft_cap, int32_t* deferred, int64_t max_work_bytes, const int32_t* order,
-                void* stream);
+                const int32_t* n_live, void* stream);
 int sfg_execute_deferred(const sfg_program* p, const sfg_corpus_dev* c, int n, const void* children,
                          const void* vals, const uint64_t* work_base, uint8_t* work, void* verdicts,
                          uint32_t* edge_counts, uint8_t* readouts, const uint64_t* readout_base,
@@ -179,7 +180,19 @@ uint32_t sfg_program_order_mask(const sfg_program* p);
 /* The same analysis on host tables, no device needed (tests, tooling). */
 uint32_t sfg_control_mask(const void* prog, size_t prog_bytes, const void* ins, const void* hostops,
                           size_t n_hostops, const void* binds);
-int sfg_order(const sfg_program* p, int n, const void* vals, int32_t* order, int32_t* scratch, void* stream);
+int sfg_order(const sfg_program* p, int n, const void* vals, int32_t* order, int32_t* scratch,
+              const int32_t* rep, int32_t* n_live, void* stream);
+/* Duplicate inputs (order.cu): rep[i] = the input whose execution stands for input i
+ * (itself, or an earlier-inserted input with equal argument descriptors, the same
+ * parent and the same data-level array op -- a COMPUTE phase is a pure function of
+ * them).  table: `slots` uint64 words (a power of two >= 2n), cleared here.  Pass
+ * rep to sfg_order (only representatives are scheduled, their count to *n_live) and
+ * n_live to sfg_execute; after sfg_execute_deferred, sfg_dup_fill copies each
+ * representative's verdict and edge-count row to its duplicates. */
+int sfg_dedupe(const sfg_program* p, int n, const void* children, const void* vals, uint64_t* table, int slots,
+               int32_t* rep, void* stream);
+int sfg_dup_fill(const sfg_program* p, int n, const int32_t* rep, void* verdicts, uint32_t* edge_counts,
+                 void* stream);
 /* Triage in three stream-ordered phases so that a multi-GPU campaign can merge
  * the per-rank partials between them: a rank owns the global
  * round indices [i_base, i_base + n).  All indices written are GLOBAL round

@@ -590,17 +590,43 @@ uint32_t sfg_control_mask(const void* prog, size_t prog_bytes, const void* ins, 
 
 size_t sfg_order_scratch_ints(int n) { return (size_t)kOrderBuckets + (size_t)(n > 0 ? n : 0); }
 
-int sfg_order(const sfg_program* p, int n, const void* vals, int32_t* order, int32_t* scratch, void* stream) {
+int sfg_order(const sfg_program* p, int n, const void* vals, int32_t* order, int32_t* scratch, const int32_t* rep,
+              int32_t* n_live, void* stream) {
   if (n <= 0) return 0;
   int* hist = scratch;
   int* sig = scratch + kOrderBuckets;
   cudaError_t e = cudaMemsetAsync(hist, 0, kOrderBuckets * sizeof(int), S(stream));
   if (e != cudaSuccess) return fail("sfg_order", e);
   sfg_order_hist_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(p->P, (const sfg_val*)vals, n, p->order_mask,
-                                                                  hist, sig);
-  sfg_order_scan_kernel<<<1, 128, 0, S(stream)>>>(hist);
-  sfg_order_scatter_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(n, sig, hist, order);
+                                                                  hist, sig, rep);
+  sfg_order_scan_kernel<<<1, 128, 0, S(stream)>>>(hist, n_live);
+  sfg_order_scatter_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(n, sig, hist, order, rep);
   SFG_CHECK_LAUNCH("sfg_order");
+  return 0;
+}
+
+int sfg_dedupe(const sfg_program* p, int n, const void* children, const void* vals, uint64_t* table, int slots,
+               int32_t* rep, void* stream) {
+  if (n <= 0) return 0;
+  if (slots < 2 * n || (slots & (slots - 1))) {
+    g_err = "sfg_dedupe: slots must be a power of two >= 2n";
+    return 1;
+  }
+  cudaError_t e = cudaMemsetAsync(table, 0, (size_t)slots * sizeof(uint64_t), S(stream));
+  if (e != cudaSuccess) return fail("sfg_dedupe", e);
+  sfg_dedupe_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(p->P, n, (const sfg_child*)children,
+                                                              (const sfg_val*)vals, (unsigned long long*)table, slots,
+                                                              rep);
+  SFG_CHECK_LAUNCH("sfg_dedupe");
+  return 0;
+}
+
+int sfg_dup_fill(const sfg_program* p, int n, const int32_t* rep, void* verdicts, uint32_t* edge_counts,
+                 void* stream) {
+  if (n <= 0) return 0;
+  sfg_dup_fill_kernel<<<blocks_for(n, 256), 256, 0, S(stream)>>>(n, p->P.n_edges, rep, (sfg_verdict*)verdicts,
+                                                                edge_counts);
+  SFG_CHECK_LAUNCH("sfg_dup_fill");
   return 0;
 }
 
@@ -608,7 +634,8 @@ int sfg_order(const sfg_program* p, int n, const void* vals, int32_t* order, int
 int sfg_execute(const sfg_program* p, const sfg_corpus_dev* c, int n, const void* children, const void* vals,
                 const uint64_t* work_base, uint8_t* work, void* verdicts, uint32_t* edge_counts, uint8_t* readouts,
                 const uint64_t* readout_base, int* work_counter, uint64_t soft_cap,
-                int32_t* deferred, int64_t max_work_bytes, const int32_t* order, void* stream) {
+                int32_t* deferred, int64_t max_work_bytes, const int32_t* order, const int32_t* n_live,
+                void* stream) {
   if (n <= 0) {
     if (work_counter) cudaMemsetAsync(work_counter, 0, 8 * sizeof(int), S(stream));
     return 0;
@@ -618,7 +645,12 @@ int sfg_execute(const sfg_program* p, const sfg_corpus_dev* c, int n, const void
              (sfg_verdict*)verdicts, edge_counts, readouts, readout_base, n,
              0ull, deferred, work_counter ? work_counter + 1 : nullptr,
              deferred ? deferred + n : nullptr, work_counter ? work_counter + 3 : nullptr, 1, 0, order,
-             nullptr, 0, nullptr, c ? (const sfg_val*)c->vals : nullptr, c ? (const uint8_t*)c->data : nullptr};
+             nullptr, 0, nullptr, c ? (const sfg_val*)c->vals : nullptr, c ? (const uint8_t*)c->data : nullptr,
+             order ? n_live : nullptr};
+  if (n_live && !order) {
+    g_err = "sfg_execute: n_live needs the schedule (order) it counts";
+    return 1;
+  }
   if (p->jit_kernel) {
     if (work_counter == nullptr || (deferred == nullptr && soft_cap != 0)) {
       g_err = "sfg_execute: the specialized kernel needs a per-launch work counter (and deferred lists for soft_cap)";

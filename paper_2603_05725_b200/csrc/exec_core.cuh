@@ -137,6 +137,9 @@ struct ExecView {
   // rule of sfg_apply (campaign.py:440-450); null: the work regions are already built
   const sfg_val* mat_vals;
   const uint8_t* mat_data;
+  // bulk pass: the schedule (order) holds *n_live inputs (duplicates left out,
+  // sfg_dedupe); null = all n
+  const int32_t* n_live;
 };
 
 namespace {

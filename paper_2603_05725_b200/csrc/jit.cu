@@ -1546,10 +1546,11 @@ struct Gen {
          "  R.soft_cap = E.soft_cap;\n"
          "  const int lane = threadIdx.x & 31;\n"
          "  const int G = E.group;\n"
+         "  const int NL = E.n_live ? *E.n_live : E.n;   // inputs in the schedule\n"
          "  if (G <= 1) {\n"
          "    const Grp g{1, 0, 1u << lane, nullptr, nullptr, 0};\n"
          "    if (mode == 0) {\n"
-         "      for (int i = atomicAdd(next, 1); i < E.n; i = atomicAdd(next, 1)) run_input<false>(P, E, i, R, g);\n"
+         "      for (int i = atomicAdd(next, 1); i < NL; i = atomicAdd(next, 1)) run_input<false>(P, E, E.order ? E.order[i] : i, R, g);\n"
          "      return;\n"
          "    }\n"
          "    __shared__ int s_done[32];\n"
@@ -1558,11 +1559,11 @@ struct Gen {
          "      int b = 0;\n"
          "      if (lane == 0) b = atomicAdd(next, 32);\n"
          "      b = __shfl_sync(0xffffffffu, b, 0);\n"
-         "      if (b >= E.n) break;\n"
+         "      if (b >= NL) break;\n"
          "      if (lane == 0) s_done[w] = 0;\n"
          "      __syncwarp();\n"
-         "      if (E.soft_cap) { R.done = &s_done[w]; R.batch_n = E.n - b < 32 ? E.n - b : 32; }\n"
-         "      if (b + lane < E.n) {\n"
+         "      if (E.soft_cap) { R.done = &s_done[w]; R.batch_n = NL - b < 32 ? NL - b : 32; }\n"
+         "      if (b + lane < NL) {\n"
          "        run_input<false>(P, E, E.order ? E.order[b + lane] : b + lane, R, g);\n"
          "        atomicAdd(&s_done[w], 1);\n"
          "      }\n"
@@ -1578,8 +1579,8 @@ struct Gen {
          "    int b = 0;\n"
          "    if (lane == 0) b = atomicAdd(next, per);\n"
          "    b = __shfl_sync(0xffffffffu, b, 0);\n"
-         "    if (b >= E.n) break;\n"
-         "    if (b + gi < E.n) run_input<true>(P, E, E.order ? E.order[b + gi] : b + gi, R, g);\n"
+         "    if (b >= NL) break;\n"
+         "    if (b + gi < NL) run_input<true>(P, E, E.order ? E.order[b + gi] : b + gi, R, g);\n"
          "    __syncwarp();\n"
          "  }\n"
          "}\n\n";

@@ -133,6 +133,9 @@ class Slot:
         self.counter = i32(8)            # work counters of this slot's execute launches
         self.deferred = i32(2 * cap)     # tail-pass lists: soft-cap deferrals, sequential re-runs
         self.order = i32(cap)            # bulk-pass schedule (sfg_order)
+        self.rep, self.n_live = i32(cap), i32(1)   # duplicate inputs' representatives (sfg_dedupe)
+        self.dup_slots = 1 << max(2 * cap - 1, 1).bit_length()
+        self.dup_table = None
         # sequential discipline: worker stream state before every input and after the last
         self.states = u8((cap + 1) * dc.state_bytes) if dc.sequential else None
         self.seq_par, self.seq_scratch, self.seq_words = False, None, 0
@@ -213,6 +216,8 @@ class DeviceCampaign:
         # K2 fused into the bulk pass (sfg_execute with the corpus); SFG_FUSE_APPLY=0:
         # a separate sfg_apply pass (A/B, tests)
         self.fuse_apply = os.environ.get("SFG_FUSE_APPLY", "1") != "0"
+        # duplicate inputs of a round executed once (sfg_dedupe); SFG_DEDUPE=0: all run
+        self.dedupe = os.environ.get("SFG_DEDUPE", "1") != "0"
         self.state_bytes = int(self.L.sfg_stream_state_bytes())
         if self.sequential and (self.comm.world > 1 or fanout):
             raise LoweringError("the sequential discipline runs on one device without fan-out")
@@ -635,10 +640,21 @@ class DeviceCampaign:
         tail = self.jit and cd is not None
         soft = soft_cap if tail else 0
         order = None
+        # duplicate inputs run once (sfg_dedupe): campaign rounds on the scheduled
+        # bulk pass, not with diff readback (readouts are per input)
+        dedupe = tail and self.order_inputs and self.dedupe and not self.diff
+        if dedupe:
+            self.launches += 2
+            if S.dup_table is None:
+                S.dup_table = torch.zeros(S.dup_slots, dtype=torch.int64, device=self.dev)
+            _native.check(self.L.sfg_dedupe(self.h, n, S.children.data_ptr(), S.vals.data_ptr(),
+                                            S.dup_table.data_ptr(), S.dup_slots, S.rep.data_ptr(), st.cuda_stream),
+                          "dedupe")
         if tail and self.order_inputs:
             self.launches += 3
             _native.check(self.L.sfg_order(self.h, n, S.vals.data_ptr(), S.order.data_ptr(),
-                                           S.order_scratch.data_ptr(), st.cuda_stream), "order")
+                                           S.order_scratch.data_ptr(), S.rep.data_ptr() if dedupe else None,
+                                           S.n_live.data_ptr() if dedupe else None, st.cuda_stream), "order")
             order = S.order.data_ptr()
             self._mark(S, "ordered")
         # the bulk pass builds each input's arrays from its parent itself (sfg_apply
@@ -648,7 +664,7 @@ class DeviceCampaign:
             self.h, ctypes.byref(fuse) if fuse is not None else None, n, S.children.data_ptr(), S.vals.data_ptr(), S.work_base.data_ptr(), S.work.data_ptr(),
             S.verdicts.data_ptr(), S.ecnt.data_ptr(), _ptr(S.readouts), S.ro_base.data_ptr(),
             S.counter.data_ptr(), soft, S.deferred.data_ptr() if tail else None, self.max_entry_work, order,
-            st.cuda_stream), "execute")
+            S.n_live.data_ptr() if dedupe else None, st.cuda_stream), "execute")
         if tail:
             self._mark(S, "bulk")
             if self.timing:
@@ -666,6 +682,10 @@ class DeviceCampaign:
                 self.max_entry_work, ts.cuda_stream), "execute_deferred")
             if ts is not st:
                 st.wait_stream(ts)
+            if dedupe:
+                self.launches += 1
+                _native.check(self.L.sfg_dup_fill(self.h, n, S.rep.data_ptr(), S.verdicts.data_ptr(),
+                                                  S.ecnt.data_ptr(), st.cuda_stream), "dup_fill")
             self._mark(S, "tail")
         if self.timing:
             ev[1].record(st)

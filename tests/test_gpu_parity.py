@@ -3,6 +3,8 @@ vectors and the CPU oracle, bit-exact."""
 
 import hashlib
 
+import numpy as np
+
 import pytest
 
 from conftest import bench_manifest, bench_names, golden, trigger_ops
@@ -490,3 +492,32 @@ def _stream_states(raw):
     st["cache32"][st["has32"] == 0] = 0
     st["pad"] = 0
     return st
+
+
+@pytest.mark.parametrize("name", ["matmul", "structcfg", "dot", "rotm"])
+def test_duplicate_inputs_run_once(engine_cls, name, monkeypatch):
+    """sfg_dedupe: children with the same parent and the same set of ops run once
+    and their duplicates take the verdict and edge row; every per-input record of
+    a batched campaign equals the one where every input runs (SFG_DEDUPE=0), and
+    a large share of a round are duplicates."""
+    from conftest import workload_manifest
+    m = bench_manifest(name) if name in bench_names() else workload_manifest(name)
+    runs = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SFG_DEDUPE", flag)
+        dc = engine_cls(m, master_seed=5)
+        got = []
+        dc.run_rounds(1, 1 + 3 * 65536, 65536, depth=3, on_round=lambda res: got.extend(dc.round_records(res)))
+        if flag == "1":
+            S = dc.slots[0]
+            rep = S.rep[:S.n].cpu().numpy()
+            runs["dups"] = int((rep != np.arange(S.n)).sum())
+        runs[flag] = (got, dc.findings.render_text(), report_to_rec(build_report(dc.coverage_map())))
+        dc.close()
+    a, b = runs["1"], runs["0"]
+    assert a[1] == b[1] and a[2] == b[2] and len(a[0]) == len(b[0])
+    for x, y in zip(a[0], b[0]):
+        assert _digest(x["child"]) == _digest(y["child"])
+        assert (x["status"], x["report"], x["retired"], x["allocs"], x["edges"], x["admitted"]) == \
+               (y["status"], y["report"], y["retired"], y["allocs"], y["edges"], y["admitted"]), x["it"]
+    assert runs["dups"] > 1000
