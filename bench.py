@@ -428,6 +428,8 @@ def run_ours(a):
     e2e = run_e2e(a, m, torch, R, world)
     if world == 1 and not a.no_sequential:
         e2e["sequential_discipline"] = run_e2e_sequential(a, m, torch)
+    if world == 1:
+        e2e["dedupe_inputs"] = run_e2e_dedupe(a, m, torch, R)
     if world == 1 and not a.no_cold:
         e2e["cold"] = run_e2e_cold(a, R, cache=True)
         e2e["cold_no_jit_cache"] = run_e2e_cold(a, R, cache=False)
@@ -584,6 +586,25 @@ def stage_profile(dc, it, R, a, peaks, torch):
     for k in out:
         k["share"] = k["ms_per_round"] / total if total else None
     return out
+
+
+def run_e2e_dedupe(a, m, torch, R):
+    """Informational, not the headline: the same campaign with the opt-in
+    CampaignConfig(dedupe_inputs=True) -- children of a round with the same parent
+    and the same set of ops run once and share the verdict (identical results, fewer
+    executions than inputs)."""
+    from paper_2603_05725_b200.campaign import CampaignConfig, fuzz_loop
+    steps = max(4 * a.steps, 96)
+    cfg = CampaignConfig(master_seed=11, iterations=steps * R, round_size=R, pipeline_depth=a.depth,
+                         dedupe_inputs=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s = fuzz_loop(m, cfg)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    return {"value": s.compute_runs / wall, "unit": UNIT, "wall_s": wall, "execs": s.compute_runs,
+            "note": "opt-in dedupe_inputs=True: duplicate children share one execution (not the headline)",
+            "api": "campaign.fuzz_loop(manifest, CampaignConfig(dedupe_inputs=True))"}
 
 
 def run_e2e_sequential(a, m, torch):

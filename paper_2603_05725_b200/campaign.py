@@ -94,6 +94,10 @@ class CampaignConfig:
     extra_seeds: tuple = ()
     fanout: int = 0
     soft_cap: int | None = None
+    # opt-in: children of a round with the same parent and the same set of ops run
+    # once and share the verdict (results identical; fewer executions than inputs --
+    # off by default, and off in the bench's headline figures)
+    dedupe_inputs: bool = False
 
 
 @dataclass
@@ -158,7 +162,7 @@ def _device_campaign(manifest, config: CampaignConfig, comm) -> DeviceCampaign:
                           ids_reset_per_input=config.mode == "reinit",
                           sequential=config.discipline == "sequential", ctx_map_bits=config.ctx_map_bits,
                           extra_seeds=tuple(as_testcase(t) for t in config.extra_seeds), fanout=config.fanout,
-                          soft_cap=config.soft_cap)
+                          soft_cap=config.soft_cap, dedupe=config.dedupe_inputs)
 
 
 def fuzz_loop(manifest, config: CampaignConfig) -> CampaignSummary:

@@ -199,6 +199,7 @@ class DeviceCampaign:
                  diff_readback=False, stop_on_first_finding=False, stop_bug_class=None, device=None,
                  extra_seeds=(), ids_reset_per_input=False, comm: RoundComm | None = None,
                  soft_cap: int | None = None, ctx_map_bits: int = 0, fanout: int = 0, sequential: bool = False,
+                 dedupe: bool = False,
                  baseline=None, jit: bool = True, term_phase: bool = False):
         if not torch.cuda.is_available():
             raise _native.NativeError("no CUDA device: the fuzzing inner loop runs only on the GPU")
@@ -216,8 +217,9 @@ class DeviceCampaign:
         # K2 fused into the bulk pass (sfg_execute with the corpus); SFG_FUSE_APPLY=0:
         # a separate sfg_apply pass (A/B, tests)
         self.fuse_apply = os.environ.get("SFG_FUSE_APPLY", "1") != "0"
-        # duplicate inputs of a round executed once (sfg_dedupe); SFG_DEDUPE=0: all run
-        self.dedupe = os.environ.get("SFG_DEDUPE", "1") != "0"
+        # opt-in: duplicate inputs of a round executed once (sfg_dedupe; SFG_DEDUPE=1/0
+        # overrides for A/B).  Off by default: every input runs.
+        self.dedupe = bool(dedupe) if "SFG_DEDUPE" not in os.environ else os.environ["SFG_DEDUPE"] == "1"
         self.state_bytes = int(self.L.sfg_stream_state_bytes())
         if self.sequential and (self.comm.world > 1 or fanout):
             raise LoweringError("the sequential discipline runs on one device without fan-out")
