@@ -193,6 +193,14 @@ int sfg_dedupe(const sfg_program* p, int n, const void* children, const void* va
                int32_t* rep, void* stream);
 int sfg_dup_fill(const sfg_program* p, int n, const int32_t* rep, void* verdicts, uint32_t* edge_counts,
                  void* stream);
+/* Grouped schedule (every input runs): full[0..n) = the representatives in `order`
+ * (the first *n_live entries, sfg_order with rep), each directly followed by its
+ * duplicates, so a warp of the bulk pass takes runs of equal inputs.  scratch:
+ * sfg_group_scratch_ints(n) int32 of device memory.  Pass full as sfg_execute's
+ * order with n_live = NULL. */
+size_t sfg_group_scratch_ints(int n);
+int sfg_group_schedule(const sfg_program* p, int n, const int32_t* rep, const int32_t* order, const int32_t* n_live,
+                       int32_t* full, int32_t* scratch, void* stream);
 /* Triage in three stream-ordered phases so that a multi-GPU campaign can merge
  * the per-rank partials between them: a rank owns the global
  * round indices [i_base, i_base + n).  All indices written are GLOBAL round

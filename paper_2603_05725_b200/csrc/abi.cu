@@ -621,6 +621,34 @@ int sfg_dedupe(const sfg_program* p, int n, const void* children, const void* va
   return 0;
 }
 
+int sfg_group_schedule(const sfg_program* p, int n, const int32_t* rep, const int32_t* order, const int32_t* n_live,
+                       int32_t* full, int32_t* scratch, void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t st = S(stream);
+  int32_t* cnt = scratch;               // n
+  int32_t* fill = scratch + n;          // n
+  int32_t* rpos = scratch + 2 * (int64_t)n;
+  int64_t* w = (int64_t*)(scratch + (3 * (int64_t)n + 1) / 2 * 2);      // n int64 (8-aligned)
+  int64_t* start = w + n;               // n int64
+  int64_t* tmp = start + n;             // scan tiles
+  cudaError_t e = cudaMemsetAsync(cnt, 0, 2 * (size_t)n * sizeof(int32_t), st);
+  if (e != cudaSuccess) return fail("sfg_group_schedule", e);
+  sfg_dup_count_kernel<<<blocks_for(n, 256), 256, 0, st>>>(n, rep, cnt);
+  sfg_group_weights_kernel<<<blocks_for(n, 256), 256, 0, st>>>(n, order, n_live, cnt, w);
+  const int rc = sfg_scan_u64((const uint64_t*)w, n, 1, 0, (uint64_t*)start, 1, 0, (uint64_t*)tmp,
+                              (uint64_t*)(tmp + ((n + 2047) / 2048 + 8)), st);
+  if (rc) return rc;
+  sfg_group_place_kernel<<<blocks_for(n, 256), 256, 0, st>>>(n, order, n_live, start, full, rpos);
+  sfg_group_dups_kernel<<<blocks_for(n, 256), 256, 0, st>>>(n, rep, rpos, fill, full);
+  SFG_CHECK_LAUNCH("sfg_group_schedule");
+  return 0;
+}
+
+size_t sfg_group_scratch_ints(int n) {
+  const size_t m = (size_t)(n > 0 ? n : 0);
+  return 3 * m + 2 + 4 * m + 2 * ((m + 2047) / 2048 + 16);
+}
+
 int sfg_dup_fill(const sfg_program* p, int n, const int32_t* rep, void* verdicts, uint32_t* edge_counts,
                  void* stream) {
   if (n <= 0) return 0;

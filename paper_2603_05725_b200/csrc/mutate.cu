@@ -276,12 +276,12 @@ template <bool EMIT = true, class Strm>
 __device__ __forceinline__ void mutate_child(const sfg_prog& P, const CorpusView& C, int64_t it, Strm& s,
                                              const uint64_t* cnt_of, const uint64_t* cnt_pre, int8_t* picks,
                                              sfg_child& ch,
-                                             sfg_val* vout) {
+                                             sfg_val* __restrict__ vout) {
   if (EMIT) {
     memset(&ch, 0, sizeof(ch));
     ch.it = it;
   }
-  const sfg_val* pv = C.vals;             // parent values (the seed for it == 1)
+  const sfg_val* __restrict__ pv = C.vals;   // parent values (the seed for it == 1)
   // picked args: the mutated value goes straight to vout; its kind / materialized
   // size / nbytes stay in registers for the layout pass
   int ma[SFG_MAX_OPS] = {-1, -1, -1};

@@ -203,3 +203,41 @@ extern "C" __global__ void sfg_dup_fill_kernel(int n, int n_edges, const int32_t
   for (int e = 0; e < n_edges; ++e) edge_counts[(size_t)i * n_edges + e] = edge_counts[(size_t)r * n_edges + e];
 }
 
+// ---------------------------------------------------------------------------
+// Grouped schedule: every input runs, each representative (sfg_dedupe) directly
+// followed by its duplicates, representatives in sfg_order's signature order.  A
+// warp of the bulk pass then takes runs of equal inputs: lanes that follow the same
+// path through the simulated kernel on the same parent bytes issue together.
+// cnt / fill: zeroed int32[n]; w: int64[n] (w[j] = 1 + duplicates of the j-th
+// scheduled representative, 0 past n_live), scanned into start by the caller.
+extern "C" __global__ void sfg_dup_count_kernel(int n, const int32_t* rep, int32_t* cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool dup = i < n && rep[i] != i;
+  warp_agg_add(cnt, dup ? rep[i] : 0, dup);
+}
+
+extern "C" __global__ void sfg_group_weights_kernel(int n, const int32_t* order, const int32_t* n_live,
+                                                    const int32_t* cnt, int64_t* w) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  w[j] = j < *n_live ? 1 + (int64_t)cnt[order[j]] : 0;
+}
+
+extern "C" __global__ void sfg_group_place_kernel(int n, const int32_t* order, const int32_t* n_live,
+                                                  const int64_t* start, int32_t* full, int32_t* rpos) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n || j >= *n_live) return;
+  const int r = order[j];
+  full[start[j]] = r;
+  rpos[r] = (int32_t)start[j];
+}
+
+extern "C" __global__ void sfg_group_dups_kernel(int n, const int32_t* rep, const int32_t* rpos, int32_t* fill,
+                                                 int32_t* full) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool dup = i < n && rep[i] != i;
+  const int r = dup ? rep[i] : 0;
+  const int k = warp_agg_add(fill, r, dup);
+  if (dup) full[rpos[r] + 1 + k] = i;
+}
+

@@ -136,6 +136,7 @@ class Slot:
         self.rep, self.n_live = i32(cap), i32(1)   # duplicate inputs' representatives (sfg_dedupe)
         self.dup_slots = 1 << max(2 * cap - 1, 1).bit_length()
         self.dup_table = None
+        self.group_scratch = self.full_order = None   # grouped schedule (sfg_group_schedule)
         # sequential discipline: worker stream state before every input and after the last
         self.states = u8((cap + 1) * dc.state_bytes) if dc.sequential else None
         self.seq_par, self.seq_scratch, self.seq_words = False, None, 0
@@ -220,6 +221,8 @@ class DeviceCampaign:
         # opt-in: duplicate inputs of a round executed once (sfg_dedupe; SFG_DEDUPE=1/0
         # overrides for A/B).  Off by default: every input runs.
         self.dedupe = bool(dedupe) if "SFG_DEDUPE" not in os.environ else os.environ["SFG_DEDUPE"] == "1"
+        # equal inputs scheduled side by side in the bulk pass (all of them run); SFG_GROUP_DUPS=0: off
+        self.group_dups = os.environ.get("SFG_GROUP_DUPS", "1") != "0"
         self.state_bytes = int(self.L.sfg_stream_state_bytes())
         if self.sequential and (self.comm.world > 1 or fanout):
             raise LoweringError("the sequential discipline runs on one device without fan-out")
@@ -645,7 +648,9 @@ class DeviceCampaign:
         # duplicate inputs run once (sfg_dedupe): campaign rounds on the scheduled
         # bulk pass, not with diff readback (readouts are per input)
         dedupe = tail and self.order_inputs and self.dedupe and not self.diff
-        if dedupe:
+        # every input runs, equal inputs side by side in the schedule (sfg_group_schedule)
+        group = tail and self.order_inputs and self.group_dups and not dedupe
+        if dedupe or group:
             self.launches += 2
             if S.dup_table is None:
                 S.dup_table = torch.zeros(S.dup_slots, dtype=torch.int64, device=self.dev)
@@ -655,9 +660,19 @@ class DeviceCampaign:
         if tail and self.order_inputs:
             self.launches += 3
             _native.check(self.L.sfg_order(self.h, n, S.vals.data_ptr(), S.order.data_ptr(),
-                                           S.order_scratch.data_ptr(), S.rep.data_ptr() if dedupe else None,
-                                           S.n_live.data_ptr() if dedupe else None, st.cuda_stream), "order")
+                                           S.order_scratch.data_ptr(), S.rep.data_ptr() if (dedupe or group) else None,
+                                           S.n_live.data_ptr() if (dedupe or group) else None, st.cuda_stream), "order")
             order = S.order.data_ptr()
+            if group:
+                self.launches += 7
+                if S.group_scratch is None:
+                    S.group_scratch = torch.empty(int(self.L.sfg_group_scratch_ints(S.cap)), dtype=torch.int32,
+                                                  device=self.dev)
+                    S.full_order = torch.empty(S.cap, dtype=torch.int32, device=self.dev)
+                _native.check(self.L.sfg_group_schedule(self.h, n, S.rep.data_ptr(), S.order.data_ptr(),
+                                                        S.n_live.data_ptr(), S.full_order.data_ptr(),
+                                                        S.group_scratch.data_ptr(), st.cuda_stream), "group")
+                order = S.full_order.data_ptr()
             self._mark(S, "ordered")
         # the bulk pass builds each input's arrays from its parent itself (sfg_apply
         # fused) when the round has a corpus and nothing was materialized before
