@@ -431,6 +431,10 @@ def run_ours(a):
     if world == 1:
         e2e["dedupe_inputs"] = run_e2e_dedupe(a, m, torch, R)
     if world == 1 and not a.no_cold:
+        # the child process needs the device memory this process's caching allocator holds
+        gc.collect()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
         e2e["cold"] = run_e2e_cold(a, R, cache=True)
         e2e["cold_no_jit_cache"] = run_e2e_cold(a, R, cache=False)
 
