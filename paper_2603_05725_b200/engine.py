@@ -135,8 +135,11 @@ class Slot:
         self.order = i32(cap)            # bulk-pass schedule (sfg_order)
         self.rep, self.n_live = i32(cap), i32(1)   # duplicate inputs' representatives (sfg_dedupe)
         self.dup_slots = 1 << max(2 * cap - 1, 1).bit_length()
-        self.dup_table = None
-        self.group_scratch = self.full_order = None   # grouped schedule (sfg_group_schedule)
+        # allocated with the slot, never mid-pipeline (a cudaMalloc there stalls the device)
+        self.dup_table = torch.zeros(self.dup_slots, dtype=torch.int64, device=dev) \
+            if (dc.dedupe or dc.group_dups) else None
+        self.group_scratch = i32(int(dc.L.sfg_group_scratch_ints(cap))) if dc.group_dups else None
+        self.full_order = i32(cap) if dc.group_dups else None   # grouped schedule (sfg_group_schedule)
         # sequential discipline: worker stream state before every input and after the last
         self.states = u8((cap + 1) * dc.state_bytes) if dc.sequential else None
         self.seq_par, self.seq_scratch, self.seq_words = False, None, 0
@@ -652,7 +655,7 @@ class DeviceCampaign:
         group = tail and self.order_inputs and self.group_dups and not dedupe
         if dedupe or group:
             self.launches += 2
-            if S.dup_table is None:
+            if S.dup_table is None:   # the mode was switched on after the slot was made
                 S.dup_table = torch.zeros(S.dup_slots, dtype=torch.int64, device=self.dev)
             _native.check(self.L.sfg_dedupe(self.h, n, S.children.data_ptr(), S.vals.data_ptr(),
                                             S.dup_table.data_ptr(), S.dup_slots, S.rep.data_ptr(), st.cuda_stream),
