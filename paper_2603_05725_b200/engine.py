@@ -315,7 +315,7 @@ class DeviceCampaign:
         self._last_done = None           # event: previous round finalized
         self._last_counts = None         # event: counts_run valid for the next submission
         self.rounds = 0
-        self.spec_depth = 2              # adaptive speculation depth (run_rounds)
+        self.spec_depth = int(os.environ.get("SFG_SPEC0", "2"))   # adaptive speculation depth (run_rounds)
         self.launches = 0                # kernels launched through the C ABI (bench evidence)
         self.ov_grows = 0                # copy-on-write overlay enlargements (rounds re-run)
         self.timing = False              # record CUDA events around each execute kernel
