@@ -86,12 +86,22 @@ def _check_rounds(dc, rounds_ref, block, depth):
         assert [r["it"] for r in got["recs"] if r["admitted"]] == want["admitted"]
 
 
-def test_c2_bench_configuration_matches_reference(cuda_ok):
+@pytest.mark.parametrize("mode", ["default", "lowcap", "plain"])
+def test_c2_bench_configuration_matches_reference(cuda_ok, mode, monkeypatch):
+    """default: bench.py's own setup.  lowcap: a 2,048-instruction soft cap sends
+    every longer input through the group-parallel long-input pass (nest summaries
+    under conflict tags).  plain: no nest summaries and no equal-input schedule."""
     from paper_2603_05725_b200.engine import DeviceCampaign
     ref = _gz("ref_bench_c2.json.gz")
     cfg = ref["config"]
     assert cfg["round_size"] == 1 << 20      # bench.py's default --round
-    dc = DeviceCampaign(workload_manifest("matmul"), master_seed=cfg["master_seed"])   # bench.py's defaults
+    kw = {}
+    if mode == "lowcap":
+        kw["soft_cap"] = 2048
+    if mode == "plain":
+        monkeypatch.setenv("SFG_NESTSUM", "0")
+        monkeypatch.setenv("SFG_GROUP_DUPS", "0")
+    dc = DeviceCampaign(workload_manifest("matmul"), master_seed=cfg["master_seed"], **kw)   # bench.py's defaults
     _check_rounds(dc, ref["rounds"], ref["block"], depth=24)
     dc.close()
 
