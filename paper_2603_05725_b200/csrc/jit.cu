@@ -1460,6 +1460,7 @@ struct Gen {
 
   bool loop_summaries = true;
   bool nest_summaries = true;
+  uint64_t strag_min = 8192;   // bulk pass: retired count past which the batch's last lane is deferred
   int n_summaries = 0, n_nests = 0;
   int tail_minb = 12;
   int bulk_minb = 4;
@@ -1496,7 +1497,7 @@ struct Gen {
          "    default: t = a <= 0 ? 0 : (b < 0 ? (a + (-b) - 1) / (-b) : SFG_I64MAX); break;\n"
          "  }\n"
          "  return t <= H ? t : SFG_I64MAX;\n}\n";
-    o << "constexpr uint32_t kStrag = 2048u;\nconstexpr uint64_t kStragMin = 8192ull;\n\n";
+    o << "constexpr uint32_t kStrag = 2048u;\nconstexpr uint64_t kStragMin = " << strag_min << "ull;\n\n";
     o << "struct JitRunner {\n  uint32_t ec[" << NE << "], ecs[" << NE
       << "];\n  bool ovf, ovfs;\n  uint64_t soft_cap;\n"
       << "  uint32_t* tags = nullptr;\n  int ntags = 0, t = 0;\n  uint32_t me = 0;\n  GroupSmem* gs = nullptr;\n  int* waw = nullptr;\n"
@@ -1695,6 +1696,7 @@ static int sfg_jit_compile(const sfg_prog& P, const sfg_ins* ins, uint64_t max_e
   g.binds = binds;
   if (const char* ls = getenv("SFG_LOOPSUM")) g.loop_summaries = atoi(ls) != 0;
   if (const char* ns = getenv("SFG_NESTSUM")) g.nest_summaries = atoi(ns) != 0;
+  if (const char* sm = getenv("SFG_STRAG_MIN")) g.strag_min = strtoull(sm, nullptr, 10) ? strtoull(sm, nullptr, 10) : 8192;
   if (const char* tb = getenv("SFG_TAIL_MINB")) g.tail_minb = atoi(tb) >= 1 ? atoi(tb) : 12;
   if (const char* bb = getenv("SFG_BULK_MINB")) g.bulk_minb = atoi(bb) >= 1 ? atoi(bb) : 4;
   source = g.run(P.n_edges, max_edge_events);
