@@ -367,9 +367,17 @@ def run_ours(a):
     retired = dc.retired_mean(results[-1].slot)
     collectives = comm.calls
     prof = {}
-    pf = REPO / "profiles" / "r01_ncu_bulk_execute.json"
-    if pf.exists():
-        prof = json.loads(pf.read_text())
+    # ncu figures of the same kernels (tools/ncu_kernels.py on the latest capture)
+    nk = REPO / "profiles" / "r02_ncu_kernels.json"
+    ncu_k = json.loads(nk.read_text()) if nk.exists() else {}
+    bulk_n = next((v for k, v in ncu_k.items() if "bulk" in k), None)
+    tail_n = next((v for k, v in ncu_k.items() if "tail" in k), None)
+    if bulk_n:
+        b = bulk_n["ncu"]
+        prof = {"dram_bytes_per_launch": bulk_n.get("traffic"), "source": bulk_n.get("traffic_source"),
+                "issue_slots_busy_pct": b.get("issue_slots_busy_pct"),
+                "active_threads_per_warp": b.get("active_threads_per_warp"),
+                "warp_cycles_per_issued": None}
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
             "traffic": prof.get("dram_bytes_per_launch"), "kernel": "sfg_jit_execute (K3 bulk pass)",
             "bytes_per_exec": bytes_exec, "launch_ms": statistics.mean(bulk_ms),
@@ -386,8 +394,12 @@ def run_ours(a):
              "lane_instr_peak_per_s": 148 * 4 * 32 * sm_mhz * 1e6}
     # the long-input pass (sfg_jit_tail): most of the serialized kernel time, few SMs
     # at a time; same issue/latency bound (ncu figures of one launch run alone)
-    tf = REPO / "profiles" / "r01_ncu_tail_execute.json"
-    tprof = json.loads(tf.read_text()) if tf.exists() else {}
+    tprof = {}
+    if tail_n:
+        t_ = tail_n["ncu"]
+        tprof = {"duration_ns": t_.get("duration_ns"), "issue_slots_busy_pct": t_.get("issue_slots_busy_pct"),
+                 "achieved_warps_per_sm": t_.get("achieved_warps_per_sm"), "dram_bytes_per_launch": tail_n.get("traffic"),
+                 "warp_cycles_per_issued": None}
     issue["tail_pass"] = {"kernel": "sfg_jit_tail", "ms_per_round_after_bulk": statistics.mean(
         e - b for e, b in zip(k3_ms, bulk_ms)) if bulk_ms else None,
         "ncu_duration_ms_alone": (tprof.get("duration_ns") or 0) / 1e6 or None,
