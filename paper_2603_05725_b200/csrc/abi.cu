@@ -335,7 +335,11 @@ int sfg_program_create(const void* prog, size_t prog_bytes, const void* ins, siz
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (const char* b = getenv("SFG_EXEC_BLOCK")) p->jit_block = atoi(b) >= 32 ? atoi(b) : 128;
+    // CTA size of the bulk pass: a multiple of 32 within the kernel's launch bounds (128)
+    if (const char* b = getenv("SFG_EXEC_BLOCK")) {
+      const int v = atoi(b);
+      p->jit_block = (v >= 32 && v <= 128 && v % 32 == 0) ? v : 128;
+    }
     if (const char* md = getenv("SFG_EXEC_MODE")) p->jit_mode = atoi(md);
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)p->jit_kernel, p->jit_block, 0);
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
