@@ -594,6 +594,10 @@ def stage_profile(dc, it, R, a, peaks, torch):
         gbs = bpe * R / (t / 1000.0) / 1e9 if t > 0 else 0.0
         k = {"kernel": label, "ms_per_round": t, "bytes_per_exec": bpe, "bytes_note": what,
              "achieved_gbs": gbs, "hbm_frac": gbs / hbm, "rounds": len(ms)}
+        if "bulk" in label:
+            k["note"] = ("issue / latency bound: each lane runs its input's simulated threads' dependent chains "
+                         "(issue_roofline); DRAM traffic above the algorithmic bytes is the 64-B argument "
+                         "descriptors read (9 x 64 B per input on C2) and the lane's allocator tables in local memory")
         n = ncu.get(label)
         if n:
             k.update(n)
