@@ -592,7 +592,7 @@ class DeviceCampaign:
         # planner cuts there); otherwise one thread walks the stream
         S.seq_par = it0 >= 2 and self._counts_sat and n >= SEQ_PAR_MIN and not self.seq_single
         if S.seq_par:
-            words = int(self._seq_mu * n * 1.25) + 256
+            words = int(self._seq_mu * n * 1.06) + 512   # a truncation costs a round cut, not correctness
             need = int(L.sfg_seq_scratch_ints(n, words))
             # one scratch for the campaign: generations are chained in submission
             # order (each waits for the last one submitted, dropped rounds included)
